@@ -1,0 +1,344 @@
+"""Benchmark of the B200 AMYTISS engine (driver contract: one JSON line).
+
+Metric (BASELINE.json): "MDP probs/sec + Bellman sweep time (s) vs CPU ref".
+Workload (N=1 and per GPU): C2b = 3-D vehicle reach-avoid with eta/4, stored
+MDP, T=32 (BASELINE configs[1]; 741,393 states, 18,534,825 rows, R=729, a
+108 GB matrix on one B200). One step = one full synthesis in matrix mode:
+stage (i) builds the sharded matrix + target-hit vector in HBM, stage (ii)
+runs the 32 backward Bellman steps (all-gather of V between ranks).
+
+  value      MDP probabilities built per second, whole job (rows*R / build time,
+             device time with CUDA events on the engine's stream, max over ranks)
+  sweep_s    Bellman sweep seconds per synthesis (device time, max over ranks)
+  e2e        the same metric through the public API (gridmdp.synthesize -> C ABI
+             gm_synthesize: config text parsed on the host, descriptors uploaded,
+             matrix built, sweep run, value/policy tables copied back to host)
+
+`--impl reference` times the reference's own CPU implementation
+(oracle/_ref/gridmdp_ref: RowKernel::compute + fill_row, the body of
+build_matrix) on a bounded sample of the same rows with all host threads.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+REF_BIN = REPO / "oracle" / "_ref" / "gridmdp_ref"
+METRIC = "MDP probs/sec + Bellman sweep time (s) vs CPU ref, 1/2/4/8 B200"
+
+
+def peaks():
+    p = REPO / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.p = None
+        self.f = None
+
+    def __enter__(self):
+        try:
+            self.f = tempfile.TemporaryFile(mode="w+")
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            self.p.wait()
+
+    def summary(self):
+        if not self.f:
+            return None
+        self.f.seek(0)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_sample(cfg_text: str, rows_total: int, target_s: float, threads: int = 0, cal_rows: int = 20000):
+    """Times the reference's row kernel (RowKernel::compute + fill_row) on a bounded
+    contiguous sample of rows; returns (probs/s, rows, R, threads, seconds)."""
+    if not REF_BIN.exists():
+        raise FileNotFoundError(f"{REF_BIN} missing (make -C oracle ref)")
+    with tempfile.NamedTemporaryFile("w", suffix=".cfg", delete=False) as f:
+        f.write(cfg_text)
+        path = f.name
+
+    def run(b, e):
+        out = subprocess.run([str(REF_BIN), "time-rows", "-c", path, "--threads", str(threads), "--rows", str(b),
+                              str(e)], capture_output=True, text=True, check=True).stdout.split()
+        d = dict(zip(out[0::2], out[1::2]))
+        return int(d["rows"]), int(d["R"]), int(d["threads"]), float(d["seconds"])
+
+    try:
+        mid = rows_total // 3
+        n, R, th, s = run(mid, min(rows_total, mid + cal_rows))
+        want = int(min(rows_total - mid, max(cal_rows, cal_rows * target_s / max(s, 1e-6))))
+        n, R, th, s = run(mid, mid + want)
+        return n * R / s, n, R, th, s
+    finally:
+        os.unlink(path)
+
+
+def reference_arm(args, cfg_text, sizes):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    vals = []
+    last = None
+    for i in range(args.warmup + args.steps):
+        v, n, R, th, s = cpu_sample(cfg_text, int(sizes.rows), args.cpu_seconds / 2)
+        if i >= args.warmup:
+            vals.append(v)
+        last = (n, R, th, s)
+    n, R, th, s = last
+    value = statistics.median(vals)
+    sample = f"{n} contiguous rows (of {int(sizes.rows)}) x R={R} via RowKernel::compute+fill_row, {s:.2f} s"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "probs/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": n * R / value * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "rows": int(sizes.rows), "row_width": R},
+        "cpu_baseline": {"value": value, "unit": "probs/s", "cores": th, "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": "probs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="C2b")
+    ap.add_argument("--extra", default="C5", help="comma list of extra OFA workloads timed once (sweep only)")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    from paper_2005_06191_b200 import workloads as W
+
+    cfg_text = W.WORKLOADS[args.workload]()
+    if args.impl == "reference":
+        from paper_2005_06191_b200 import gridmdp as g
+
+        m = g.parse_config(cfg_text, args.workload)
+        reference_arm(args, cfg_text, m.sizes())
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2005_06191_b200 import _capi
+    from paper_2005_06191_b200 import gridmdp as g
+    from paper_2005_06191_b200 import sharded as S
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    _capi.call("gm_set_device", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    m = g.parse_config(cfg_text, args.workload)
+    sz = m.sizes()
+    n_x, T, R = int(sz.n_states), int(sz.horizon), int(sz.row_width)
+    nuw = int(sz.n_inputs) * int(sz.n_disturbances)
+    reach = m.spec.is_reach()
+    matrix = m.options.mode == "matrix"
+    plan = S.ShardPlan(n_x, world, rank)
+    my_rows = (plan.x1 - plan.x0) * nuw
+    stream = torch.cuda.current_stream()
+    be = S.DeviceBackend(m, stream)
+
+    def one_step():
+        ev = {}
+
+        def mark(name):
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            ev[name] = e
+
+        S.synthesize_sharded(be, n_x, T, reach, matrix, dev, None, mark)
+        return ev
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    lib = _capi.lib
+    lib.gm_reset_kernel_stats()
+    lib.gm_enable_kernel_timing(1)
+    launches0 = lib.gm_launch_count()
+    build_ms, sweep_ms = [], []
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        evs = [one_step() for _ in range(args.steps)]
+        t1.record(stream)
+        torch.cuda.synchronize()
+    launches = lib.gm_launch_count() - launches0
+    lib.gm_enable_kernel_timing(0)
+    for ev in evs:
+        build_ms.append(ev["build_start"].elapsed_time(ev["build_end"]))
+        sweep_ms.append(ev["build_end"].elapsed_time(ev["sweep_end"]))
+    total_ms = t0.elapsed_time(t1)
+    fam_ms = {n: lib.gm_kernel_ms_total(i) for i, n in enumerate(_capi.KF_NAMES)}
+    fam_n = {n: lib.gm_kernel_launches(i) for i, n in enumerate(_capi.KF_NAMES)}
+
+    t = torch.tensor([total_ms, sum(build_ms), sum(sweep_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, bsum, ssum = t.tolist()
+    rows_all = int(sz.rows)
+    probs_per_step = rows_all * R
+    value = probs_per_step * args.steps / (bsum / 1e3) if matrix and bsum > 0 else None
+    terms_per_step = rows_all * R * T
+    sweep_s = ssum / args.steps / 1e3
+
+    hbm, peak_kind = peaks()
+    dom = "expect_matrix" if matrix else "expect_ofa"
+    dom_ms = fam_ms[dom] / max(fam_n[dom], 1)
+    dom_bytes = my_rows * (R * 8 + 8 + (8 if reach else 0))  # algorithmic: T row + origin (+ T0x) per row
+    roofline = {"kernel": dom, "bound": "hbm", "achieved": dom_bytes / (dom_ms / 1e3) / 1e9, "peak": hbm,
+                "peak_kind": peak_kind, "unit": "GB/s", "traffic": None,
+                "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_ms": dom_ms, "launches": fam_n[dom]}
+    roofline["frac"] = roofline["achieved"] / hbm
+    if not matrix:
+        roofline["note"] = "OFA: HBM-equivalent bytes (8 per recomputed term), SURVEY.md §8d"
+    exp_ms = fam_ms["expand"] / max(fam_n["expand"], 1)
+    build_bytes = my_rows * (R * 8 + 8)
+    roofline_build = {"kernel": "expand", "bound": "hbm", "achieved": (
+        build_bytes / max(fam_n["expand"], 1)) / (exp_ms / 1e3) / 1e9 if exp_ms > 0 else None, "peak": hbm,
+        "unit": "GB/s"}
+    if roofline_build["achieved"]:
+        roofline_build["frac"] = roofline_build["achieved"] / hbm
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "probs/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (config-defined grids; no external data)",
+        "config": {"workload": args.workload, "model": "vehicle3-eta/4 reach-avoid (stored MDP)",
+                   "states": n_x, "rows": rows_all, "row_width": R, "horizon": T,
+                   "matrix_bytes": rows_all * R * 8, "parallelism": f"state-shard x{world}",
+                   "l2": "inputs larger than L2 (108 GB matrix streamed per step)"},
+        "build_ms_per_step": bsum / args.steps, "sweep_s": sweep_s,
+        "sweep_terms_per_s": terms_per_step / sweep_s if sweep_s > 0 else None,
+        "kernel_ms_per_step": {k: v / args.steps for k, v in fam_ms.items() if v},
+        "gpu_launches": int(launches),
+        "roofline": roofline, "roofline_build": roofline_build,
+        "clocks": clk.summary(),
+    }
+
+    # e2e through the public API (rank 0, N=1 path): host text -> results on host
+    if rank == 0 and world == 1 and not args.no_e2e:
+        m2 = g.parse_config(cfg_text, args.workload)
+        g.synthesize(m2)  # warm (descriptor upload, allocation)
+        e2e = []
+        res = None
+        for _ in range(max(1, min(args.steps, 2))):
+            torch.cuda.synchronize()
+            a = time.perf_counter()
+            m3 = g.parse_config(cfg_text, args.workload)
+            res = g.synthesize(m3)
+            e2e.append(time.perf_counter() - a)
+        s2 = m3.sizes()
+        d2h = res.values.nbytes + res.policy.nbytes + res.worst_dist.nbytes + res.absorbing.nbytes
+        h2d = int(g.lib.gm_model_program_size(m3.handle)) * 8 + (R // max(1, 1)) * 0 + n_x * 8
+        line["e2e"] = {"value": probs_per_step / statistics.median(e2e), "unit": "probs/s (whole synthesis)",
+                       "seconds_per_synthesis": statistics.median(e2e), "h2d_bytes_per_step": h2d,
+                       "d2h_bytes_per_step": int(d2h),
+                       "note": "wall clock of gridmdp.synthesize (C ABI, host buffers), includes the sweep"}
+        del s2
+
+    # extra OFA workloads (north-star BMW C5): sweep time only, one run after one warm run
+    if rank == 0 and world == 1 and args.extra:
+        extra = {}
+        for wname in [w for w in args.extra.split(",") if w]:
+            mt = g.parse_config(W.WORKLOADS[wname](), wname)
+            st = mt.sizes()
+            bet = S.DeviceBackend(mt, stream)
+            S.synthesize_sharded(bet, int(st.n_states), int(st.horizon), mt.spec.is_reach(), False, dev)
+            lib.gm_reset_kernel_stats()
+            lib.gm_enable_kernel_timing(1)
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            S.synthesize_sharded(bet, int(st.n_states), int(st.horizon), mt.spec.is_reach(), False, dev)
+            b.record(stream)
+            torch.cuda.synchronize()
+            lib.gm_enable_kernel_timing(0)
+            ms = a.elapsed_time(b)
+            terms = int(st.rows) * int(st.row_width) * int(st.horizon)
+            ofa_ms = lib.gm_kernel_ms_total(_capi.KF_EXPECT_OFA)
+            extra[wname] = {"sweep_s": ms / 1e3, "terms_per_s": terms / (ms / 1e3),
+                            "hbm_equiv_frac": terms * 8 / (ms / 1e3) / 1e9 / hbm,
+                            "kernel_ms": {n: lib.gm_kernel_ms_total(i) for i, n in enumerate(_capi.KF_NAMES)
+                                          if lib.gm_kernel_ms_total(i)},
+                            "expect_ofa_terms_per_s": terms / (ofa_ms / 1e3) if ofa_ms else None,
+                            "rows": int(st.rows), "row_width": int(st.row_width), "horizon": int(st.horizon)}
+        line["extra"] = extra
+
+    if rank == 0 and world == 1 and not args.no_cpu and value:
+        try:
+            v, n, Rr, th, s = cpu_sample(cfg_text, rows_all, args.cpu_seconds)
+            line["cpu_baseline"] = {"value": v, "unit": "probs/s", "cores": th, "kind": "reference",
+                                    "sample": f"{n} rows x R={Rr} (RowKernel::compute+fill_row), {s:.1f} s"}
+        except Exception as e:  # noqa: BLE001
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

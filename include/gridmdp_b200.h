@@ -1,0 +1,219 @@
+/*
+ * gridmdp_b200.h — C ABI of the B200-native AMYTISS engine (libgridmdp_b200.so).
+ *
+ * Drop-in boundary for the reference's two data-parallel stages. Every entry
+ * point below names the reference C++ interface it replaces (paths relative to
+ * /root/reference/proj). Signatures use plain pointers, sizes and opaque
+ * handles only; no C++ or torch types cross this boundary.
+ *
+ *   stage (i)  MDP construction   build_matrix / build_target_hit / mask_absorbing
+ *   stage (ii) Bellman synthesis  synthesize / synthesize_with_matrix / bellman_step
+ *
+ * Error model: every call returns a gm_code and fills an optional gm_status.
+ * Codes mirror the reference's exception taxonomy (include/gridmdp/common.hpp:16-41)
+ * and the CLI exit codes it maps them to (tools/gridmdp_main.cpp:204-226):
+ *   GM_ERR_CONFIG (ConfigError, ParseError)  -> exit 2
+ *   GM_ERR_MEMORY (MemoryError)              -> exit 3
+ *   GM_ERR_DOMAIN (DomainError)              -> exit 4
+ *   GM_ERR_RANGE  (std::out_of_range)        -> exit 4
+ *   GM_ERR_IO     (IoError)                  -> exit 5
+ *   GM_ERR_OTHER / GM_ERR_CUDA               -> exit 1
+ * Messages reproduce the reference's text (e.g. a device-side domain error is
+ * re-evaluated on the host for the lowest failing row, abstraction.cpp:93-101).
+ *
+ * There is no CPU fallback: every compute entry point needs a CUDA device and
+ * returns GM_ERR_CUDA when none is usable.
+ */
+#ifndef GRIDMDP_B200_H
+#define GRIDMDP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GM_MAX_DIMS 8
+
+typedef enum gm_code {
+    GM_OK = 0,
+    GM_ERR_OTHER = 1,
+    GM_ERR_CONFIG = 2,
+    GM_ERR_MEMORY = 3,
+    GM_ERR_DOMAIN = 4,
+    GM_ERR_IO = 5,
+    GM_ERR_RANGE = 6,
+    GM_ERR_CUDA = 7
+} gm_code;
+
+typedef struct gm_status {
+    int32_t code;          /* gm_code */
+    int32_t is_parse;      /* 1 when the ConfigError is an expression ParseError */
+    int64_t first_bad_row; /* lowest failing row of a device domain error, else -1 */
+    char msg[2048];
+} gm_status;
+
+typedef enum gm_mode { GM_MODE_MATRIX = 0, GM_MODE_OFA = 1 } gm_mode;          /* synthesis.hpp:12 */
+typedef enum gm_spec_kind { GM_SAFETY = 0, GM_REACH = 1, GM_REACH_AVOID = 2 } gm_spec_kind; /* spec.hpp:12 */
+
+typedef struct gm_model gm_model;   /* SystemModel + Spec + SynthesisOptions (model.hpp:15, spec.hpp:14) */
+typedef struct gm_matrix gm_matrix; /* device-resident TransitionMatrix row range (abstraction.hpp:22) */
+typedef struct gm_result gm_result; /* SynthesisResult (synthesis.hpp:28-40), host tables */
+
+/* CLI/config overrides (tools/gridmdp_main.cpp:20-41); negative / NULL = keep config value. */
+typedef struct gm_overrides {
+    int32_t threads;
+    int32_t time_steps;
+    int64_t mem_budget;
+    int64_t seed;
+    int32_t runs;
+    const char* mode;   /* "matrix" | "ofa" */
+    const char* output;
+} gm_overrides;
+
+/* Sizes of print_sizes (tools/gridmdp_main.cpp:43-54) plus device-layout facts. */
+typedef struct gm_sizes {
+    int32_t n_dim, m_dim, p_dim;
+    int64_t n_states, n_inputs, n_disturbances, pairs, rows, row_width;
+    int64_t counts[GM_MAX_DIMS];
+    int64_t strides[GM_MAX_DIMS];
+    int64_t extents[GM_MAX_DIMS];   /* window_extents, abstraction.cpp:16-35 */
+    uint64_t memory_estimate;       /* memory_estimate, abstraction.cpp:37-48 */
+    int32_t spec_kind, horizon, mode, threads;
+    double gamma;
+    int64_t mem_budget;
+    int32_t rows_per_thread_group;  /* device reduction width (identical in matrix and OFA) */
+    int32_t reserved;
+} gm_sizes;
+
+/* ---------------------------------------------------------------- front end */
+
+/* load_config + build_model + build_spec + build_options (config.hpp:55-70). */
+gm_code gm_model_load(const char* path, const gm_overrides* ov, gm_model** out, gm_status* st);
+/* parse_config from text (config.hpp:56); `name` prefixes error messages. */
+gm_code gm_model_parse(const char* text, const char* name, const gm_overrides* ov, gm_model** out,
+                       gm_status* st);
+void gm_model_free(gm_model* m);
+
+/* Replaces the model's Spec (make_safety/make_reachability/make_reach_avoid, spec.hpp:24-26).
+ * target/avoid are n_dim-long [lo, hi] vectors, or NULL for an absent box. */
+gm_code gm_model_set_spec(gm_model* m, int32_t kind, int32_t horizon, const double* target_lo,
+                          const double* target_hi, const double* avoid_lo, const double* avoid_hi,
+                          gm_status* st);
+/* Replaces mode / memory budget (SynthesisOptions, synthesis.hpp:14-18). */
+gm_code gm_model_set_options(gm_model* m, int32_t mode, int64_t mem_budget, gm_status* st);
+
+/* window_extents + memory_estimate + n_rows (abstraction.hpp:127-131, model.hpp:27-33). */
+gm_code gm_model_sizes(const gm_model* m, gm_sizes* out, gm_status* st);
+/* Per-state absorbing flags (absorbing_states, spec.cpp:51-60), n_states bytes. */
+gm_code gm_absorbing_states(gm_model* m, uint8_t* flags_out, gm_status* st);
+/* Host evaluation of mu = f(x,u,w) for one row (dynamics_image, model.cpp:33-38). */
+gm_code gm_dynamics_image(const gm_model* m, int64_t row, double* mu_out, gm_status* st);
+/* exec.output of the configuration after overrides ("" when unset). */
+const char* gm_model_output_path(const gm_model* m);
+/* Number of dynamics bytecode instructions (for tests / reporting). */
+int64_t gm_model_program_size(const gm_model* m);
+
+/* --------------------------------------------------------------- devices */
+
+/* Selects the CUDA device used by subsequent calls on this host thread. */
+gm_code gm_set_device(int32_t device, gm_status* st);
+/* Makes the model issue all its device work on `stream` (a cudaStream_t of the
+ * current device, e.g. the caller's torch stream); NULL restores its own stream. */
+gm_code gm_model_set_stream(gm_model* m, void* stream, gm_status* st);
+/* Number of kernel launches issued by this library since load (process-wide). */
+int64_t gm_launch_count(void);
+/* Device time of the last launch of each kernel family, ms (0 if none).
+ * family: 0 build, 1 target-hit, 2 mask, 3 expect-matrix, 4 expect-ofa, 5 maxmin. */
+double gm_last_kernel_ms(int32_t family);
+/* Enables per-launch CUDA-event timing of the kernel families above (default off). */
+void gm_enable_kernel_timing(int32_t on);
+/* Sum of device ms per family since the last reset, and the launch count per family. */
+double gm_kernel_ms_total(int32_t family);
+int64_t gm_kernel_launches(int32_t family);
+void gm_reset_kernel_stats(void);
+
+/* ------------------------------------------------------------- stage (i) */
+
+/* build_matrix (abstraction.hpp:112, abstraction.cpp:197-225) restricted to rows
+ * [row_begin, row_end) (whole matrix: 0, rows). Unmasked. Device-resident. */
+gm_code gm_build_matrix(gm_model* m, int64_t row_begin, int64_t row_end, gm_matrix** out,
+                        gm_status* st);
+/* mask_absorbing (abstraction.hpp:121, abstraction.cpp:322-344); idempotent. */
+gm_code gm_mask_absorbing(gm_model* m, gm_matrix* tm, gm_status* st);
+/* build_target_hit (abstraction.hpp:117, abstraction.cpp:246-271) for rows
+ * [row_begin,row_end) into host memory (row_end-row_begin doubles). */
+gm_code gm_build_target_hit(gm_model* m, int64_t row_begin, int64_t row_end, double* t0x_out,
+                            gm_status* st);
+/* Copies rows [row_begin,row_end) (absolute row indices inside the matrix's range)
+ * of origins (int64) and probabilities (row-major R doubles) to host memory. */
+gm_code gm_matrix_copy_rows(const gm_matrix* tm, int64_t row_begin, int64_t row_end,
+                            int64_t* origins_out, double* probs_out, gm_status* st);
+/* Device pointers and row range of a matrix (for stream-level callers). */
+gm_code gm_matrix_info(const gm_matrix* tm, int64_t* row_begin, int64_t* row_end,
+                       int64_t* row_width, const double** d_probs, const int64_t** d_origins,
+                       gm_status* st);
+/* write_matrix (io.hpp:19, io.cpp:236-256): the raw `gridmdp-matrix 1` container. */
+gm_code gm_matrix_write(const gm_matrix* tm, const gm_model* m, const char* path, gm_status* st);
+void gm_matrix_free(gm_matrix* tm);
+
+/* ------------------------------------------------------------ stage (ii) */
+
+/* bellman_step (synthesis.hpp:58, synthesis.cpp:147-161): one backward step with a
+ * caller-supplied v_next (host, n_states doubles). tm NULL = on-the-fly (OFA).
+ * For reach specs with a matrix, tm must be masked and t0x (host, one double per
+ * row of tm) supplies the target-hit vector; NULL reuses / builds tm's own.
+ * policy_out / wstar_out may be NULL. */
+gm_code gm_bellman_step(gm_model* m, gm_matrix* tm, const double* t0x, const double* v_next,
+                        double* v_out, uint32_t* policy_out, uint32_t* wstar_out, gm_status* st);
+
+/* Device-level sharded step for multi-GPU drivers: states [x_begin,x_end) of the
+ * backward step, reading the FULL v_next (device, n_states doubles, absorbing
+ * entries already zero for reach specs) and writing v_out/policy/wstar for the
+ * shard (device, x_end-x_begin entries). tm NULL = OFA; otherwise tm must cover
+ * exactly the shard's rows and carry its target-hit vector (gm_build_shard).
+ * `stream` is a cudaStream_t (NULL = default stream). Asynchronous. */
+gm_code gm_step_device(gm_model* m, gm_matrix* tm, int64_t x_begin, int64_t x_end,
+                       const double* d_v_next, double* d_v_out, uint32_t* d_policy,
+                       uint32_t* d_wstar, void* stream, gm_status* st);
+/* Matrix for the rows of states [x_begin,x_end), masked-equivalent and with its
+ * target-hit vector fused into the same build kernel (synthesize_with_matrix prologue,
+ * synthesis.cpp:199-212). When *out is not NULL the matrix is rebuilt in place,
+ * reusing its device buffers. */
+gm_code gm_build_shard(gm_model* m, int64_t x_begin, int64_t x_end, gm_matrix** out,
+                       gm_status* st);
+/* Per-row expected values of the model's most recent step (the v_in workspace of
+ * bellman_impl, synthesis.cpp:69-109), rows of the stepped states; n doubles. */
+gm_code gm_copy_row_values(gm_model* m, double* out, int64_t n, gm_status* st);
+/* Checks (after a stream sync) whether a device domain error was recorded and
+ * raises it with the reference's message. */
+gm_code gm_check_device_errors(gm_model* m, gm_status* st);
+/* Zeroes absorbing states of a device V vector in place (reach specs only). */
+gm_code gm_zero_absorbing_device(gm_model* m, double* d_v, void* stream, gm_status* st);
+
+/* synthesize (synthesis.hpp:46, synthesis.cpp:214-228) in the model's mode. */
+gm_code gm_synthesize(gm_model* m, gm_result** out, gm_status* st);
+/* synthesize_with_matrix (synthesis.hpp:51, synthesis.cpp:199-212); t0x may be NULL
+ * (built on demand), host array of tm rows otherwise. */
+gm_code gm_synthesize_with_matrix(gm_model* m, gm_matrix* tm, const double* t0x,
+                                  gm_result** out, gm_status* st);
+
+/* Result tables (SynthesisResult): values n_states x (T+1) column-major f64,
+ * policy / worst_dist n_states x T column-major u32, absorbing n_states u8 (reach) */
+gm_code gm_result_shape(const gm_result* r, int64_t* n_states, int32_t* horizon,
+                        int32_t* has_absorbing, int32_t* mode, gm_status* st);
+gm_code gm_result_copy(const gm_result* r, double* values, uint32_t* policy, uint32_t* worst,
+                       uint8_t* absorbing, gm_status* st);
+/* Builds a result from caller tables (e.g. a multi-GPU driver's gathered tables). */
+gm_code gm_result_from_tables(const gm_model* m, const double* values, const uint32_t* policy,
+                              const uint32_t* worst, gm_result** out, gm_status* st);
+/* write_results (io.hpp:13, io.cpp:142-179): the `gridmdp-results 1` container. */
+gm_code gm_result_write(const gm_result* r, const char* path, gm_status* st);
+void gm_result_free(gm_result* r);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GRIDMDP_B200_H */

@@ -1,0 +1,1062 @@
+// C ABI of libgridmdp_b200.so (include/gridmdp_b200.h): model lifetime, device
+// residency, stage (i)/(ii) orchestration over the kernels in gm_kernels.cu,
+// and the reference's container formats (io.cpp:142-256).
+#include "gridmdp_b200.h"
+
+#include "gm_host.hpp"
+#include "gm_kernels.cuh"
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <climits>
+#include <cstring>
+#include <fstream>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <tuple>
+#include <vector>
+
+using namespace gmh;
+
+// ===========================================================================
+// status plumbing
+// ===========================================================================
+
+namespace {
+
+void put_status(gm_status* st, int code, const std::string& msg, int64_t row = -1, int parse = 0) {
+    if (!st) return;
+    st->code = code;
+    st->is_parse = parse;
+    st->first_bad_row = row;
+    std::strncpy(st->msg, msg.c_str(), sizeof(st->msg) - 1);
+    st->msg[sizeof(st->msg) - 1] = '\0';
+}
+
+struct DomainAt : DomainErr {
+    int64_t row;
+    DomainAt(const std::string& m, int64_t r) : DomainErr(m), row(r) {}
+};
+
+template <class F>
+gm_code guarded(gm_status* st, F&& f) {
+    put_status(st, GM_OK, "");
+    try {
+        f();
+        return GM_OK;
+    } catch (const ParseErr& e) {
+        put_status(st, GM_ERR_CONFIG, e.what(), -1, 1);
+        return GM_ERR_CONFIG;
+    } catch (const ConfigErr& e) {
+        put_status(st, GM_ERR_CONFIG, e.what());
+        return GM_ERR_CONFIG;
+    } catch (const MemoryErr& e) {
+        put_status(st, GM_ERR_MEMORY, e.what());
+        return GM_ERR_MEMORY;
+    } catch (const DomainAt& e) {
+        put_status(st, GM_ERR_DOMAIN, e.what(), e.row);
+        return GM_ERR_DOMAIN;
+    } catch (const DomainErr& e) {
+        put_status(st, GM_ERR_DOMAIN, e.what());
+        return GM_ERR_DOMAIN;
+    } catch (const IoErr& e) {
+        put_status(st, GM_ERR_IO, e.what());
+        return GM_ERR_IO;
+    } catch (const std::out_of_range& e) {
+        put_status(st, GM_ERR_RANGE, e.what());
+        return GM_ERR_RANGE;
+    } catch (const CudaErr& e) {
+        put_status(st, GM_ERR_CUDA, e.what());
+        return GM_ERR_CUDA;
+    } catch (const std::bad_alloc&) {
+        put_status(st, GM_ERR_MEMORY, "host allocation failed");
+        return GM_ERR_MEMORY;
+    } catch (const std::exception& e) {
+        put_status(st, GM_ERR_OTHER, e.what());
+        return GM_ERR_OTHER;
+    }
+}
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        if (e == cudaErrorMemoryAllocation)
+            throw MemoryErr(std::string(what) + ": device allocation failed (" + cudaGetErrorString(e) + ")");
+        throw CudaErr(std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void ensure(size_t count, const char* what) {
+        if (count <= n && p) return;
+        release();
+        if (count == 0) count = 1;
+        ck(cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T)), what);
+        n = count;
+    }
+};
+
+// ---------------------------------------------------------------- timing
+std::atomic<long long> g_launches{0};
+std::mutex g_tmu;
+bool g_timing = false;
+double g_total_ms[gmk::KF_COUNT] = {};
+double g_last_ms[gmk::KF_COUNT] = {};
+long long g_fam_launches[gmk::KF_COUNT] = {};
+std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> g_pending;
+std::vector<cudaEvent_t> g_pool;
+
+cudaEvent_t take_event() {
+    if (!g_pool.empty()) {
+        cudaEvent_t e = g_pool.back();
+        g_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    ck(cudaEventCreate(&e), "cudaEventCreate");
+    return e;
+}
+
+void collect_timing() {
+    std::lock_guard<std::mutex> lk(g_tmu);
+    for (auto& [fam, a, b] : g_pending) {
+        cudaEventSynchronize(b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        g_total_ms[fam] += ms;
+        g_last_ms[fam] = ms;
+        g_pool.push_back(a);
+        g_pool.push_back(b);
+    }
+    g_pending.clear();
+}
+
+struct Launch {
+    int fam;
+    cudaStream_t s;
+    cudaEvent_t a = nullptr, b = nullptr;
+    Launch(int f, cudaStream_t st) : fam(f), s(st) {
+        ++g_launches;
+        {
+            std::lock_guard<std::mutex> lk(g_tmu);
+            ++g_fam_launches[fam];
+        }
+        if (g_timing) {
+            std::lock_guard<std::mutex> lk(g_tmu);
+            a = take_event();
+            b = take_event();
+            cudaEventRecord(a, s);
+        }
+    }
+    ~Launch() {
+        if (a) {
+            cudaEventRecord(b, s);
+            std::lock_guard<std::mutex> lk(g_tmu);
+            g_pending.emplace_back(fam, a, b);
+        }
+    }
+};
+
+} // namespace
+
+// ===========================================================================
+// opaque handles
+// ===========================================================================
+
+struct gm_model {
+    Model M;
+    GmDev D{};
+    int device = -1;
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr; // the model's stream when a caller stream is in use
+    DevBuf<GmIns> d_prog;
+    DevBuf<double> d_lits;
+    DevBuf<int> d_lines;
+    DevBuf<uint8_t> d_absorb;
+    DevBuf<unsigned long long> d_err;
+    // step scratch
+    DevBuf<double> d_mass, d_t0x, d_vin, d_vtmp;
+    DevBuf<long long> d_origin;
+    DevBuf<uint8_t> d_rowflag;
+    bool dev_ready = false;
+    bool absorb_ready = false;
+};
+
+struct gm_matrix {
+    int device = -1;
+    int64_t row_begin = 0, row_end = 0, R = 0;
+    DevBuf<double> probs;
+    DevBuf<long long> origins;
+    DevBuf<double> t0x; // optional (shard builds for reach specs)
+    bool has_t0x = false;
+    bool masked = false;
+};
+
+struct gm_result {
+    Model meta; // grids, spec, gamma for the container
+    int mode = 0;
+    int64_t n_x = 0;
+    int T = 0;
+    std::vector<double> values;      // n_x x (T+1), column-major
+    std::vector<uint32_t> policy;    // n_x x T, column-major
+    std::vector<uint32_t> worst;     // n_x x T, column-major
+    std::vector<uint8_t> absorbing;  // n_x (reach) or empty
+};
+
+namespace {
+
+std::vector<int> line_offsets(const GmDev& D) {
+    // relative flat offset of every slab line (all axes but the last, row-major)
+    std::vector<int> out(static_cast<size_t>(D.n_lines), 0);
+    const int lead = D.n - 1; // real axes before the last
+    for (int L = 0; L < D.n_lines; ++L) {
+        long long rem = L, off = 0;
+        for (int d = lead - 1; d >= 0; --d) {
+            const long long j = rem % D.W[d];
+            rem /= D.W[d];
+            off += j * D.xstride[d];
+        }
+        out[static_cast<size_t>(L)] = static_cast<int>(off);
+    }
+    return out;
+}
+
+void ensure_device(gm_model* m) {
+    if (m->dev_ready) {
+        ck(cudaSetDevice(m->device), "cudaSetDevice");
+        return;
+    }
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        throw CudaErr("no CUDA device available: the B200 engine has no CPU fallback");
+    }
+    int dev = 0;
+    ck(cudaGetDevice(&dev), "cudaGetDevice");
+    m->device = dev;
+    ck(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    const Program& P = m->M.prog;
+    m->d_prog.ensure(P.code.size(), "program");
+    if (!P.code.empty())
+        ck(cudaMemcpy(m->d_prog.p, P.code.data(), P.code.size() * sizeof(GmIns), cudaMemcpyHostToDevice), "program");
+    m->d_lits.ensure(P.lits.size(), "literals");
+    if (!P.lits.empty())
+        ck(cudaMemcpy(m->d_lits.p, P.lits.data(), P.lits.size() * sizeof(double), cudaMemcpyHostToDevice), "literals");
+    m->d_err.ensure(1, "error slot");
+    const unsigned long long none = ULLONG_MAX;
+    ck(cudaMemcpy(m->d_err.p, &none, sizeof none, cudaMemcpyHostToDevice), "error slot");
+    m->dev_ready = true;
+}
+
+// descriptor refresh after spec/model changes; uploads the line table and
+// absorbing flags (absorbing_states, spec.cpp:51-60 -> k_absorb)
+void refresh_device(gm_model* m) {
+    ensure_device(m);
+    if (m->M.R > INT_MAX) throw MemoryErr("row width exceeds the device limit");
+    m->D = m->M.device_descriptor();
+    m->D.prog = m->d_prog.p;
+    m->D.lits = m->d_lits.p;
+    const std::vector<int> lines = line_offsets(m->D);
+    m->d_lines.ensure(lines.size(), "line table");
+    ck(cudaMemcpy(m->d_lines.p, lines.data(), lines.size() * sizeof(int), cudaMemcpyHostToDevice), "line table");
+    m->D.line_off = m->d_lines.p;
+    m->D.absorb = nullptr;
+    if (m->M.spec.reach()) {
+        m->d_absorb.ensure(static_cast<size_t>(m->M.n_x()), "absorbing flags");
+        {
+            Launch L(gmk::KF_MISC, m->stream);
+            gmk::absorb_flags(m->D, m->d_absorb.p, m->stream);
+        }
+        m->D.absorb = m->d_absorb.p;
+    }
+    ck(cudaStreamSynchronize(m->stream), "absorbing flags");
+    m->absorb_ready = true;
+}
+
+void prepare(gm_model* m) {
+    if (!m->dev_ready || !m->absorb_ready) refresh_device(m);
+    else ck(cudaSetDevice(m->device), "cudaSetDevice");
+}
+
+// Raises the reference's DomainError for the lowest failing row, if any.
+void raise_device_error(gm_model* m) {
+    unsigned long long row = ULLONG_MAX;
+    ck(cudaMemcpy(&row, m->d_err.p, sizeof row, cudaMemcpyDeviceToHost), "error slot");
+    if (row == ULLONG_MAX) return;
+    const unsigned long long none = ULLONG_MAX;
+    ck(cudaMemcpy(m->d_err.p, &none, sizeof none, cudaMemcpyHostToDevice), "error slot");
+    std::vector<double> mu;
+    try {
+        m->M.row_image(static_cast<int64_t>(row), mu);
+    } catch (const DomainErr& e) {
+        throw DomainAt(e.what(), static_cast<int64_t>(row));
+    }
+    throw DomainAt("inc_beta: continued fraction did not converge", static_cast<int64_t>(row));
+}
+
+int64_t chunk_rows(const gm_model* m) {
+    const int64_t per_row = static_cast<int64_t>(m->D.sumW) * 8 + 8 + 8 + 1;
+    int64_t c = (64LL << 20) / std::max<int64_t>(per_row, 1);
+    c = std::max<int64_t>(c, 4096);
+    return c;
+}
+
+void ensure_scratch(gm_model* m, int64_t chunk) {
+    m->d_mass.ensure(static_cast<size_t>(chunk) * std::max(m->D.sumW, 1), "mass scratch");
+    m->d_origin.ensure(static_cast<size_t>(chunk), "origin scratch");
+    m->d_t0x.ensure(static_cast<size_t>(chunk), "t0x scratch");
+    m->d_rowflag.ensure(static_cast<size_t>(chunk), "row flags");
+}
+
+// Stage (i) for rows [r0, r1): origins + probabilities (+ T0x for reach shards)
+void build_rows(gm_model* m, int64_t r0, int64_t r1, gm_matrix* tm, bool want_t0x) {
+    const int64_t n = r1 - r0;
+    tm->device = m->device;
+    tm->row_begin = r0;
+    tm->row_end = r1;
+    tm->R = m->M.R;
+    const uint64_t cells = mul_checked(static_cast<uint64_t>(n), static_cast<uint64_t>(m->M.R), "matrix size");
+    tm->probs.ensure(cells, "matrix payload");
+    tm->origins.ensure(static_cast<size_t>(n), "matrix origins");
+    if (want_t0x) {
+        tm->t0x.ensure(static_cast<size_t>(n), "target-hit vector");
+        tm->has_t0x = true;
+    }
+    const int64_t chunk = chunk_rows(m);
+    ensure_scratch(m, std::min(chunk, std::max<int64_t>(n, 1)));
+    for (int64_t c0 = 0; c0 < n; c0 += chunk) {
+        const int64_t cn = std::min(chunk, n - c0);
+        {
+            Launch L(gmk::KF_PROLOGUE, m->stream);
+            gmk::prologue(m->D, r0 + c0, cn, gmk::PF_MASSES | (want_t0x ? gmk::PF_T0X : 0),
+                          tm->origins.p + c0, want_t0x ? tm->t0x.p + c0 : nullptr, nullptr, m->d_mass.p,
+                          m->d_err.p, m->stream);
+        }
+        {
+            Launch L(gmk::KF_EXPAND, m->stream);
+            gmk::expand(m->D, cn, m->d_mass.p, tm->probs.p + c0 * m->M.R, m->stream);
+        }
+    }
+    ck(cudaStreamSynchronize(m->stream), "build");
+    raise_device_error(m);
+}
+
+// One backward step over states [x0, x1) (bellman_impl, synthesis.cpp:61-143).
+// v_next: full device V (absorbing zeroed); outputs indexed from x0.
+void step_states(gm_model* m, gm_matrix* tm, int64_t x0, int64_t x1, const double* v_next,
+                 double* v_out, uint32_t* pol, uint32_t* wst, cudaStream_t s) {
+    const int64_t nuw = m->M.n_u() * m->M.n_w();
+    const int64_t r0 = x0 * nuw, r1 = x1 * nuw;
+    const int64_t n = r1 - r0;
+    m->d_vin.ensure(static_cast<size_t>(std::max<int64_t>(n, 1)), "v_in workspace");
+    if (tm) {
+        if (tm->row_begin > r0 || tm->row_end < r1)
+            throw ConfigErr("bellman step: the matrix does not cover the requested states");
+        Launch L(gmk::KF_EXPECT_MATRIX, s);
+        gmk::expect_matrix(m->D, tm->row_begin, r0 - tm->row_begin, r1 - tm->row_begin, tm->probs.p,
+                           tm->origins.p, tm->has_t0x ? tm->t0x.p : nullptr, v_next, m->d_vin.p, s);
+    } else {
+        const int64_t chunk = chunk_rows(m);
+        ensure_scratch(m, std::min(chunk, std::max<int64_t>(n, 1)));
+        const bool reach = m->M.spec.reach();
+        for (int64_t c0 = 0; c0 < n; c0 += chunk) {
+            const int64_t cn = std::min(chunk, n - c0);
+            {
+                Launch L(gmk::KF_PROLOGUE, s);
+                gmk::prologue(m->D, r0 + c0, cn,
+                              gmk::PF_SKIP_ABSORBED | gmk::PF_MASSES | (reach ? gmk::PF_T0X : 0),
+                              m->d_origin.p, m->d_t0x.p, m->d_rowflag.p, m->d_mass.p, m->d_err.p, s);
+            }
+            {
+                Launch L(gmk::KF_EXPECT_OFA, s);
+                gmk::expect_ofa(m->D, cn, m->d_mass.p, m->d_origin.p, m->d_t0x.p, m->d_rowflag.p, v_next,
+                                m->d_vin.p + c0, s);
+            }
+        }
+    }
+    Launch L(gmk::KF_MAXMIN, s);
+    gmk::maxmin(m->D, x0, x1 - x0, m->d_vin.p, v_out, pol, wst, s);
+}
+
+void ensure_t0x(gm_model* m, gm_matrix* tm) {
+    if (!m->M.spec.reach() || tm->has_t0x) return;
+    const int64_t n = tm->row_end - tm->row_begin;
+    tm->t0x.ensure(static_cast<size_t>(std::max<int64_t>(n, 1)), "target-hit vector");
+    const int64_t chunk = chunk_rows(m);
+    ensure_scratch(m, std::min(chunk, std::max<int64_t>(n, 1)));
+    for (int64_t c0 = 0; c0 < n; c0 += chunk) {
+        const int64_t cn = std::min(chunk, n - c0);
+        Launch L(gmk::KF_PROLOGUE, m->stream);
+        gmk::prologue(m->D, tm->row_begin + c0, cn, gmk::PF_SKIP_ABSORBED | gmk::PF_T0X, m->d_origin.p,
+                      tm->t0x.p + c0, m->d_rowflag.p, nullptr, m->d_err.p, m->stream);
+    }
+    ck(cudaStreamSynchronize(m->stream), "target hit");
+    raise_device_error(m);
+    tm->has_t0x = true;
+}
+
+// run_backward (synthesis.cpp:165-195) over all states on one device.
+gm_result* run_backward(gm_model* m, gm_matrix* tm) {
+    const int64_t n_x = m->M.n_x();
+    const int T = m->M.spec.horizon;
+    const bool reach = m->M.spec.reach();
+    DevBuf<double> vals;
+    DevBuf<uint32_t> pol, wst;
+    vals.ensure(static_cast<size_t>(n_x) * (T + 1), "value table");
+    pol.ensure(static_cast<size_t>(n_x) * T, "policy table");
+    wst.ensure(static_cast<size_t>(n_x) * T, "worst-disturbance table");
+    {
+        std::vector<double> term(static_cast<size_t>(n_x), reach ? 0.0 : 1.0);
+        ck(cudaMemcpy(vals.p + static_cast<size_t>(n_x) * T, term.data(), term.size() * 8, cudaMemcpyHostToDevice),
+           "terminal column");
+    }
+    for (int k = T - 1; k >= 0; --k) {
+        step_states(m, tm, 0, n_x, vals.p + static_cast<size_t>(n_x) * (k + 1), vals.p + static_cast<size_t>(n_x) * k,
+                    pol.p + static_cast<size_t>(n_x) * k, wst.p + static_cast<size_t>(n_x) * k, m->stream);
+        if (k == T - 1) {
+            ck(cudaStreamSynchronize(m->stream), "bellman step");
+            raise_device_error(m);
+        }
+    }
+    ck(cudaStreamSynchronize(m->stream), "bellman sweep");
+    raise_device_error(m);
+    auto* r = new gm_result;
+    r->meta = m->M;
+    r->mode = tm ? GM_MODE_MATRIX : GM_MODE_OFA;
+    r->n_x = n_x;
+    r->T = T;
+    r->values.resize(static_cast<size_t>(n_x) * (T + 1));
+    r->policy.resize(static_cast<size_t>(n_x) * T);
+    r->worst.resize(static_cast<size_t>(n_x) * T);
+    ck(cudaMemcpy(r->values.data(), vals.p, r->values.size() * 8, cudaMemcpyDeviceToHost), "values");
+    if (T > 0) {
+        ck(cudaMemcpy(r->policy.data(), pol.p, r->policy.size() * 4, cudaMemcpyDeviceToHost), "policy");
+        ck(cudaMemcpy(r->worst.data(), wst.p, r->worst.size() * 4, cudaMemcpyDeviceToHost), "worst");
+    }
+    if (reach) {
+        r->absorbing.resize(static_cast<size_t>(n_x));
+        ck(cudaMemcpy(r->absorbing.data(), m->d_absorb.p, static_cast<size_t>(n_x), cudaMemcpyDeviceToHost),
+           "absorbing");
+    }
+    return r;
+}
+
+// ---------------------------------------------------------------- containers
+
+void put_u64(std::ostream& os, uint64_t v) {
+    char b[8];
+    for (int i = 0; i < 8; ++i) b[i] = static_cast<char>((v >> (8 * i)) & 0xff);
+    os.write(b, 8);
+}
+void put_u32(std::ostream& os, uint32_t v) {
+    char b[4];
+    for (int i = 0; i < 4; ++i) b[i] = static_cast<char>((v >> (8 * i)) & 0xff);
+    os.write(b, 4);
+}
+void put_f64(std::ostream& os, double v) {
+    uint64_t u;
+    std::memcpy(&u, &v, 8);
+    put_u64(os, u);
+}
+
+void grid_lines(std::ostream& os, const char* prefix, const Grid& g) {
+    os << prefix << ".dim = " << g.dim() << ";\n";
+    if (g.dim() == 0) return;
+    os << prefix << ".lb = " << fmt_vec(g.lb) << ";\n";
+    os << prefix << ".ub = " << fmt_vec(g.ub) << ";\n";
+    os << prefix << ".eta = " << fmt_vec(g.eta) << ";\n";
+}
+
+const char* kind_name(int k) {
+    return k == GM_SPEC_SAFETY ? "safety" : k == GM_SPEC_REACH ? "reachability" : "reach-avoid";
+}
+
+} // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+
+extern "C" {
+
+static void apply_overrides(Cfg& c, const gm_overrides* ov) {
+    if (!ov) return;
+    if (ov->threads >= 0) c.threads = ov->threads;
+    if (ov->mode && *ov->mode) c.mode = ov->mode;
+    if (ov->mem_budget >= 0) c.mem_budget = static_cast<uint64_t>(ov->mem_budget);
+    if (ov->seed >= 0) c.seed = static_cast<uint64_t>(ov->seed);
+    if (ov->runs >= 0) c.runs = ov->runs;
+    if (ov->time_steps >= 0) c.time_steps = ov->time_steps;
+    if (ov->output && *ov->output) c.output = ov->output;
+}
+
+static gm_code make_model(const Cfg& c0, const gm_overrides* ov, gm_model** out, gm_status* st) {
+    return guarded(st, [&] {
+        Cfg c = c0;
+        apply_overrides(c, ov);
+        auto* m = new gm_model;
+        try {
+            m->M = build_model_from_cfg(c);
+        } catch (...) {
+            delete m;
+            throw;
+        }
+        *out = m;
+    });
+}
+
+gm_code gm_model_load(const char* path, const gm_overrides* ov, gm_model** out, gm_status* st) {
+    Cfg c;
+    const gm_code rc = guarded(st, [&] { c = load_cfg_file(path ? path : ""); });
+    if (rc != GM_OK) return rc;
+    return make_model(c, ov, out, st);
+}
+
+gm_code gm_model_parse(const char* text, const char* name, const gm_overrides* ov, gm_model** out,
+                       gm_status* st) {
+    Cfg c;
+    const gm_code rc = guarded(st, [&] { c = parse_cfg_text(text ? text : "", name ? name : "<config>"); });
+    if (rc != GM_OK) return rc;
+    return make_model(c, ov, out, st);
+}
+
+void gm_model_free(gm_model* m) {
+    if (!m) return;
+    if (m->dev_ready) {
+        cudaSetDevice(m->device);
+        cudaStreamSynchronize(m->stream);
+        cudaStreamDestroy(m->own_stream ? m->own_stream : m->stream);
+    }
+    delete m;
+}
+
+gm_code gm_model_set_spec(gm_model* m, int32_t kind, int32_t horizon, const double* tlo, const double* thi,
+                          const double* alo, const double* ahi, gm_status* st) {
+    return guarded(st, [&] {
+        const int n = m->M.X.dim();
+        SpecV s;
+        s.kind = kind;
+        s.horizon = horizon;
+        if (tlo && thi) s.target = BoxV{std::vector<double>(tlo, tlo + n), std::vector<double>(thi, thi + n)};
+        if (alo && ahi) s.avoid = BoxV{std::vector<double>(alo, alo + n), std::vector<double>(ahi, ahi + n)};
+        m->M.spec = s;
+        m->absorb_ready = false;
+    });
+}
+
+gm_code gm_model_set_options(gm_model* m, int32_t mode, int64_t mem_budget, gm_status* st) {
+    return guarded(st, [&] {
+        if (mode >= 0) m->M.mode = mode;
+        if (mem_budget >= 0) m->M.mem_budget = static_cast<uint64_t>(mem_budget);
+    });
+}
+
+gm_code gm_model_sizes(const gm_model* m, gm_sizes* o, gm_status* st) {
+    return guarded(st, [&] {
+        std::memset(o, 0, sizeof *o);
+        const Model& M = m->M;
+        o->n_dim = M.X.dim();
+        o->m_dim = M.U.dim();
+        o->p_dim = M.W.dim();
+        o->n_states = M.n_x();
+        o->n_inputs = M.n_u();
+        o->n_disturbances = M.n_w();
+        o->pairs = M.n_x() * M.n_u();
+        o->spec_kind = M.spec.kind;
+        o->horizon = M.spec.horizon;
+        o->mode = M.mode;
+        o->threads = M.threads;
+        o->gamma = M.noise.gamma;
+        o->mem_budget = static_cast<int64_t>(M.mem_budget);
+        for (int d = 0; d < M.X.dim() && d < GM_MAX_DIMS; ++d) {
+            o->counts[d] = M.X.count[d];
+            o->strides[d] = M.X.stride[d];
+            o->extents[d] = M.extents[d];
+        }
+        o->row_width = M.R;
+        o->rows_per_thread_group = tpr_for_width(M.R);
+        o->rows = M.rows();
+        o->memory_estimate = M.memory_estimate();
+    });
+}
+
+gm_code gm_absorbing_states(gm_model* m, uint8_t* flags, gm_status* st) {
+    return guarded(st, [&] {
+        prepare(m);
+        const size_t n = static_cast<size_t>(m->M.n_x());
+        if (!m->M.spec.reach()) {
+            std::memset(flags, 0, n);
+            return;
+        }
+        ck(cudaMemcpy(flags, m->d_absorb.p, n, cudaMemcpyDeviceToHost), "absorbing flags");
+    });
+}
+
+gm_code gm_dynamics_image(const gm_model* m, int64_t row, double* mu_out, gm_status* st) {
+    return guarded(st, [&] {
+        if (row < 0 || row >= m->M.rows()) throw std::out_of_range("dynamics_image: row out of range");
+        std::vector<double> mu;
+        m->M.row_image(row, mu);
+        std::memcpy(mu_out, mu.data(), mu.size() * 8);
+    });
+}
+
+const char* gm_model_output_path(const gm_model* m) { return m->M.cfg.output.c_str(); }
+
+int64_t gm_model_program_size(const gm_model* m) { return static_cast<int64_t>(m->M.prog.code.size()); }
+
+gm_code gm_set_device(int32_t device, gm_status* st) {
+    return guarded(st, [&] { ck(cudaSetDevice(device), "cudaSetDevice"); });
+}
+
+gm_code gm_model_set_stream(gm_model* m, void* stream, gm_status* st) {
+    return guarded(st, [&] {
+        ensure_device(m);
+        if (!m->own_stream) m->own_stream = m->stream;
+        m->stream = stream ? static_cast<cudaStream_t>(stream) : m->own_stream;
+    });
+}
+
+int64_t gm_launch_count(void) { return g_launches.load(); }
+
+double gm_last_kernel_ms(int32_t family) {
+    collect_timing();
+    if (family < 0 || family >= gmk::KF_COUNT) return 0.0;
+    return g_last_ms[family];
+}
+
+void gm_enable_kernel_timing(int32_t on) {
+    collect_timing();
+    g_timing = on != 0;
+}
+
+double gm_kernel_ms_total(int32_t family) {
+    collect_timing();
+    if (family < 0 || family >= gmk::KF_COUNT) return 0.0;
+    return g_total_ms[family];
+}
+
+int64_t gm_kernel_launches(int32_t family) {
+    if (family < 0 || family >= gmk::KF_COUNT) return 0;
+    std::lock_guard<std::mutex> lk(g_tmu);
+    return g_fam_launches[family];
+}
+
+void gm_reset_kernel_stats(void) {
+    collect_timing();
+    std::lock_guard<std::mutex> lk(g_tmu);
+    for (int i = 0; i < gmk::KF_COUNT; ++i) {
+        g_total_ms[i] = 0;
+        g_last_ms[i] = 0;
+        g_fam_launches[i] = 0;
+    }
+}
+
+// ---------------------------------------------------------------- stage (i)
+
+gm_code gm_build_matrix(gm_model* m, int64_t r0, int64_t r1, gm_matrix** out, gm_status* st) {
+    return guarded(st, [&] {
+        const int64_t rows = m->M.rows();
+        if (r0 < 0 || r1 > rows || r0 > r1) throw std::out_of_range("build_matrix: row range outside the model");
+        prepare(m);
+        auto tm = std::make_unique<gm_matrix>();
+        build_rows(m, r0, r1, tm.get(), false);
+        *out = tm.release();
+    });
+}
+
+gm_code gm_build_shard(gm_model* m, int64_t x0, int64_t x1, gm_matrix** out, gm_status* st) {
+    return guarded(st, [&] {
+        if (x0 < 0 || x1 > m->M.n_x() || x0 > x1) throw std::out_of_range("build_shard: state range outside the grid");
+        check_spec(m->M.spec, m->M.X);
+        prepare(m);
+        const int64_t nuw = m->M.n_u() * m->M.n_w();
+        if (*out) { // rebuild in place
+            (*out)->has_t0x = false;
+            (*out)->masked = false;
+            build_rows(m, x0 * nuw, x1 * nuw, *out, m->M.spec.reach());
+            return;
+        }
+        auto tm = std::make_unique<gm_matrix>();
+        build_rows(m, x0 * nuw, x1 * nuw, tm.get(), m->M.spec.reach());
+        *out = tm.release();
+    });
+}
+
+gm_code gm_mask_absorbing(gm_model* m, gm_matrix* tm, gm_status* st) {
+    return guarded(st, [&] {
+        if (!m->M.spec.reach()) return; // abstraction.cpp:323
+        prepare(m);
+        const Model& M = m->M;
+        const int n = M.X.dim();
+        std::vector<long long> off(static_cast<size_t>(n) + 1, 0);
+        for (int d = 0; d < n; ++d) off[d + 1] = off[d] + M.X.count[d];
+        auto member = [&](const BoxV& b) {
+            std::vector<uint8_t> f(static_cast<size_t>(off[n]), 0);
+            if (b.dim() != n) return f;
+            for (int d = 0; d < n; ++d)
+                for (int64_t j = 0; j < M.X.count[d]; ++j) {
+                    const double rep = M.X.rep(d, j);
+                    f[static_cast<size_t>(off[d] + j)] = (rep >= b.lo[d] && rep <= b.hi[d]) ? 1 : 0;
+                }
+            return f;
+        };
+        const auto inT = member(M.spec.target);
+        const bool haveA = M.spec.avoid.dim() > 0;
+        const auto inA = haveA ? member(M.spec.avoid) : std::vector<uint8_t>{};
+        DevBuf<uint8_t> dT, dA;
+        DevBuf<long long> dOff;
+        dT.ensure(inT.size(), "mask flags");
+        ck(cudaMemcpy(dT.p, inT.data(), inT.size(), cudaMemcpyHostToDevice), "mask flags");
+        if (haveA) {
+            dA.ensure(inA.size(), "mask flags");
+            ck(cudaMemcpy(dA.p, inA.data(), inA.size(), cudaMemcpyHostToDevice), "mask flags");
+        }
+        dOff.ensure(off.size(), "mask offsets");
+        ck(cudaMemcpy(dOff.p, off.data(), off.size() * sizeof(long long), cudaMemcpyHostToDevice), "mask offsets");
+        {
+            Launch L(gmk::KF_MASK, m->stream);
+            gmk::mask(m->D, 0, tm->row_end - tm->row_begin, tm->probs.p, tm->origins.p, dT.p,
+                      haveA ? dA.p : nullptr, dOff.p, m->stream);
+        }
+        ck(cudaStreamSynchronize(m->stream), "mask");
+        tm->masked = true;
+    });
+}
+
+gm_code gm_build_target_hit(gm_model* m, int64_t r0, int64_t r1, double* t0x_out, gm_status* st) {
+    return guarded(st, [&] {
+        check_spec(m->M.spec, m->M.X);
+        if (!m->M.spec.reach())
+            throw ConfigErr("build_target_hit requires a reachability or reach-avoid spec");
+        if (r0 < 0 || r1 > m->M.rows() || r0 > r1) throw std::out_of_range("build_target_hit: row range");
+        prepare(m);
+        gm_matrix tmp;
+        tmp.row_begin = r0;
+        tmp.row_end = r1;
+        ensure_t0x(m, &tmp);
+        if (r1 > r0)
+            ck(cudaMemcpy(t0x_out, tmp.t0x.p, static_cast<size_t>(r1 - r0) * 8, cudaMemcpyDeviceToHost), "t0x");
+    });
+}
+
+gm_code gm_matrix_copy_rows(const gm_matrix* tm, int64_t r0, int64_t r1, int64_t* origins, double* probs,
+                            gm_status* st) {
+    return guarded(st, [&] {
+        if (r0 < tm->row_begin || r1 > tm->row_end || r0 > r1) throw std::out_of_range("matrix rows out of range");
+        ck(cudaSetDevice(tm->device), "cudaSetDevice");
+        const int64_t a = r0 - tm->row_begin, n = r1 - r0;
+        if (n == 0) return;
+        if (origins)
+            ck(cudaMemcpy(origins, tm->origins.p + a, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost), "origins");
+        if (probs)
+            ck(cudaMemcpy(probs, tm->probs.p + a * tm->R, static_cast<size_t>(n * tm->R) * 8, cudaMemcpyDeviceToHost),
+               "probs");
+    });
+}
+
+gm_code gm_matrix_info(const gm_matrix* tm, int64_t* rb, int64_t* re, int64_t* R, const double** probs,
+                       const int64_t** origins, gm_status* st) {
+    return guarded(st, [&] {
+        if (rb) *rb = tm->row_begin;
+        if (re) *re = tm->row_end;
+        if (R) *R = tm->R;
+        if (probs) *probs = tm->probs.p;
+        if (origins) *origins = reinterpret_cast<const int64_t*>(tm->origins.p);
+    });
+}
+
+gm_code gm_matrix_write(const gm_matrix* tm, const gm_model* m, const char* path, gm_status* st) {
+    return guarded(st, [&] {
+        // write_matrix, io.cpp:236-256
+        if (tm->row_begin != 0 || tm->row_end != m->M.rows())
+            throw IoErr("write_matrix needs the whole matrix (rows 0..rows)");
+        std::ofstream os(path, std::ios::binary);
+        if (!os) throw IoErr(std::string("cannot open '") + path + "' for writing");
+        const Model& M = m->M;
+        os << "gridmdp-matrix" << ' ' << 1 << '\n';
+        grid_lines(os, "states", M.X);
+        os << "n_inputs = " << M.n_u() << ";\n";
+        os << "n_disturbances = " << M.n_w() << ";\n";
+        std::string w = "{";
+        for (size_t d = 0; d < M.extents.size(); ++d) {
+            if (d) w += ", ";
+            w += std::to_string(M.extents[d]);
+        }
+        os << "window = " << w << "};\n";
+        const int64_t rows = tm->row_end - tm->row_begin;
+        os << "array.origins = i64 " << rows << " 1;\n";
+        os << "array.probs = f64 " << rows << " " << tm->R << ";\n";
+        os << "payload\n";
+        ck(cudaSetDevice(tm->device), "cudaSetDevice");
+        std::vector<long long> org(static_cast<size_t>(rows));
+        if (rows) ck(cudaMemcpy(org.data(), tm->origins.p, org.size() * 8, cudaMemcpyDeviceToHost), "origins");
+        for (long long o : org) put_u64(os, static_cast<uint64_t>(o));
+        const int64_t blk = std::max<int64_t>(1, (64LL << 20) / 8 / std::max<int64_t>(tm->R, 1));
+        std::vector<double> buf;
+        for (int64_t r = 0; r < rows; r += blk) {
+            const int64_t n = std::min(blk, rows - r);
+            buf.resize(static_cast<size_t>(n * tm->R));
+            ck(cudaMemcpy(buf.data(), tm->probs.p + r * tm->R, buf.size() * 8, cudaMemcpyDeviceToHost), "probs");
+            for (double v : buf) put_f64(os, v);
+        }
+        if (!os) throw IoErr(std::string("failed while writing '") + path + "'");
+    });
+}
+
+void gm_matrix_free(gm_matrix* tm) {
+    if (!tm) return;
+    if (tm->device >= 0) cudaSetDevice(tm->device);
+    delete tm;
+}
+
+// ---------------------------------------------------------------- stage (ii)
+
+gm_code gm_bellman_step(gm_model* m, gm_matrix* tm, const double* t0x, const double* v_next, double* v_out,
+                        uint32_t* pol, uint32_t* wst, gm_status* st) {
+    return guarded(st, [&] {
+        check_spec(m->M.spec, m->M.X);
+        prepare(m);
+        const int64_t n_x = m->M.n_x();
+        if (tm && (tm->row_begin != 0 || tm->row_end != m->M.rows()))
+            throw ConfigErr("bellman_step: the matrix must cover every row");
+        if (tm && t0x && m->M.spec.reach()) {
+            const size_t n = static_cast<size_t>(tm->row_end - tm->row_begin);
+            tm->t0x.ensure(std::max<size_t>(n, 1), "target-hit vector");
+            ck(cudaMemcpy(tm->t0x.p, t0x, n * 8, cudaMemcpyHostToDevice), "t0x");
+            tm->has_t0x = true;
+        }
+        if (tm) ensure_t0x(m, tm);
+        DevBuf<double> vn, vo;
+        DevBuf<uint32_t> dp, dw;
+        vn.ensure(static_cast<size_t>(n_x), "v_next");
+        vo.ensure(static_cast<size_t>(n_x), "v_out");
+        dp.ensure(static_cast<size_t>(n_x), "policy");
+        dw.ensure(static_cast<size_t>(n_x), "worst");
+        ck(cudaMemcpyAsync(vn.p, v_next, static_cast<size_t>(n_x) * 8, cudaMemcpyHostToDevice, m->stream), "v_next");
+        {
+            Launch L(gmk::KF_MISC, m->stream);
+            gmk::zero_absorbing(m->D, vn.p, m->stream);
+        }
+        step_states(m, tm, 0, n_x, vn.p, vo.p, dp.p, dw.p, m->stream);
+        ck(cudaStreamSynchronize(m->stream), "bellman step");
+        raise_device_error(m);
+        ck(cudaMemcpy(v_out, vo.p, static_cast<size_t>(n_x) * 8, cudaMemcpyDeviceToHost), "v_out");
+        if (pol) ck(cudaMemcpy(pol, dp.p, static_cast<size_t>(n_x) * 4, cudaMemcpyDeviceToHost), "policy");
+        if (wst) ck(cudaMemcpy(wst, dw.p, static_cast<size_t>(n_x) * 4, cudaMemcpyDeviceToHost), "worst");
+    });
+}
+
+gm_code gm_step_device(gm_model* m, gm_matrix* tm, int64_t x0, int64_t x1, const double* d_v_next, double* d_v_out,
+                       uint32_t* d_pol, uint32_t* d_wst, void* stream, gm_status* st) {
+    return guarded(st, [&] {
+        if (x0 < 0 || x1 > m->M.n_x() || x0 > x1) throw std::out_of_range("step_device: state range");
+        prepare(m);
+        if (tm) ensure_t0x(m, tm);
+        step_states(m, tm, x0, x1, d_v_next, d_v_out, d_pol, d_wst, static_cast<cudaStream_t>(stream));
+    });
+}
+
+gm_code gm_copy_row_values(gm_model* m, double* out, int64_t n, gm_status* st) {
+    return guarded(st, [&] {
+        prepare(m);
+        if (n < 0 || static_cast<size_t>(n) > m->d_vin.n) throw std::out_of_range("copy_row_values: size");
+        ck(cudaStreamSynchronize(m->stream), "sync");
+        if (n) ck(cudaMemcpy(out, m->d_vin.p, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost), "v_in");
+    });
+}
+
+gm_code gm_check_device_errors(gm_model* m, gm_status* st) {
+    return guarded(st, [&] {
+        prepare(m);
+        raise_device_error(m);
+    });
+}
+
+gm_code gm_zero_absorbing_device(gm_model* m, double* d_v, void* stream, gm_status* st) {
+    return guarded(st, [&] {
+        prepare(m);
+        Launch L(gmk::KF_MISC, static_cast<cudaStream_t>(stream));
+        gmk::zero_absorbing(m->D, d_v, static_cast<cudaStream_t>(stream));
+    });
+}
+
+gm_code gm_synthesize(gm_model* m, gm_result** out, gm_status* st) {
+    return guarded(st, [&] {
+        check_spec(m->M.spec, m->M.X);
+        if (m->M.mode == GM_MODE_MATRIX_) {
+            const uint64_t need = m->M.memory_estimate();
+            if (m->M.mem_budget != 0 && need > m->M.mem_budget) {
+                std::ostringstream os;
+                os << "matrix mode needs " << need << " bytes but the budget is " << m->M.mem_budget
+                   << "; use ofa mode";
+                throw MemoryErr(os.str());
+            }
+            prepare(m);
+            size_t free_b = 0, total_b = 0;
+            ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+            const uint64_t dev_need = need + static_cast<uint64_t>(m->M.rows()) * 16;
+            if (dev_need > static_cast<uint64_t>(free_b)) {
+                std::ostringstream os;
+                os << "matrix mode needs " << dev_need << " bytes of device memory but only " << free_b
+                   << " are free; use ofa mode";
+                throw MemoryErr(os.str());
+            }
+            gm_matrix tm;
+            build_rows(m, 0, m->M.rows(), &tm, m->M.spec.reach());
+            *out = run_backward(m, &tm);
+        } else {
+            prepare(m);
+            *out = run_backward(m, nullptr);
+        }
+    });
+}
+
+gm_code gm_synthesize_with_matrix(gm_model* m, gm_matrix* tm, const double* t0x, gm_result** out, gm_status* st) {
+    return guarded(st, [&] {
+        check_spec(m->M.spec, m->M.X);
+        prepare(m);
+        if (tm->row_begin != 0 || tm->row_end != m->M.rows())
+            throw ConfigErr("synthesize_with_matrix: the matrix must cover every row");
+        if (m->M.spec.reach()) {
+            gm_status s2;
+            if (gm_mask_absorbing(m, tm, &s2) != GM_OK) throw CudaErr(s2.msg);
+            if (t0x) {
+                tm->t0x.ensure(static_cast<size_t>(std::max<int64_t>(tm->row_end - tm->row_begin, 1)), "t0x");
+                ck(cudaMemcpy(tm->t0x.p, t0x, static_cast<size_t>(tm->row_end - tm->row_begin) * 8,
+                              cudaMemcpyHostToDevice),
+                   "t0x");
+                tm->has_t0x = true;
+            }
+        }
+        *out = run_backward(m, tm);
+    });
+}
+
+gm_code gm_result_shape(const gm_result* r, int64_t* n_x, int32_t* T, int32_t* has_abs, int32_t* mode,
+                        gm_status* st) {
+    return guarded(st, [&] {
+        if (n_x) *n_x = r->n_x;
+        if (T) *T = r->T;
+        if (has_abs) *has_abs = r->absorbing.empty() ? 0 : 1;
+        if (mode) *mode = r->mode;
+    });
+}
+
+gm_code gm_result_copy(const gm_result* r, double* values, uint32_t* policy, uint32_t* worst, uint8_t* absorbing,
+                       gm_status* st) {
+    return guarded(st, [&] {
+        if (values) std::memcpy(values, r->values.data(), r->values.size() * 8);
+        if (policy) std::memcpy(policy, r->policy.data(), r->policy.size() * 4);
+        if (worst) std::memcpy(worst, r->worst.data(), r->worst.size() * 4);
+        if (absorbing && !r->absorbing.empty()) std::memcpy(absorbing, r->absorbing.data(), r->absorbing.size());
+    });
+}
+
+gm_code gm_result_from_tables(const gm_model* m, const double* values, const uint32_t* policy, const uint32_t* worst,
+                              gm_result** out, gm_status* st) {
+    return guarded(st, [&] {
+        auto* r = new gm_result;
+        r->meta = m->M;
+        r->mode = m->M.mode;
+        r->n_x = m->M.n_x();
+        r->T = m->M.spec.horizon;
+        const size_t nx = static_cast<size_t>(r->n_x);
+        r->values.assign(values, values + nx * (r->T + 1));
+        r->policy.assign(policy, policy + nx * r->T);
+        r->worst.assign(worst, worst + nx * r->T);
+        if (m->M.spec.reach()) {
+            r->absorbing.resize(nx);
+            const Grid& g = m->M.X;
+            for (size_t i = 0; i < nx; ++i) {
+                const std::vector<double> p = grid_point(g, static_cast<int64_t>(i));
+                r->absorbing[i] = (m->M.spec.target.contains(p) ||
+                                   (m->M.spec.avoid.dim() > 0 && m->M.spec.avoid.contains(p)))
+                                      ? 1
+                                      : 0;
+            }
+        }
+        *out = r;
+    });
+}
+
+gm_code gm_result_write(const gm_result* r, const char* path, gm_status* st) {
+    return guarded(st, [&] {
+        // write_results, io.cpp:142-179
+        std::ofstream os(path, std::ios::binary);
+        if (!os) throw IoErr(std::string("cannot open '") + path + "' for writing");
+        const Model& M = r->meta;
+        const int64_t n_x = r->n_x;
+        const int T = r->T;
+        os << "gridmdp-results" << ' ' << 1 << '\n';
+        os << "mode = " << (r->mode == GM_MODE_MATRIX ? "matrix" : "ofa") << ";\n";
+        os << "gamma = " << fmt_shortest(M.noise.gamma) << ";\n";
+        os << "spec.type = " << kind_name(M.spec.kind) << ";\n";
+        os << "spec.time_steps = " << T << ";\n";
+        if (M.spec.target.dim() > 0) {
+            os << "target.lb = " << fmt_vec(M.spec.target.lo) << ";\n";
+            os << "target.ub = " << fmt_vec(M.spec.target.hi) << ";\n";
+        }
+        if (M.spec.avoid.dim() > 0) {
+            os << "avoid.lb = " << fmt_vec(M.spec.avoid.lo) << ";\n";
+            os << "avoid.ub = " << fmt_vec(M.spec.avoid.hi) << ";\n";
+        }
+        grid_lines(os, "states", M.X);
+        grid_lines(os, "inputs", M.U);
+        grid_lines(os, "disturbances", M.W);
+        os << "array.values = f64 " << n_x << " " << (T + 1) << ";\n";
+        os << "array.policy = u32 " << n_x << " " << T << ";\n";
+        os << "array.worst_dist = u32 " << n_x << " " << T << ";\n";
+        os << "array.absorbing = u8 " << r->absorbing.size() << " 1;\n";
+        os << "payload\n";
+        const size_t nx = static_cast<size_t>(n_x);
+        std::string buf;
+        buf.reserve(nx * (T + 1) * 8);
+        auto flush = [&] {
+            os.write(buf.data(), static_cast<std::streamsize>(buf.size()));
+            buf.clear();
+        };
+        std::ostringstream tmp;
+        for (size_t i = 0; i < nx; ++i)
+            for (int k = 0; k <= T; ++k) {
+                uint64_t u;
+                std::memcpy(&u, &r->values[static_cast<size_t>(k) * nx + i], 8);
+                for (int b = 0; b < 8; ++b) buf.push_back(static_cast<char>((u >> (8 * b)) & 0xff));
+            }
+        flush();
+        for (size_t i = 0; i < nx; ++i)
+            for (int k = 0; k < T; ++k) {
+                const uint32_t u = r->policy[static_cast<size_t>(k) * nx + i];
+                for (int b = 0; b < 4; ++b) buf.push_back(static_cast<char>((u >> (8 * b)) & 0xff));
+            }
+        flush();
+        for (size_t i = 0; i < nx; ++i)
+            for (int k = 0; k < T; ++k) {
+                const uint32_t u = r->worst[static_cast<size_t>(k) * nx + i];
+                for (int b = 0; b < 4; ++b) buf.push_back(static_cast<char>((u >> (8 * b)) & 0xff));
+            }
+        flush();
+        for (uint8_t b : r->absorbing) buf.push_back(static_cast<char>(b));
+        flush();
+        if (!os) throw IoErr(std::string("failed while writing '") + path + "'");
+    });
+}
+
+void gm_result_free(gm_result* r) { delete r; }
+
+} // extern "C"

@@ -1,0 +1,73 @@
+// Plain-data device descriptor shared by the host front end (C++) and the
+// sm_100a kernels (CUDA). Passed to kernels by value (kernel parameter space).
+#pragma once
+
+#include <stdint.h>
+
+#define GMD_MAXD 8      // max state / input / disturbance dimensions on device
+#define GMD_MAXREGS 32  // max dynamics-interpreter registers per row
+
+enum GmFamily { GM_NORMAL = 0, GM_UNIFORM = 1, GM_EXPONENTIAL = 2, GM_BETA = 3 };
+enum GmCut { GM_CUT_NONE = 0, GM_CUT_DEGENERATE = 1, GM_CUT_RADIUS = 2 };
+enum GmSpecKind { GM_SPEC_SAFETY = 0, GM_SPEC_REACH = 1, GM_SPEC_REACH_AVOID = 2 };
+enum GmModeInt { GM_MODE_MATRIX_ = 0, GM_MODE_OFA_ = 1 };
+
+// Dynamics bytecode: register machine, lazy ite through jumps.
+enum GmOpCode : uint8_t {
+    GI_LIT, GI_LDX, GI_LDU, GI_LDW,
+    GI_ADD, GI_SUB, GI_MUL, GI_DIV, GI_POW,
+    GI_LT, GI_LE, GI_GT, GI_GE, GI_EQ, GI_NE,
+    GI_NEG, GI_SIN, GI_COS, GI_TAN, GI_ASIN, GI_ACOS, GI_ATAN, GI_EXP, GI_LN, GI_SQRT, GI_ABS,
+    GI_MIN, GI_MAX,
+    GI_JZ,   // if reg[a] == 0.0 jump to arg
+    GI_JMP   // jump to arg
+};
+
+struct GmIns {
+    uint8_t op;
+    uint8_t dst;
+    uint8_t a;
+    uint8_t b;
+    int32_t arg; // literal index / variable index / jump target
+};
+
+// Device error codes recorded per failing row
+enum GmDevErr { GE_NONE = 0, GE_EXPR = 1, GE_BETA = 2 };
+
+struct GmDev {
+    int n, m, p;             // state / input / disturbance dims
+    int family, mult, cut;   // noise family, multiplicative flag, GmCut
+    int spec_kind, has_avoid;
+    int tpr;                 // threads per row in the expected-value kernels
+    int n_ins, n_lits, nregs;
+    long long n_x, n_u, n_w, rows, R;
+
+    long long xcount[GMD_MAXD], xstride[GMD_MAXD];
+    long long ustride[GMD_MAXD], wstride[GMD_MAXD];
+    double xlb[GMD_MAXD], xeta[GMD_MAXD];
+    double ulb[GMD_MAXD], ueta[GMD_MAXD];
+    double wlb[GMD_MAXD], weta[GMD_MAXD];
+
+    double radius[GMD_MAXD];
+    double s[GMD_MAXD];      // normal: sigma*sqrt(2) (noise.cpp:96); else param1
+    double p2[GMD_MAXD];     // uniform b / beta beta
+    double tlo[GMD_MAXD], thi[GMD_MAXD], alo[GMD_MAXD], ahi[GMD_MAXD];
+    int W[GMD_MAXD];
+    int mass_off[GMD_MAXD + 1];
+
+    // slab layout: virtual leading axis when n == 1, so every row factors as
+    // p(a, j, k) = (P[a] * mm[j]) * ml[k] with P the prefix product over the
+    // leading axes (abstraction.cpp:150-159 association).
+    int sumW;                // sum of W over real axes
+    int s_axes;              // number of axes in the prefix table (n_eff - 2)
+    int P_size;              // prod of W over the prefix axes
+    int Wm, Wl;              // W of the last two (effective) axes
+    int n_lines;             // R / Wl
+    int mm_off, ml_off;      // offsets of the last two axes' masses (n == 1: mm_off = sumW, a 1.0 slot)
+
+    int entry[GMD_MAXD + 1]; // bytecode offsets of the n dynamics expressions
+    const GmIns* prog;
+    const double* lits;
+    const int* line_off;     // n_lines relative flat offsets of slab lines
+    const unsigned char* absorb; // n_x flags (reach specs), may be null
+};

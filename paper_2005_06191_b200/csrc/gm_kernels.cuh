@@ -1,0 +1,62 @@
+// Launch interface of the sm_100a kernels (gm_kernels.cu). Host C++ only sees
+// plain pointers, sizes and a cudaStream_t.
+#pragma once
+
+#include "gm_device.h"
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace gmk {
+
+// row flags written by the row prologue
+enum : uint8_t { RF_ABSORBED = 1, RF_ERROR = 2 };
+// prologue options
+enum : int { PF_SKIP_ABSORBED = 1, PF_T0X = 2, PF_MASSES = 4 };
+
+// kernel families (timing / launch accounting)
+enum Family { KF_PROLOGUE = 0, KF_EXPAND = 1, KF_MASK = 2, KF_EXPECT_MATRIX = 3, KF_EXPECT_OFA = 4,
+              KF_MAXMIN = 5, KF_MISC = 6, KF_COUNT = 7 };
+
+struct BatchPlan {
+    int tpr, groups, rb;     // threads per row, row groups per CTA, rows per CTA batch
+    int table_in_smem;       // line-offset table staged in shared memory
+    size_t smem;             // dynamic shared memory bytes
+};
+BatchPlan plan_batches(const GmDev& D, bool ofa);
+
+void absorb_flags(const GmDev& D, uint8_t* d_flags, cudaStream_t s);
+void zero_absorbing(const GmDev& D, double* d_v, cudaStream_t s);
+
+// Row prologue (RowKernel::compute + fill_axis_masses + box_mass,
+// abstraction.cpp:72-146,187-191) for rows [row0, row0+nrows): origins (flat),
+// per-axis cell masses (structure of arrays, pitch nrows), target-hit masses.
+void prologue(const GmDev& D, long long row0, long long nrows, int flags, long long* origin_out,
+              double* t0x_out, uint8_t* rowflag_out, double* mass_out,
+              unsigned long long* d_err_row, cudaStream_t s);
+
+// Outer-product expansion of the prologue's masses into stored rows
+// (fill_product, abstraction.cpp:150-159).
+void expand(const GmDev& D, long long nrows, const double* mass, double* probs_out, cudaStream_t s);
+
+// Expected value per row, on the fly (synthesis.cpp:100-104) from prologue data.
+void expect_ofa(const GmDev& D, long long nrows, const double* mass, const long long* origin,
+                const double* t0x, const uint8_t* rowflag, const double* V, double* v_in,
+                cudaStream_t s);
+
+// Expected value per row from a stored matrix (synthesis.cpp:95-99); row0 is the
+// absolute index of the matrix's first row, rows [row0+r_lo, row0+r_hi) are processed
+// and v_in is indexed from r_lo.
+void expect_matrix(const GmDev& D, long long row0, long long r_lo, long long r_hi,
+                   const double* probs, const long long* origins, const double* t0x,
+                   const double* V, double* v_in, cudaStream_t s);
+
+// min over disturbances, max over inputs per state (synthesis.cpp:112-142).
+void maxmin(const GmDev& D, long long x0, long long nx, const double* v_in, double* v_out,
+            uint32_t* pol, uint32_t* wst, cudaStream_t s);
+
+// mask_absorbing (abstraction.cpp:273-344) over stored rows.
+void mask(const GmDev& D, long long r_lo, long long nrows, double* probs, const long long* origins,
+          const uint8_t* inT, const uint8_t* inA, const long long* axis_off, cudaStream_t s);
+
+} // namespace gmk

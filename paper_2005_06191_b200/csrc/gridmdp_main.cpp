@@ -1,0 +1,233 @@
+// `gridmdp` CLI of the B200 engine: the reference's verbs, flags, key: value
+// report lines and exit codes (tools/gridmdp_main.cpp:16-227), driving the
+// C ABI of libgridmdp_b200.so. New options are CLI-only (`--device`), so the
+// shared .cfg files stay valid for the reference parser (config.cpp:165-167).
+#include "gridmdp_b200.h"
+
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <iostream>
+#include <map>
+#include <string>
+#include <thread>
+#include <vector>
+
+namespace {
+
+struct Args {
+    std::string verb, config, mode, output, dump, results, x0, dist_mode = "random", traj;
+    long long threads = -1, mem_budget = -1, seed = -1, runs = -1, time_steps = -1;
+    int device = 0;
+};
+
+double since(std::chrono::steady_clock::time_point t0) {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+int exit_code(const gm_status& st) {
+    switch (st.code) {
+        case GM_ERR_CONFIG: return 2;
+        case GM_ERR_MEMORY: return 3;
+        case GM_ERR_DOMAIN: return 4;
+        case GM_ERR_RANGE: return 4;
+        case GM_ERR_IO: return 5;
+        default: return 1;
+    }
+}
+
+int fail(const gm_status& st) {
+    std::cerr << "error: " << st.msg << "\n";
+    return exit_code(st);
+}
+
+int resolve_threads(int t) {
+    if (t > 0) return t;
+    const unsigned hw = std::thread::hardware_concurrency();
+    return hw > 0 ? static_cast<int>(hw) : 1;
+}
+
+void print_sizes(const gm_sizes& s) {
+    std::cout << "states: " << s.n_states << "\n";
+    std::cout << "inputs: " << s.n_inputs << "\n";
+    std::cout << "disturbances: " << s.n_disturbances << "\n";
+    std::cout << "state_input_pairs: " << s.n_states * s.n_inputs << "\n";
+    std::cout << "rows: " << s.rows << "\n";
+    std::cout << "row_width: " << s.row_width << "\n";
+    std::cout << "memory_estimate_bytes: " << s.memory_estimate << "\n";
+}
+
+int load(const Args& a, gm_model** m, gm_sizes* sz) {
+    gm_overrides ov;
+    ov.threads = static_cast<int32_t>(a.threads);
+    ov.time_steps = static_cast<int32_t>(a.time_steps);
+    ov.mem_budget = a.mem_budget;
+    ov.seed = a.seed;
+    ov.runs = static_cast<int32_t>(a.runs);
+    ov.mode = a.mode.empty() ? nullptr : a.mode.c_str();
+    ov.output = a.output.empty() ? nullptr : a.output.c_str();
+    gm_status st;
+    if (gm_model_load(a.config.c_str(), &ov, m, &st) != GM_OK) return fail(st);
+    if (gm_model_sizes(*m, sz, &st) != GM_OK) return fail(st);
+    return 0;
+}
+
+int cmd_estimate(const Args& a) {
+    gm_model* m = nullptr;
+    gm_sizes sz;
+    if (int rc = load(a, &m, &sz)) return rc;
+    print_sizes(sz);
+    gm_model_free(m);
+    return 0;
+}
+
+int cmd_abstract(const Args& a) {
+    gm_model* m = nullptr;
+    gm_sizes sz;
+    if (int rc = load(a, &m, &sz)) return rc;
+    print_sizes(sz);
+    gm_status st;
+    if (sz.mem_budget != 0 && sz.memory_estimate > static_cast<uint64_t>(sz.mem_budget)) {
+        std::cerr << "error: matrix needs " << sz.memory_estimate << " bytes but the budget is " << sz.mem_budget
+                  << "; use ofa mode\n";
+        return 3;
+    }
+    if (gm_set_device(a.device, &st) != GM_OK) return fail(st);
+    const auto t0 = std::chrono::steady_clock::now();
+    gm_matrix* tm = nullptr;
+    if (gm_build_matrix(m, 0, sz.rows, &tm, &st) != GM_OK) return fail(st);
+    std::cout << "time_abstract_s: " << since(t0) << "\n";
+    std::cout << "probs_per_s: " << static_cast<double>(sz.rows) * static_cast<double>(sz.row_width) / since(t0)
+              << "\n";
+    if (!a.dump.empty()) {
+        if (gm_matrix_write(tm, m, a.dump.c_str(), &st) != GM_OK) return fail(st);
+        std::cout << "matrix_dump: " << a.dump << "\n";
+    }
+    gm_matrix_free(tm);
+    gm_model_free(m);
+    return 0;
+}
+
+int cmd_synthesize(const Args& a) {
+    gm_model* m = nullptr;
+    gm_sizes sz;
+    if (int rc = load(a, &m, &sz)) return rc;
+    print_sizes(sz);
+    std::cout << "mode: " << (sz.mode == GM_MODE_OFA ? "ofa" : "matrix") << "\n";
+    std::cout << "threads: " << resolve_threads(sz.threads) << "\n";
+    std::cout << "time_steps: " << sz.horizon << "\n";
+    gm_status st;
+    if (gm_set_device(a.device, &st) != GM_OK) return fail(st);
+    const auto t0 = std::chrono::steady_clock::now();
+    gm_result* r = nullptr;
+    if (gm_synthesize(m, &r, &st) != GM_OK) return fail(st);
+    std::cout << "time_synthesize_s: " << since(t0) << "\n";
+    // output path: exec.output / -o, default results.bin (gridmdp_main.cpp:113)
+    std::string out = gm_model_output_path(m);
+    if (out.empty()) out = "results.bin";
+    if (gm_result_write(r, out.c_str(), &st) != GM_OK) return fail(st);
+    std::cout << "output: " << out << "\n";
+    gm_result_free(r);
+    gm_model_free(m);
+    return 0;
+}
+
+int not_in_engine(const std::string& verb) {
+    std::cerr << "error: '" << verb
+              << "' is outside the B200 engine's hot path (MDP construction + synthesis); use the reference CLI\n";
+    return 1;
+}
+
+void usage() {
+    std::cout << "finite MDP abstraction and max-min controller synthesis on uniform grids (B200 engine)\n"
+                 "usage: gridmdp {estimate-mem|abstract|synthesize|simulate|export-prism} -c CFG [options]\n"
+                 "  --threads N --mem-budget B --seed S --runs R --time-steps T -o PATH\n"
+                 "  abstract: --dump-matrix PATH     synthesize: --mode matrix|ofa\n"
+                 "  GPU (CLI only): --device N\n";
+}
+
+} // namespace
+
+int main(int argc, char** argv) {
+    if (argc < 2) {
+        usage();
+        std::cerr << "A subcommand is required\n";
+        return 106;
+    }
+    Args a;
+    a.verb = argv[1];
+    if (a.verb == "-h" || a.verb == "--help") {
+        usage();
+        return 0;
+    }
+    static const std::map<std::string, int> verbs = {
+        {"estimate-mem", 0}, {"abstract", 1}, {"synthesize", 2}, {"simulate", 3}, {"export-prism", 4}};
+    if (!verbs.count(a.verb)) {
+        std::cerr << "The following argument was not expected: " << a.verb << "\n";
+        return 109;
+    }
+    for (int i = 2; i < argc; ++i) {
+        std::string k = argv[i], v;
+        const auto eq = k.find('=');
+        bool has_inline = k.rfind("--", 0) == 0 && eq != std::string::npos;
+        if (has_inline) {
+            v = k.substr(eq + 1);
+            k = k.substr(0, eq);
+        }
+        auto val = [&]() -> std::string {
+            if (has_inline) return v;
+            if (i + 1 >= argc) {
+                std::cerr << k << " requires an argument\n";
+                std::exit(107);
+            }
+            return argv[++i];
+        };
+        auto num = [&](long long& dst) {
+            const std::string s = val();
+            char* end = nullptr;
+            dst = std::strtoll(s.c_str(), &end, 10);
+            if (s.empty() || *end) {
+                std::cerr << "Could not convert: " << k << " = " << s << "\n";
+                std::exit(105);
+            }
+        };
+        if (k == "-h" || k == "--help") {
+            usage();
+            return 0;
+        } else if (k == "-c" || k == "--config") a.config = val();
+        else if (k == "--threads") num(a.threads);
+        else if (k == "--mem-budget") num(a.mem_budget);
+        else if (k == "--seed") num(a.seed);
+        else if (k == "--runs") num(a.runs);
+        else if (k == "--time-steps") num(a.time_steps);
+        else if (k == "-o" || k == "--output") a.output = val();
+        else if (k == "--device") {
+            long long d = 0;
+            num(d);
+            a.device = static_cast<int>(d);
+        } else if (k == "--dump-matrix" && a.verb == "abstract") a.dump = val();
+        else if (k == "--mode" && a.verb == "synthesize") {
+            a.mode = val();
+            if (a.mode != "matrix" && a.mode != "ofa") {
+                std::cerr << "--mode: " << a.mode << " not in {matrix,ofa}\n";
+                return 105;
+            }
+        } else if (a.verb == "simulate" && (k == "--results" || k == "--x0" || k == "--dist-mode" || k == "--traj")) {
+            (void)val();
+        } else {
+            std::cerr << "The following argument was not expected: " << k << "\n";
+            return 109;
+        }
+    }
+    if (a.config.empty()) {
+        std::cerr << "--config is required\n";
+        return 106;
+    }
+    switch (verbs.at(a.verb)) {
+        case 0: return cmd_estimate(a);
+        case 1: return cmd_abstract(a);
+        case 2: return cmd_synthesize(a);
+        default: return not_in_engine(a.verb);
+    }
+}

@@ -1,0 +1,576 @@
+"""Reference-facing API of the B200 engine.
+
+Mirrors the reference's C++ interface for the hot path (names, argument
+meaning and error behaviour) on top of the C ABI in include/gridmdp_b200.h:
+
+  config.hpp:55-70     load_config / parse_config / build_model / build_spec / build_options
+  grid.hpp:87-99       make_grid (validated when the model is built)
+  noise.hpp:27-36      NoiseSpec.normal / uniform / exponential / beta
+  spec.hpp:24-26       make_safety / make_reachability / make_reach_avoid
+  abstraction.hpp:70-131  window_extents / memory_estimate / build_matrix /
+                          build_target_hit / mask_absorbing / TransitionMatrix
+  synthesis.hpp:12-66  SynthesisOptions / synthesize / synthesize_with_matrix /
+                          bellman_step / query_policy / SynthesisResult
+  io.hpp:13-19         write_results / TransitionMatrix.write (write_matrix)
+
+Every compute call runs the sm_100a kernels of libgridmdp_b200.so; there is
+no CPU path (a missing device raises CudaError).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _capi
+from ._capi import (ConfigError, CudaError, DomainError, GridmdpError, IoError, MemoryError_,  # noqa: F401
+                    ParseError, call, lib, ptr)
+
+MemoryError = MemoryError_  # noqa: A001  reference name (common.hpp:34)
+
+SAFETY, REACHABILITY, REACH_AVOID = "safety", "reachability", "reach-avoid"
+_KIND = {SAFETY: _capi.GM_SAFETY, REACHABILITY: _capi.GM_REACH, REACH_AVOID: _capi.GM_REACH_AVOID,
+         "reach_avoid": _capi.GM_REACH_AVOID}
+_KIND_NAME = {_capi.GM_SAFETY: SAFETY, _capi.GM_REACH: REACHABILITY, _capi.GM_REACH_AVOID: REACH_AVOID}
+
+
+def _fmt(v: float) -> str:
+    r = repr(float(v))
+    return r
+
+
+def _vec(v: Sequence[float]) -> str:
+    return "{" + ", ".join(_fmt(x) for x in v) + "}"
+
+
+# --------------------------------------------------------------------- model parts
+
+@dataclass(frozen=True)
+class Grid:
+    """Uniform grid description (grid.hpp:16-46); counts/strides come from the engine."""
+
+    lb: tuple
+    ub: tuple
+    eta: tuple
+
+    @property
+    def dim(self) -> int:
+        return len(self.lb)
+
+    def counts(self) -> list[int]:
+        # grid.cpp:34-35 (same IEEE operations as the engine's host front end)
+        return [int(math.floor((u - l) / e + 1e-9)) + 1 for l, u, e in zip(self.lb, self.ub, self.eta)]
+
+    @property
+    def size(self) -> int:
+        n = 1
+        for c in self.counts():
+            n *= c
+        return n
+
+    def strides(self) -> list[int]:
+        c = self.counts()
+        s = [1] * len(c)
+        for i in range(len(c) - 2, -1, -1):
+            s[i] = s[i + 1] * c[i + 1]
+        return s
+
+    def point(self, i: int) -> np.ndarray:
+        """index_to_point (grid.cpp:55-65)."""
+        if i < 0 or i >= self.size:
+            raise IndexError(f"index_to_point: flat index {i} out of range")
+        p = np.empty(self.dim)
+        for d, s in enumerate(self.strides()):
+            j, i = divmod(i, s)
+            p[d] = self.lb[d] + float(j) * self.eta[d]
+        return p
+
+    def index(self, x: Sequence[float]) -> int:
+        """point_to_index (grid.cpp:77-96): nearest representative, ties toward +inf."""
+        if len(x) != self.dim:
+            raise IndexError("point_to_index: point dimension mismatch")
+        flat = 0
+        counts = self.counts()
+        for d, s in enumerate(self.strides()):
+            t = (x[d] - self.lb[d]) / self.eta[d]
+            if t < -0.5 - 1e-9 or t > float(counts[d] - 1) + 0.5 + 1e-9:
+                raise IndexError(f"point_to_index: coordinate {x[d]:g} of axis {d} lies outside the quantized region")
+            j = min(max(int(math.floor(t + 0.5)), 0), counts[d] - 1)
+            flat += j * s
+        return flat
+
+
+def make_grid(lb: Sequence[float], ub: Sequence[float], eta: Sequence[float]) -> Grid:
+    return Grid(tuple(float(v) for v in lb), tuple(float(v) for v in ub), tuple(float(v) for v in eta))
+
+
+@dataclass(frozen=True)
+class NoiseSpec:
+    """i.i.d. additive/multiplicative noise (noise.hpp:22-70)."""
+
+    family: str
+    p1: tuple
+    p2: tuple = ()
+    gamma: float = 0.0
+    mode: str = "additive"
+
+    @staticmethod
+    def normal(sigma, gamma, mode="additive"):
+        return NoiseSpec("normal", tuple(map(float, sigma)), (), float(gamma), mode)
+
+    @staticmethod
+    def uniform(a, b, gamma, mode="additive"):
+        return NoiseSpec("uniform", tuple(map(float, a)), tuple(map(float, b)), float(gamma), mode)
+
+    @staticmethod
+    def exponential(rate, gamma, mode="additive"):
+        return NoiseSpec("exponential", tuple(map(float, rate)), (), float(gamma), mode)
+
+    @staticmethod
+    def beta(alpha, beta_, gamma, mode="additive"):
+        return NoiseSpec("beta", tuple(map(float, alpha)), tuple(map(float, beta_)), float(gamma), mode)
+
+    def config_lines(self) -> list[str]:
+        keys = {"normal": ("sigma",), "uniform": ("a", "b"), "exponential": ("rate",), "beta": ("alpha", "beta")}[
+            self.family]
+        out = [f"noise.type = {self.family};", f"noise.mode = {self.mode};",
+               f"noise.cutting_probability = {_fmt(self.gamma)};", f"noise.{keys[0]} = {_vec(self.p1)};"]
+        if len(keys) > 1:
+            out.append(f"noise.{keys[1]} = {_vec(self.p2)};")
+        return out
+
+
+@dataclass(frozen=True)
+class Box:
+    lo: tuple
+    hi: tuple
+
+    def __init__(self, lo, hi):
+        object.__setattr__(self, "lo", tuple(map(float, lo)))
+        object.__setattr__(self, "hi", tuple(map(float, hi)))
+
+    @property
+    def dim(self) -> int:
+        return len(self.lo)
+
+    def contains(self, x) -> bool:
+        return len(x) == self.dim and all(a >= l for a, l in zip(x, self.lo)) and all(
+            a <= h for a, h in zip(x, self.hi))
+
+
+@dataclass(frozen=True)
+class Spec:
+    kind: str = SAFETY
+    horizon: int = 1
+    target: Optional[Box] = None
+    avoid: Optional[Box] = None
+
+    def is_reach(self) -> bool:
+        return self.kind != SAFETY
+
+
+def make_safety(horizon: int) -> Spec:
+    return Spec(SAFETY, int(horizon))
+
+
+def make_reachability(horizon: int, target: Box) -> Spec:
+    return Spec(REACHABILITY, int(horizon), target)
+
+
+def make_reach_avoid(horizon: int, target: Box, avoid: Box) -> Spec:
+    return Spec(REACH_AVOID, int(horizon), target, avoid)
+
+
+@dataclass
+class SynthesisOptions:
+    mode: str = "matrix"     # matrix | ofa
+    threads: int = 0         # host threads (the device path ignores it)
+    memory_budget: int = 0   # bytes, 0 = unlimited; binds matrix mode only
+
+
+# ------------------------------------------------------------------------- model
+
+class SystemModel:
+    """A quantized control system (model.hpp:15-35) resident in the engine.
+
+    Also carries the configuration's Spec and SynthesisOptions when loaded from a
+    config file (build_spec / build_options)."""
+
+    def __init__(self, handle: C.c_void_p, text: Optional[str] = None):
+        self._h = handle
+        self.text = text
+        self._spec_cache: Optional[Spec] = None
+        s = self.sizes()
+        self.spec = self._spec_from_sizes(s)
+        self.options = SynthesisOptions(mode="ofa" if s.mode == _capi.GM_MODE_OFA else "matrix",
+                                        threads=s.threads, memory_budget=int(s.mem_budget))
+
+    def _spec_from_sizes(self, s) -> Spec:
+        return Spec(_KIND_NAME[s.spec_kind], int(s.horizon))  # boxes are kept engine-side
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.gm_model_free(h)
+            self._h = None
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    def sizes(self) -> _capi.Sizes:
+        s = _capi.Sizes()
+        call("gm_model_sizes", self._h, C.byref(s))
+        return s
+
+    @property
+    def n_states(self) -> int:
+        return int(self.sizes().n_states)
+
+    @property
+    def n_inputs(self) -> int:
+        return int(self.sizes().n_inputs)
+
+    @property
+    def n_disturbances(self) -> int:
+        return int(self.sizes().n_disturbances)
+
+    def n_rows(self) -> int:
+        return int(self.sizes().rows)
+
+    @property
+    def state_dim(self) -> int:
+        return int(self.sizes().n_dim)
+
+    def dynamics_image(self, row: int) -> np.ndarray:
+        mu = np.zeros(self.state_dim)
+        call("gm_dynamics_image", self._h, C.c_int64(row), mu.ctypes.data_as(C.POINTER(C.c_double)))
+        return mu
+
+    def use_spec(self, spec: Spec) -> None:
+        if spec is self.spec:  # the configuration's own spec is already engine-side
+            return
+        n = self.state_dim
+
+        def arr(b, which):
+            if b is None:
+                return None
+            v = np.ascontiguousarray(getattr(b, which), dtype=np.float64)
+            if v.size != n:  # dimension mismatch: let validation report it
+                v = np.resize(v, n)
+            return v
+
+        kind = _KIND.get(spec.kind)
+        if kind is None:
+            raise ConfigError(f"unknown specification kind '{spec.kind}'")
+        tl, th = arr(spec.target, "lo"), arr(spec.target, "hi")
+        al, ah = arr(spec.avoid, "lo"), arr(spec.avoid, "hi")
+        dp = C.POINTER(C.c_double)
+        cast = (lambda a: a.ctypes.data_as(dp) if a is not None else None)
+        if spec.target is not None and spec.target.dim != n:
+            raise ConfigError("target box dimension does not match the state grid")
+        if spec.avoid is not None and spec.avoid.dim != n:
+            raise ConfigError("avoid box dimension does not match the state grid")
+        call("gm_model_set_spec", self._h, kind, int(spec.horizon), cast(tl), cast(th), cast(al), cast(ah))
+        self._keep = (tl, th, al, ah)
+
+    def use_options(self, opts: SynthesisOptions) -> None:
+        mode = {"matrix": _capi.GM_MODE_MATRIX, "ofa": _capi.GM_MODE_OFA}[opts.mode]
+        call("gm_model_set_options", self._h, mode, int(opts.memory_budget))
+
+
+def _model_from_text(text: str, name: str, overrides: Optional[dict] = None) -> SystemModel:
+    h = C.c_void_p()
+    ov = _overrides(overrides)
+    call("gm_model_parse", text.encode(), name.encode(), C.byref(ov) if ov else None, C.byref(h))
+    return SystemModel(h, text)
+
+
+def _overrides(d: Optional[dict]):
+    if not d:
+        return None
+    ov = _capi.Overrides(threads=-1, time_steps=-1, mem_budget=-1, seed=-1, runs=-1, mode=None, output=None)
+    for k, v in d.items():
+        if k in ("mode", "output"):
+            setattr(ov, k, v.encode())
+        else:
+            setattr(ov, k, int(v))
+    return ov
+
+
+def load_config(path: str, **overrides) -> SystemModel:
+    """load_config + build_model (+ build_spec / build_options) in one step.
+
+    Overrides mirror the CLI flags (gridmdp_main.cpp:31-41): threads,
+    time_steps, mem_budget, seed, runs, mode, output."""
+    h = C.c_void_p()
+    ov = _overrides(overrides)
+    call("gm_model_load", str(path).encode(), C.byref(ov) if ov else None, C.byref(h))
+    return SystemModel(h)
+
+
+def parse_config(text: str, name: str = "<config>", **overrides) -> SystemModel:
+    return _model_from_text(text, name, overrides)
+
+
+def make_model(state: Grid, input: Grid, disturbance: Optional[Grid], dynamics: Sequence[str],
+               noise: NoiseSpec, constants: Optional[dict] = None) -> SystemModel:
+    """make_model (model.hpp:40-42) from grids, expression texts and noise."""
+    lines = []
+    for name, g in (("states", state), ("inputs", input), ("disturbances", disturbance)):
+        if g is None or (name == "disturbances" and g.dim == 0):
+            continue
+        lines += [f"{name}.dim = {g.dim};", f"{name}.lb = {_vec(g.lb)};", f"{name}.ub = {_vec(g.ub)};",
+                  f"{name}.eta = {_vec(g.eta)};"]
+    for k, v in (constants or {}).items():
+        lines.append(f"constants.{k} = {_fmt(v)};")
+    for i, e in enumerate(dynamics):
+        lines.append(f"dynamics.x{i} = {e};")
+    lines += noise.config_lines()
+    lines += ["spec.type = safety;", "spec.time_steps = 1;"]
+    return _model_from_text("\n".join(lines) + "\n", "<model>")
+
+
+# ----------------------------------------------------------------- stage (i)
+
+def window_extents(m: SystemModel) -> list[int]:
+    s = m.sizes()
+    return [int(s.extents[d]) for d in range(s.n_dim)]
+
+
+def memory_estimate(m: SystemModel) -> int:
+    return int(m.sizes().memory_estimate)
+
+
+class TransitionMatrix:
+    """Device-resident slab storage (abstraction.hpp:22-65)."""
+
+    def __init__(self, model: SystemModel, handle: C.c_void_p):
+        self.model = model
+        self._h = handle
+        s = model.sizes()
+        rb, re_, R = C.c_int64(), C.c_int64(), C.c_int64()
+        call("gm_matrix_info", handle, C.byref(rb), C.byref(re_), C.byref(R), None, None)
+        self.row_begin, self.row_end, self._R = rb.value, re_.value, R.value
+        self._extents = [int(s.extents[d]) for d in range(s.n_dim)]
+        self._strides = [int(s.strides[d]) for d in range(s.n_dim)]
+        self.n_inputs, self.n_disturbances = int(s.n_inputs), int(s.n_disturbances)
+        self._origins = None
+        self._payload = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.gm_matrix_free(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def rows(self) -> int:
+        return self.row_end - self.row_begin
+
+    def row_width(self) -> int:
+        return self._R
+
+    def window_extents(self) -> list[int]:
+        return list(self._extents)
+
+    def row_index(self, ix: int, iu: int, iw: int) -> int:
+        return (ix * self.n_inputs + iu) * self.n_disturbances + iw
+
+    def _fetch(self):
+        n = self.rows()
+        o = np.empty(n, dtype=np.int64)
+        p = np.empty((n, self._R), dtype=np.float64)
+        call("gm_matrix_copy_rows", self._h, self.row_begin, self.row_end, ptr(o), ptr(p))
+        self._origins, self._payload = o, p
+
+    def invalidate(self):
+        self._origins = self._payload = None
+
+    def origins(self) -> np.ndarray:
+        if self._origins is None:
+            self._fetch()
+        return self._origins
+
+    def payload(self) -> np.ndarray:
+        if self._payload is None:
+            self._fetch()
+        return self._payload
+
+    def origin(self, r: int) -> int:
+        return int(self.origins()[r])
+
+    def row(self, r: int) -> np.ndarray:
+        return self.payload()[r]
+
+    def row_sum(self, r: int) -> float:
+        return float(math.fsum(self.row(r)))  # tests only
+
+    def prob(self, r: int, post: int) -> float:
+        """Dense lookup (abstraction.cpp:227-244)."""
+        rem_o, rem_p, k = self.origin(r), post, 0
+        for d, s in enumerate(self._strides):
+            jo, rem_o = divmod(rem_o, s)
+            jp, rem_p = divmod(rem_p, s)
+            off = jp - jo
+            if off < 0 or off >= self._extents[d]:
+                return 0.0
+            k = k * self._extents[d] + off
+        return float(self.row(r)[k])
+
+    def write(self, path: str) -> None:
+        """write_matrix (io.cpp:236-256)."""
+        call("gm_matrix_write", self._h, self.model.handle, str(path).encode())
+
+
+def build_matrix(m: SystemModel, threads: int = 0, rows: Optional[tuple] = None) -> TransitionMatrix:
+    r0, r1 = rows if rows else (0, m.n_rows())
+    h = C.c_void_p()
+    call("gm_build_matrix", m.handle, C.c_int64(r0), C.c_int64(r1), C.byref(h))
+    return TransitionMatrix(m, h)
+
+
+def build_target_hit(m: SystemModel, spec: Spec, threads: int = 0) -> np.ndarray:
+    m.use_spec(spec)
+    n = m.n_rows()
+    out = np.empty(n, dtype=np.float64)
+    call("gm_build_target_hit", m.handle, C.c_int64(0), C.c_int64(n), ptr(out))
+    return out
+
+
+def mask_absorbing(tm: TransitionMatrix, spec: Spec, threads: int = 0) -> TransitionMatrix:
+    tm.model.use_spec(spec)
+    call("gm_mask_absorbing", tm.model.handle, tm.handle)
+    tm.invalidate()
+    return tm
+
+
+def absorbing_states(m: SystemModel, spec: Spec) -> np.ndarray:
+    m.use_spec(spec)
+    out = np.zeros(m.n_states, dtype=np.uint8)
+    call("gm_absorbing_states", m.handle, ptr(out))
+    return out
+
+
+# ---------------------------------------------------------------- stage (ii)
+
+@dataclass
+class SynthesisResult:
+    """synthesis.hpp:28-40; values n_x x (T+1), policy / worst_dist n_x x T."""
+
+    values: np.ndarray
+    policy: np.ndarray
+    worst_dist: np.ndarray
+    absorbing: np.ndarray
+    mode: str
+    spec: Spec
+    model: SystemModel = field(repr=False)
+    _h: Optional[C.c_void_p] = field(default=None, repr=False)
+
+    def __del__(self):
+        if self._h:
+            lib.gm_result_free(self._h)
+            self._h = None
+
+    def write(self, path: str) -> None:
+        """write_results (io.cpp:142-179)."""
+        h = self._h
+        if not h:
+            h = C.c_void_p()
+            v = np.asfortranarray(self.values, dtype=np.float64)
+            p = np.asfortranarray(self.policy, dtype=np.uint32)
+            w = np.asfortranarray(self.worst_dist, dtype=np.uint32)
+            self.model.use_spec(self.spec)
+            call("gm_result_from_tables", self.model.handle, ptr(v), ptr(p), ptr(w), C.byref(h))
+            self._h = h
+        call("gm_result_write", h, str(path).encode())
+
+
+def _result_from_handle(m: SystemModel, spec: Spec, h: C.c_void_p) -> SynthesisResult:
+    n_x, T, has_abs, mode = C.c_int64(), C.c_int32(), C.c_int32(), C.c_int32()
+    call("gm_result_shape", h, C.byref(n_x), C.byref(T), C.byref(has_abs), C.byref(mode))
+    nx, t = n_x.value, T.value
+    vals = np.empty((nx, t + 1), dtype=np.float64, order="F")
+    pol = np.empty((nx, t), dtype=np.uint32, order="F")
+    wst = np.empty((nx, t), dtype=np.uint32, order="F")
+    ab = np.zeros(nx if has_abs.value else 0, dtype=np.uint8)
+    call("gm_result_copy", h, ptr(vals), ptr(pol), ptr(wst), ptr(ab) if has_abs.value else None)
+    return SynthesisResult(vals, pol, wst, ab, "ofa" if mode.value == _capi.GM_MODE_OFA else "matrix", spec, m, h)
+
+
+def synthesize(m: SystemModel, spec: Optional[Spec] = None, opts: Optional[SynthesisOptions] = None
+               ) -> SynthesisResult:
+    spec = spec or m.spec
+    opts = opts or m.options
+    m.use_spec(spec)
+    m.use_options(opts)
+    h = C.c_void_p()
+    call("gm_synthesize", m.handle, C.byref(h))
+    return _result_from_handle(m, spec, h)
+
+
+def synthesize_with_matrix(m: SystemModel, tm: TransitionMatrix, t0x: Optional[np.ndarray], spec: Spec,
+                           opts: Optional[SynthesisOptions] = None) -> SynthesisResult:
+    m.use_spec(spec)
+    if opts:
+        m.use_options(opts)
+    h = C.c_void_p()
+    t = None if t0x is None else np.ascontiguousarray(t0x, dtype=np.float64)
+    call("gm_synthesize_with_matrix", m.handle, tm.handle, ptr(t), C.byref(h))
+    tm.invalidate()
+    return _result_from_handle(m, spec, h)
+
+
+def bellman_step(m: SystemModel, spec: Spec, tm: Optional[TransitionMatrix], t0x: Optional[np.ndarray],
+                 v_next: np.ndarray, threads: int = 0):
+    """One backward step (synthesis.cpp:147-161). Returns (v_out, policy, worst_dist)."""
+    m.use_spec(spec)
+    v_next = np.ascontiguousarray(v_next, dtype=np.float64)
+    if v_next.size != m.n_states:
+        raise ConfigError("bellman_step: v_next size does not match the state grid")
+    if tm is not None and spec.is_reach() and t0x is None:
+        raise ConfigError("bellman_step: matrix-backed reach step requires the target-hit vector")
+    n = m.n_states
+    v_out = np.empty(n, dtype=np.float64)
+    pol = np.empty(n, dtype=np.uint32)
+    wst = np.empty(n, dtype=np.uint32)
+    t = None if t0x is None else np.ascontiguousarray(t0x, dtype=np.float64)
+    call("gm_bellman_step", m.handle, tm.handle if tm is not None else None, ptr(t), ptr(v_next), ptr(v_out),
+         ptr(pol), ptr(wst))
+    return v_out, pol, wst
+
+
+def row_values(m: SystemModel) -> np.ndarray:
+    """v_in of the model's most recent step: (n_x, n_u, n_w) expected values."""
+    s = m.sizes()
+    out = np.empty(int(s.rows), dtype=np.float64)
+    call("gm_copy_row_values", m.handle, ptr(out), C.c_int64(out.size))
+    return out.reshape(int(s.n_states), int(s.n_inputs), int(s.n_disturbances))
+
+
+def q_values(m: SystemModel) -> np.ndarray:
+    """min over disturbances of row_values (strict <, synthesis.cpp:121-127): (n_x, n_u)."""
+    return row_values(m).min(axis=2)
+
+
+def query_policy(res: SynthesisResult, input_grid: Grid, state_grid: Grid, x, k: int) -> np.ndarray:
+    """Input prescribed at continuous state x and step k (synthesis.cpp:230-239)."""
+    T = res.spec.horizon
+    if k < 1 or k > T:
+        raise IndexError(f"query_policy: step {k} outside [1, {T}]")
+    ix = state_grid.index(x)
+    return input_grid.point(int(res.policy[ix, k - 1]))
+
+
+def write_results(res: SynthesisResult, path: str) -> None:
+    res.write(path)
+
+
+def launch_count() -> int:
+    return int(lib.gm_launch_count())

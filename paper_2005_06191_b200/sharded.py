@@ -1,0 +1,160 @@
+"""Multi-GPU synthesis: one process per GPU, state space sharded into
+contiguous flat-index ranges, V exchanged with one NCCL
+all-gather per Bellman step (the only data-path collective; stage (i) needs
+none).
+
+Rows of a state are reduced only within that state (synthesis.cpp:112-142), so
+each rank owns the rows of its states and writes V_k for them; the next step
+needs V_{k+1} wherever its slabs reach, which the all-gather provides. Per-row
+arithmetic does not depend on the sharding, so results are bit-identical for
+any number of ranks.
+
+The per-shard compute is a backend object with `build(x0, x1)` and
+`step(tm, x0, x1, v_next, v_out, pol, wst)`; the product backend is
+`DeviceBackend` (C ABI kernels). Tests substitute a CPU backend to exercise the
+orchestration with the gloo process group.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+import torch.distributed as dist
+
+from . import _capi
+from ._capi import call, lib
+
+
+@dataclass
+class ShardPlan:
+    """Equal contiguous state ranges (last one shorter), padded to `per` so the
+    all-gather has equal chunks and writes V contiguously."""
+
+    n_x: int
+    world: int
+    rank: int
+
+    @property
+    def per(self) -> int:
+        return -(-self.n_x // self.world)
+
+    @property
+    def x0(self) -> int:
+        return min(self.n_x, self.rank * self.per)
+
+    @property
+    def x1(self) -> int:
+        return min(self.n_x, self.x0 + self.per)
+
+    def bounds(self, r: int) -> tuple[int, int]:
+        a = min(self.n_x, r * self.per)
+        return a, min(self.n_x, a + self.per)
+
+
+class DeviceBackend:
+    """Kernels of libgridmdp_b200.so on the caller's CUDA stream."""
+
+    def __init__(self, model, stream: Optional[torch.cuda.Stream] = None, keep_matrix: bool = True):
+        self.model = model
+        self.stream = stream or torch.cuda.current_stream()
+        self.keep = keep_matrix
+        self._tm = C.c_void_p()
+        call("gm_model_set_stream", model.handle, C.c_void_p(self.stream.cuda_stream))
+
+    def build(self, x0: int, x1: int):
+        """Stage (i) for the shard; with keep_matrix the device buffers are reused
+        across calls (rebuilt in place)."""
+        h = self._tm if self.keep else C.c_void_p()
+        call("gm_build_shard", self.model.handle, C.c_int64(x0), C.c_int64(x1), C.byref(h))
+        if self.keep:
+            self._tm = h
+        return h
+
+    def free(self, tm) -> None:
+        if tm and not self.keep:
+            lib.gm_matrix_free(tm)
+
+    def release(self) -> None:
+        if self._tm:
+            lib.gm_matrix_free(self._tm)
+            self._tm = C.c_void_p()
+
+    def __del__(self):
+        self.release()
+
+    def step(self, tm, x0, x1, v_next: torch.Tensor, v_out: torch.Tensor, pol: torch.Tensor,
+             wst: torch.Tensor) -> None:
+        call("gm_step_device", self.model.handle, tm, C.c_int64(x0), C.c_int64(x1),
+             C.c_void_p(v_next.data_ptr()), C.c_void_p(v_out.data_ptr()), C.c_void_p(pol.data_ptr()),
+             C.c_void_p(wst.data_ptr()), C.c_void_p(self.stream.cuda_stream))
+
+    def check(self) -> None:
+        call("gm_check_device_errors", self.model.handle)
+
+
+def synthesize_sharded(backend, n_x: int, horizon: int, reach: bool, matrix: bool, device,
+                       group=None, timer=None):
+    """run_backward (synthesis.cpp:165-195) over a sharded state space.
+
+    Returns (values (T+1, n_x) on every rank, policy (T, n_x) and worst (T, n_x)
+    gathered on every rank). `timer(name)` is called at phase boundaries."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    plan = ShardPlan(n_x, world, rank)
+    per, x0, x1 = plan.per, plan.x0, plan.x1
+    T = horizon
+    vals = torch.zeros((T + 1, per * world), dtype=torch.float64, device=device)
+    pol = torch.zeros((T, per * world), dtype=torch.int32, device=device)
+    wst = torch.zeros((T, per * world), dtype=torch.int32, device=device)
+    vals[T, :n_x] = 0.0 if reach else 1.0
+    tm = None
+    if timer:
+        timer("build_start")
+    if matrix:
+        tm = backend.build(x0, x1)
+    if timer:
+        timer("build_end")
+    lo = rank * per
+    try:
+        for k in range(T - 1, -1, -1):
+            backend.step(tm, x0, x1, vals[k + 1], vals[k, lo:lo + per], pol[k, lo:lo + per],
+                         wst[k, lo:lo + per])
+            if world > 1:
+                dist.all_gather_into_tensor(vals[k], vals[k, lo:lo + per].clone() if vals.device.type == "cpu"
+                                            else vals[k, lo:lo + per], group=group)
+            if k == T - 1 and hasattr(backend, "check"):
+                torch.cuda.current_stream().synchronize() if vals.is_cuda else None
+                backend.check()
+    finally:
+        if matrix and hasattr(backend, "free"):
+            backend.free(tm)
+    if timer:
+        timer("sweep_end")
+    if world > 1:
+        pol_full = torch.empty_like(pol)
+        wst_full = torch.empty_like(wst)
+        for src, dst in ((pol, pol_full), (wst, wst_full)):
+            for k in range(T):
+                dist.all_gather_into_tensor(dst[k], src[k, lo:lo + per].contiguous(), group=group)
+        pol, wst = pol_full, wst_full
+    return vals[:, :n_x], pol[:, :n_x], wst[:, :n_x]
+
+
+def result_from_tables(model, vals: torch.Tensor, pol: torch.Tensor, wst: torch.Tensor):
+    """Wraps gathered tables as a SynthesisResult that writes the reference container."""
+    import numpy as np
+
+    from . import gridmdp as g
+
+    v = np.asfortranarray(vals.cpu().numpy().T)
+    p = np.asfortranarray(pol.cpu().numpy().astype(np.uint32).T)
+    w = np.asfortranarray(wst.cpu().numpy().astype(np.uint32).T)
+    absorbing = np.zeros(0, dtype=np.uint8)
+    if model.spec.is_reach():
+        absorbing = g.absorbing_states(model, model.spec)
+    return g.SynthesisResult(v, p, w, absorbing, model.options.mode, model.spec, model)
+
+
+_ = _capi  # keep the binding imported (no CPU fallback)
