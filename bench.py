@@ -225,6 +225,8 @@ def main():
         torch.cuda.synchronize()
     launches = lib.gm_launch_count() - launches0
     lib.gm_enable_kernel_timing(0)
+    be.release()  # free the shard's matrix before the end-to-end run allocates its own
+    torch.cuda.empty_cache()
     for ev in evs:
         build_ms.append(ev["build_start"].elapsed_time(ev["build_end"]))
         sweep_ms.append(ev["build_end"].elapsed_time(ev["sweep_end"]))
@@ -245,7 +247,13 @@ def main():
     hbm, peak_kind = peaks()
     dom = "expect_matrix" if matrix else "expect_ofa"
     dom_ms = fam_ms[dom] / max(fam_n[dom], 1)
-    dom_bytes = my_rows * (R * 8 + 8 + (8 if reach else 0))  # algorithmic: T row + origin (+ T0x) per row
+    # algorithmic bytes: per non-absorbed row its stored T row + origin (+ T0x); absorbed
+    # rows are never read (synthesis.cpp:86-89), as in the reference
+    live_rows = my_rows
+    if reach:
+        ab = g.absorbing_states(m, m.spec)[plan.x0:plan.x1]
+        live_rows = int((ab == 0).sum()) * nuw
+    dom_bytes = live_rows * (R * 8 + 8 + (8 if reach else 0))
     roofline = {"kernel": dom, "bound": "hbm", "achieved": dom_bytes / (dom_ms / 1e3) / 1e9, "peak": hbm,
                 "peak_kind": peak_kind, "unit": "GB/s", "traffic": None,
                 "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_ms": dom_ms, "launches": fam_n[dom]}
@@ -253,10 +261,10 @@ def main():
     if not matrix:
         roofline["note"] = "OFA: HBM-equivalent bytes (8 per recomputed term), SURVEY.md §8d"
     exp_ms = fam_ms["expand"] / max(fam_n["expand"], 1)
-    build_bytes = my_rows * (R * 8 + 8)
-    roofline_build = {"kernel": "expand", "bound": "hbm", "achieved": (
-        build_bytes / max(fam_n["expand"], 1)) / (exp_ms / 1e3) / 1e9 if exp_ms > 0 else None, "peak": hbm,
-        "unit": "GB/s"}
+    build_bytes = my_rows * (R * 8 + 8 + (8 if reach else 0))  # rows written + origins (+ T0x)
+    roofline_build = {"kernel": "k_build", "bound": "hbm",
+                      "achieved": build_bytes / (exp_ms / 1e3) / 1e9 if exp_ms > 0 else None, "peak": hbm,
+                      "unit": "GB/s", "algorithmic_bytes_per_launch": build_bytes, "avg_launch_ms": exp_ms}
     if roofline_build["achieved"]:
         roofline_build["frac"] = roofline_build["achieved"] / hbm
 

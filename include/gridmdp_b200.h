@@ -120,8 +120,9 @@ int64_t gm_model_program_size(const gm_model* m);
 /* Selects the CUDA device used by subsequent calls on this host thread. */
 gm_code gm_set_device(int32_t device, gm_status* st);
 /* Makes the model issue all its device work on `stream` (a cudaStream_t of the
- * current device, e.g. the caller's torch stream); NULL restores its own stream. */
-gm_code gm_model_set_stream(gm_model* m, void* stream, gm_status* st);
+ * current device, e.g. the caller's torch stream; NULL is the legacy default
+ * stream). use_own != 0 restores the model's own stream instead. */
+gm_code gm_model_set_stream(gm_model* m, void* stream, int32_t use_own, gm_status* st);
 /* Number of kernel launches issued by this library since load (process-wide). */
 int64_t gm_launch_count(void);
 /* Device time of the last launch of each kernel family, ms (0 if none).

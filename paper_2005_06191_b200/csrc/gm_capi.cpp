@@ -189,9 +189,11 @@ struct gm_model {
     DevBuf<uint8_t> d_absorb;
     DevBuf<unsigned long long> d_err;
     // step scratch
-    DevBuf<double> d_mass, d_t0x, d_vin, d_vtmp;
-    DevBuf<long long> d_origin;
-    DevBuf<uint8_t> d_rowflag;
+    DevBuf<double> d_mass[2], d_t0x[2], d_vin;
+    DevBuf<long long> d_origin[2];
+    DevBuf<uint8_t> d_rowflag[2];
+    cudaStream_t aux = nullptr; // producer stream of the row-prologue pipeline
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_ready[2] = {}, ev_used[2] = {};
     bool dev_ready = false;
     bool absorb_ready = false;
 };
@@ -310,17 +312,51 @@ void raise_device_error(gm_model* m) {
 }
 
 int64_t chunk_rows(const gm_model* m) {
+    // 32 MB of per-axis masses per scratch buffer: two buffers stay L2-resident
+    // next to V while the prologue of chunk c+1 overlaps the consumer of chunk c
     const int64_t per_row = static_cast<int64_t>(m->D.sumW) * 8 + 8 + 8 + 1;
-    int64_t c = (64LL << 20) / std::max<int64_t>(per_row, 1);
+    int64_t c = (32LL << 20) / std::max<int64_t>(per_row, 1);
     c = std::max<int64_t>(c, 4096);
     return c;
 }
 
 void ensure_scratch(gm_model* m, int64_t chunk) {
-    m->d_mass.ensure(static_cast<size_t>(chunk) * std::max(m->D.sumW, 1), "mass scratch");
-    m->d_origin.ensure(static_cast<size_t>(chunk), "origin scratch");
-    m->d_t0x.ensure(static_cast<size_t>(chunk), "t0x scratch");
-    m->d_rowflag.ensure(static_cast<size_t>(chunk), "row flags");
+    for (int b = 0; b < 2; ++b) {
+        m->d_mass[b].ensure(static_cast<size_t>(chunk) * std::max(m->D.sumW, 1), "mass scratch");
+        m->d_origin[b].ensure(static_cast<size_t>(chunk), "origin scratch");
+        m->d_t0x[b].ensure(static_cast<size_t>(chunk), "t0x scratch");
+        m->d_rowflag[b].ensure(static_cast<size_t>(chunk), "row flags");
+    }
+    if (!m->aux) {
+        int lo = 0, hi = 0; // the producer (row prologue) gets the higher priority
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        ck(cudaStreamCreateWithPriority(&m->aux, cudaStreamNonBlocking, hi), "aux stream");
+        for (cudaEvent_t* e : {&m->ev_fork, &m->ev_join, &m->ev_ready[0], &m->ev_ready[1], &m->ev_used[0],
+                               &m->ev_used[1]})
+            ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "pipeline events");
+    }
+}
+
+// Producer/consumer pipeline over row chunks: the row prologue of chunk c runs on
+// the aux stream into scratch buffer c&1 while the consumer of chunk c-1 runs on
+// `s`; `consume(c0, cn, buf)` enqueues the consumer of one chunk on `s`.
+template <class Produce, class Consume>
+void pipeline(gm_model* m, int64_t n, int64_t chunk, cudaStream_t s, Produce&& produce, Consume&& consume) {
+    ck(cudaEventRecord(m->ev_fork, s), "fork");
+    ck(cudaStreamWaitEvent(m->aux, m->ev_fork, 0), "fork");
+    int64_t c = 0;
+    for (int64_t c0 = 0; c0 < n; c0 += chunk, ++c) {
+        const int64_t cn = std::min(chunk, n - c0);
+        const int b = static_cast<int>(c & 1);
+        if (c >= 2) ck(cudaStreamWaitEvent(m->aux, m->ev_used[b], 0), "reuse");
+        produce(c0, cn, b);
+        ck(cudaEventRecord(m->ev_ready[b], m->aux), "ready");
+        ck(cudaStreamWaitEvent(s, m->ev_ready[b], 0), "ready");
+        consume(c0, cn, b);
+        ck(cudaEventRecord(m->ev_used[b], s), "used");
+    }
+    ck(cudaEventRecord(m->ev_join, m->aux), "join");
+    ck(cudaStreamWaitEvent(s, m->ev_join, 0), "join");
 }
 
 // Stage (i) for rows [r0, r1): origins + probabilities (+ T0x for reach shards)
@@ -337,20 +373,9 @@ void build_rows(gm_model* m, int64_t r0, int64_t r1, gm_matrix* tm, bool want_t0
         tm->t0x.ensure(static_cast<size_t>(n), "target-hit vector");
         tm->has_t0x = true;
     }
-    const int64_t chunk = chunk_rows(m);
-    ensure_scratch(m, std::min(chunk, std::max<int64_t>(n, 1)));
-    for (int64_t c0 = 0; c0 < n; c0 += chunk) {
-        const int64_t cn = std::min(chunk, n - c0);
-        {
-            Launch L(gmk::KF_PROLOGUE, m->stream);
-            gmk::prologue(m->D, r0 + c0, cn, gmk::PF_MASSES | (want_t0x ? gmk::PF_T0X : 0),
-                          tm->origins.p + c0, want_t0x ? tm->t0x.p + c0 : nullptr, nullptr, m->d_mass.p,
-                          m->d_err.p, m->stream);
-        }
-        {
-            Launch L(gmk::KF_EXPAND, m->stream);
-            gmk::expand(m->D, cn, m->d_mass.p, tm->probs.p + c0 * m->M.R, m->stream);
-        }
+    {
+        Launch L(gmk::KF_EXPAND, m->stream);
+        gmk::build(m->D, r0, n, tm->origins.p, want_t0x ? tm->t0x.p : nullptr, tm->probs.p, m->d_err.p, m->stream);
     }
     ck(cudaStreamSynchronize(m->stream), "build");
     raise_device_error(m);
@@ -370,24 +395,23 @@ void step_states(gm_model* m, gm_matrix* tm, int64_t x0, int64_t x1, const doubl
         Launch L(gmk::KF_EXPECT_MATRIX, s);
         gmk::expect_matrix(m->D, tm->row_begin, r0 - tm->row_begin, r1 - tm->row_begin, tm->probs.p,
                            tm->origins.p, tm->has_t0x ? tm->t0x.p : nullptr, v_next, m->d_vin.p, s);
-    } else {
-        const int64_t chunk = chunk_rows(m);
-        ensure_scratch(m, std::min(chunk, std::max<int64_t>(n, 1)));
+    } else if (n > 0) {
+        const int64_t chunk = std::min(chunk_rows(m), n);
+        ensure_scratch(m, chunk);
         const bool reach = m->M.spec.reach();
-        for (int64_t c0 = 0; c0 < n; c0 += chunk) {
-            const int64_t cn = std::min(chunk, n - c0);
-            {
-                Launch L(gmk::KF_PROLOGUE, s);
-                gmk::prologue(m->D, r0 + c0, cn,
-                              gmk::PF_SKIP_ABSORBED | gmk::PF_MASSES | (reach ? gmk::PF_T0X : 0),
-                              m->d_origin.p, m->d_t0x.p, m->d_rowflag.p, m->d_mass.p, m->d_err.p, s);
-            }
-            {
+        pipeline(
+            m, n, chunk, s,
+            [&](int64_t c0, int64_t cn, int b) {
+                Launch L(gmk::KF_PROLOGUE, m->aux);
+                gmk::prologue(m->D, r0 + c0, cn, gmk::PF_SKIP_ABSORBED | gmk::PF_MASSES | (reach ? gmk::PF_T0X : 0),
+                              m->d_origin[b].p, m->d_t0x[b].p, m->d_rowflag[b].p, m->d_mass[b].p, m->d_err.p,
+                              m->aux);
+            },
+            [&](int64_t c0, int64_t cn, int b) {
                 Launch L(gmk::KF_EXPECT_OFA, s);
-                gmk::expect_ofa(m->D, cn, m->d_mass.p, m->d_origin.p, m->d_t0x.p, m->d_rowflag.p, v_next,
-                                m->d_vin.p + c0, s);
-            }
-        }
+                gmk::expect_ofa(m->D, cn, m->d_mass[b].p, m->d_origin[b].p, m->d_t0x[b].p, m->d_rowflag[b].p,
+                                v_next, m->d_vin.p + c0, s);
+            });
     }
     Launch L(gmk::KF_MAXMIN, s);
     gmk::maxmin(m->D, x0, x1 - x0, m->d_vin.p, v_out, pol, wst, s);
@@ -402,8 +426,8 @@ void ensure_t0x(gm_model* m, gm_matrix* tm) {
     for (int64_t c0 = 0; c0 < n; c0 += chunk) {
         const int64_t cn = std::min(chunk, n - c0);
         Launch L(gmk::KF_PROLOGUE, m->stream);
-        gmk::prologue(m->D, tm->row_begin + c0, cn, gmk::PF_SKIP_ABSORBED | gmk::PF_T0X, m->d_origin.p,
-                      tm->t0x.p + c0, m->d_rowflag.p, nullptr, m->d_err.p, m->stream);
+        gmk::prologue(m->D, tm->row_begin + c0, cn, gmk::PF_SKIP_ABSORBED | gmk::PF_T0X, m->d_origin[0].p,
+                      tm->t0x.p + c0, m->d_rowflag[0].p, nullptr, m->d_err.p, m->stream);
     }
     ck(cudaStreamSynchronize(m->stream), "target hit");
     raise_device_error(m);
@@ -540,6 +564,12 @@ void gm_model_free(gm_model* m) {
     if (m->dev_ready) {
         cudaSetDevice(m->device);
         cudaStreamSynchronize(m->stream);
+        if (m->aux) {
+            cudaStreamSynchronize(m->aux);
+            cudaStreamDestroy(m->aux);
+            for (cudaEvent_t e : {m->ev_fork, m->ev_join, m->ev_ready[0], m->ev_ready[1], m->ev_used[0], m->ev_used[1]})
+                cudaEventDestroy(e);
+        }
         cudaStreamDestroy(m->own_stream ? m->own_stream : m->stream);
     }
     delete m;
@@ -624,11 +654,11 @@ gm_code gm_set_device(int32_t device, gm_status* st) {
     return guarded(st, [&] { ck(cudaSetDevice(device), "cudaSetDevice"); });
 }
 
-gm_code gm_model_set_stream(gm_model* m, void* stream, gm_status* st) {
+gm_code gm_model_set_stream(gm_model* m, void* stream, int32_t use_own, gm_status* st) {
     return guarded(st, [&] {
         ensure_device(m);
         if (!m->own_stream) m->own_stream = m->stream;
-        m->stream = stream ? static_cast<cudaStream_t>(stream) : m->own_stream;
+        m->stream = use_own ? m->own_stream : static_cast<cudaStream_t>(stream);
     });
 }
 

@@ -34,6 +34,28 @@ struct GmIns {
 // Device error codes recorded per failing row
 enum GmDevErr { GE_NONE = 0, GE_EXPR = 1, GE_BETA = 2 };
 
+// Division by a loop-invariant divisor d >= 1 for 0 <= n < 2^31:
+// q = (umulhi(n, m) + n) >> s with s = ceil(log2 d), m = floor(2^32 (2^s - d) / d) + 1.
+struct GmFastDiv {
+    uint32_t d, m, s;
+#ifdef __CUDACC__
+    __device__ __forceinline__ int div(int n) const {
+        const uint32_t t = __umulhi(static_cast<uint32_t>(n), m);
+        return static_cast<int>((static_cast<uint64_t>(t) + static_cast<uint32_t>(n)) >> s);
+    }
+#endif
+};
+
+static inline GmFastDiv gm_fastdiv(uint32_t d) {
+    GmFastDiv f;
+    f.d = d ? d : 1;
+    uint32_t s = 0;
+    while ((1ULL << s) < f.d) ++s;
+    f.s = s;
+    f.m = static_cast<uint32_t>(((1ULL << 32) * ((1ULL << s) - f.d)) / f.d + 1);
+    return f;
+}
+
 struct GmDev {
     int n, m, p;             // state / input / disturbance dims
     int family, mult, cut;   // noise family, multiplicative flag, GmCut
@@ -64,6 +86,8 @@ struct GmDev {
     int Wm, Wl;              // W of the last two (effective) axes
     int n_lines;             // R / Wl
     int mm_off, ml_off;      // offsets of the last two axes' masses (n == 1: mm_off = sumW, a 1.0 slot)
+    GmFastDiv div_Wm, div_Wl, div_lines, div_P, div_mw; // n / d for n < 2^31 by multiply-shift
+    GmFastDiv div_W[GMD_MAXD];
 
     int entry[GMD_MAXD + 1]; // bytecode offsets of the n dynamics expressions
     const GmIns* prog;

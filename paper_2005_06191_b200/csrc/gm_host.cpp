@@ -1184,6 +1184,12 @@ GmDev Model::device_descriptor() const {
         D.ml_off = D.mass_off[n - 1];
     }
     D.n_lines = static_cast<int>(R / D.Wl);
+    D.div_Wm = gm_fastdiv(static_cast<uint32_t>(D.Wm));
+    D.div_Wl = gm_fastdiv(static_cast<uint32_t>(D.Wl));
+    D.div_lines = gm_fastdiv(static_cast<uint32_t>(D.n_lines));
+    D.div_P = gm_fastdiv(static_cast<uint32_t>(D.P_size));
+    D.div_mw = gm_fastdiv(static_cast<uint32_t>(D.sumW + 1));
+    for (int d = 0; d < n; ++d) D.div_W[d] = gm_fastdiv(static_cast<uint32_t>(D.W[d]));
     for (size_t i = 0; i < prog.entry.size() && i <= GMD_MAXD; ++i) D.entry[i] = prog.entry[i];
     return D;
 }

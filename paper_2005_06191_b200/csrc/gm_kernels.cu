@@ -377,165 +377,366 @@ __global__ void __launch_bounds__(kThreads) k_prologue(GmDev D, long long row0, 
     if (rowflag_out) rowflag_out[i] = fl;
 }
 
-// Shared-memory layout of a batch of rows for expand / expect_ofa.
-struct BatchSmem {
-    double* mass;   // [rb][sumW+1]  (slot sumW = 1.0: virtual axis)
-    double* P;      // [rb][P_size]  prefix products over the leading axes
-    double* red;    // [kThreads/32] cross-warp partial sums
-    int* lines;     // [n_lines] (when staged)
+// ---------------------------------------------------------------------------
+// Row batches in shared memory (expand / expect_ofa)
+//
+// A row's probabilities factor as p(L, k) = Q[L] * ml[k] with L the slab line
+// (all axes but the last), Q[L] = P[a] * mm[j] the line prefix, P[a] the prefix
+// product over the leading axes (1.0*m0[j0]*m1[j1]*..., abstraction.cpp:150-159)
+// and ml the last axis' masses. Q is staged per row when it fits (TAB_Q);
+// otherwise P is staged and Q[L] is formed per term (TAB_P). Both give the
+// same bits: the rounding sequence is identical.
+//
+// Shared memory is one double array addressed by integer offsets (so every
+// access compiles to LDS with a register offset):
+//   [0, rb*mw)            per-axis masses, slot sumW of each row = 1.0
+//   [offP, +rb*P_size)    prefix products over the leading axes
+//   [offQ, +rb*n_lines)   line prefixes (TAB_Q)
+//   [offR, +8)            cross-warp partial sums
+//   ints after that       slab line offsets (when staged)
+// ---------------------------------------------------------------------------
+
+enum { TAB_Q = 0, TAB_P = 1 };
+
+extern __shared__ __align__(16) double g_sm[];
+
+struct Layout {
+    int mw, offP, offQ, offR, offL; // offL in ints
+    __device__ __forceinline__ Layout(const GmDev& D, int rb, int tab) {
+        mw = D.sumW + 1;
+        offP = rb * mw;
+        offQ = offP + rb * D.P_size;
+        offR = offQ + (tab == TAB_Q ? rb * D.n_lines : 0);
+        offL = 2 * (offR + kThreads / 32);
+    }
 };
 
-__device__ __forceinline__ BatchSmem carve(const GmDev& D, int rb, int table_in_smem) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    BatchSmem S;
-    double* p = reinterpret_cast<double*>(smem_raw);
-    S.mass = p;
-    p += static_cast<long long>(rb) * (D.sumW + 1);
-    S.P = p;
-    p += static_cast<long long>(rb) * D.P_size;
-    S.red = p;
-    p += kThreads / 32;
-    S.lines = table_in_smem ? reinterpret_cast<int*>(p) : const_cast<int*>(D.line_off);
-    return S;
+__device__ __forceinline__ const int* sm_ints() { return reinterpret_cast<const int*>(g_sm); }
+
+// Builds the prefix tables P (and Q) from the staged masses of rb rows.
+__device__ __forceinline__ void stage_tables(const GmDev& D, const Layout& Y, int rb, int tab) {
+    const int mw = Y.mw;
+    for (int c = threadIdx.x; c < rb * D.P_size; c += blockDim.x) {
+        const int i = D.div_P.div(c), a = c - i * D.P_size;
+        const int mrow = i * mw;
+        int jv[GMD_MAXD];
+        int rem = a;
+#pragma unroll
+        for (int d = GMD_MAXD - 1; d >= 0; --d) { // row-major decode, last axis fastest
+            if (d < D.s_axes) {
+                const int q = D.div_W[d].div(rem);
+                jv[d] = rem - q * D.W[d];
+                rem = q;
+            }
+        }
+        double acc = 1.0;
+#pragma unroll
+        for (int d = 0; d < GMD_MAXD; ++d) // axis order, as the recursion multiplies
+            if (d < D.s_axes) acc *= g_sm[mrow + D.mass_off[d] + jv[d]];
+        g_sm[Y.offP + c] = acc;
+    }
+    if (tab == TAB_Q) {
+        __syncthreads();
+        for (int c = threadIdx.x; c < rb * D.n_lines; c += blockDim.x) {
+            const int i = D.div_lines.div(c), L = c - i * D.n_lines;
+            const int a = D.div_Wm.div(L), j = L - a * D.Wm;
+            g_sm[Y.offQ + c] = g_sm[Y.offP + i * D.P_size + a] * g_sm[i * mw + D.mm_off + j];
+        }
+    }
 }
 
-// Loads masses of rows [b0, b0+rb) and builds their prefix tables P (the
-// prefix product 1.0*m0[j0]*m1[j1]*... over axes 0..n-3, abstraction.cpp:157).
-__device__ __forceinline__ void stage_rows(const GmDev& D, const BatchSmem& S, const double* __restrict__ mass,
-                                           long long nrows, long long b0, int rb) {
-    const int mw = D.sumW + 1;
+// Loads the masses of rows [b0, b0+rb) (SoA, pitch nrows) and builds P (and Q).
+__device__ __forceinline__ void stage_rows(const GmDev& D, const Layout& Y, const double* __restrict__ mass,
+                                           long long nrows, long long b0, int rb, GmFastDiv div_rb, int tab) {
+    const int mw = Y.mw;
+    // all threads load in parallel; consecutive threads -> consecutive rows of a plane
     for (int c = threadIdx.x; c < rb * mw; c += blockDim.x) {
-        const int i = c % rb, q = c / rb; // consecutive threads -> consecutive rows (coalesced SoA)
+        const int q = div_rb.div(c), i = c - q * rb;
         double v = 1.0;
         if (q < D.sumW && b0 + i < nrows) v = mass[static_cast<long long>(q) * nrows + b0 + i];
-        S.mass[i * mw + q] = v;
+        g_sm[i * mw + q] = v;
     }
     __syncthreads();
-    for (int c = threadIdx.x; c < rb * D.P_size; c += blockDim.x) {
-        const int i = c / D.P_size, a = c % D.P_size;
-        const double* mrow = S.mass + i * mw;
-        // decode a over W[0..s_axes) row-major, multiply in axis order
-        int rem = a;
-        int div = D.P_size;
-        double acc = 1.0;
-        for (int d = 0; d < D.s_axes; ++d) {
-            div /= D.W[d];
-            const int j = rem / div;
-            rem -= j * div;
-            acc *= mrow[D.mass_off[d] + j];
-        }
-        S.P[i * D.P_size + a] = acc;
-    }
+    stage_tables(D, Y, rb, tab);
 }
 
-__device__ __forceinline__ void stage_table(const GmDev& D, const BatchSmem& S, int table_in_smem) {
-    if (!table_in_smem) return;
-    for (int c = threadIdx.x; c < D.n_lines; c += blockDim.x) S.lines[c] = D.line_off[c];
-}
-
-// Lane-stride walk over the slab: lane l of a row group visits t = l, l+tpr, ...
-// tracking (a, j, k) = (prefix index, second-to-last axis, last axis).
+// Lane-stride walk over a row: lane l of a group of tpr visits t = l, l+tpr, ...
+// as (L, k) = (slab line, last-axis offset), plus (a, j) for TAB_P.
 struct Walk {
-    int a, j, k;
-    int qa, qj, qk;
-    int Wm, Wl;
+    int L, k, a, j;
+    int qL, qk, qa, qj, Wl, Wm;
     __device__ __forceinline__ void init(const GmDev& D, int lane, int tpr) {
-        Wm = D.Wm;
         Wl = D.Wl;
-        const int B2 = Wm * Wl;
-        a = lane / B2;
-        int r = lane - a * B2;
-        j = r / Wl;
-        k = r - j * Wl;
-        qa = tpr / B2;
-        r = tpr - qa * B2;
-        qj = r / Wl;
-        qk = r - qj * Wl;
+        Wm = D.Wm;
+        L = D.div_Wl.div(lane);
+        k = lane - L * Wl;
+        a = D.div_Wm.div(L);
+        j = L - a * Wm;
+        qL = D.div_Wl.div(tpr);
+        qk = tpr - qL * Wl;
+        qa = D.div_Wm.div(qL);
+        qj = qL - qa * Wm;
     }
+    template <bool AJ>
     __device__ __forceinline__ void next() {
         k += qk;
-        int c = k >= Wl;
+        const int c = k >= Wl;
         k -= c ? Wl : 0;
-        j += qj + c;
-        c = j >= Wm;
-        j -= c ? Wm : 0;
-        a += qa + c;
+        L += qL + c;
+        if (AJ) {
+            j += qj + c;
+            const int c2 = j >= Wm;
+            j -= c2 ? Wm : 0;
+            a += qa + c2;
+        }
     }
-    __device__ __forceinline__ int line() const { return a * Wm + j; }
 };
 
-// Sum over the tpr lanes of a row group (fixed butterfly; then warps in order).
-__device__ __forceinline__ double group_reduce(double s, int tpr, const BatchSmem& S, int group_lane0_tid) {
+// Sum over the tpr lanes of a row group: fixed xor butterfly inside the warp,
+// then the group's warps in increasing order. Identical in every kernel.
+__device__ __forceinline__ double group_reduce(double s, int tpr, int offR, int group_lane0_tid) {
     const int wl = tpr < 32 ? tpr : 32;
     for (int off = wl >> 1; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if (tpr > 32) {
+    if (tpr > 32) { // per-group named barrier: groups of a CTA do not wait for each other
         const int warp = threadIdx.x >> 5;
-        if ((threadIdx.x & 31) == 0) S.red[warp] = s;
-        __syncthreads();
+        const int bar = 1 + group_lane0_tid / tpr;
+        if ((threadIdx.x & 31) == 0) g_sm[offR + warp] = s;
+        asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(tpr) : "memory");
         if (threadIdx.x == group_lane0_tid) {
             const int w0 = group_lane0_tid >> 5, nw = tpr >> 5;
-            double t = S.red[w0];
-            for (int q = 1; q < nw; ++q) t += S.red[w0 + q];
+            double t = g_sm[offR + w0];
+            for (int q = 1; q < nw; ++q) t += g_sm[offR + w0 + q];
             s = t;
         }
-        __syncthreads();
+        asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(tpr) : "memory");
     }
     return s;
 }
 
-// Stage (i) expansion: a warp writes one row's R products per pass, lane-strided
-// (coalesced 256-byte stores).
-__global__ void __launch_bounds__(kThreads) k_expand(GmDev D, long long nrows, int rb, int table_in_smem,
+// V gather at vb[off]: one mad.wide.s32 per access (keeps the 64-bit row base
+// in registers instead of re-extending origin + offset per term).
+__device__ __forceinline__ double ldg_at(const double* vb, int off) {
+    const double* a;
+    asm("mad.wide.s32 %0, %1, 8, %2;" : "=l"(a) : "r"(off), "l"(vb));
+    return __ldg(a);
+}
+
+// One row's dot product in the canonical order: lane-strided terms accumulated
+// with fma in increasing t (padding slots contribute fma(0,0,s) == s).
+// MODE 0: stored row; MODE 1: recompute from Q; MODE 2: recompute from P.
+// Term sources: stored row `prow` (global); Q row at g_sm[qo]; P row at g_sm[po];
+// masses mm at g_sm[mmo], ml at g_sm[mlo]; line table `lines` (smem ints or global).
+template <int MODE, int U, bool LS>
+__device__ __forceinline__ double row_dot(const GmDev& D, int lane, int tpr, const double* __restrict__ prow,
+                                          int qo, int po, int mmo, int mlo, const double* __restrict__ vb,
+                                          const int* __restrict__ gl, int lo) {
+    const int R = static_cast<int>(D.R);
+    const int n_it = lane < R ? (R - lane + tpr - 1) / tpr : 0;
+    Walk w;
+    w.init(D, lane, tpr);
+    const double* pp = prow + lane;
+    const int* si = sm_ints();
+    double s = 0.0;
+    auto term = [&](double& p, double& v) {
+        if (MODE == 0) p = __ldcs(pp);
+        else if (MODE == 1) p = g_sm[qo + w.L] * g_sm[mlo + w.k];
+        else p = (g_sm[po + w.a] * g_sm[mmo + w.j]) * g_sm[mlo + w.k];
+        const int off = (LS ? si[lo + w.L] : __ldg(gl + w.L)) + w.k;
+        v = ldg_at(vb, off);
+        pp += tpr;
+        w.template next<MODE == 2>();
+    };
+    const int n_full = n_it - n_it % U;
+    for (int b = 0; b < n_full; b += U) {
+        double p[U], v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) term(p[u], v[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) s = fma(p[u], v[u], s);
+    }
+    const int rem = n_it - n_full;
+    if (rem) {
+        double p[U], v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            p[u] = 0.0;
+            v[u] = 0.0;
+            if (u < rem) term(p[u], v[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) s = fma(p[u], v[u], s);
+    }
+    return s;
+}
+
+// Stage (i) expansion: a warp writes one row's R products lane-strided
+// (coalesced 256-byte stores, evict-first).
+template <int TAB>
+__global__ void __launch_bounds__(kThreads) k_expand(GmDev D, long long nrows, int rb, GmFastDiv div_rb,
                                                     const double* __restrict__ mass,
                                                     double* __restrict__ probs) {
-    const BatchSmem S = carve(D, rb, 0);
-    (void)table_in_smem;
+    const Layout Y(D, rb, TAB);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = blockDim.x >> 5;
-    const int mw = D.sumW + 1;
+    const int R = static_cast<int>(D.R);
     for (long long b0 = static_cast<long long>(blockIdx.x) * rb; b0 < nrows;
          b0 += static_cast<long long>(gridDim.x) * rb) {
         __syncthreads();
-        stage_rows(D, S, mass, nrows, b0, rb);
+        stage_rows(D, Y, mass, nrows, b0, rb, div_rb, TAB);
         __syncthreads();
         for (int i = warp; i < rb; i += nwarps) {
             const long long row = b0 + i;
             if (row >= nrows) break;
-            const double* Pr = S.P + i * D.P_size;
-            const double* mm = S.mass + i * mw + D.mm_off;
-            const double* ml = S.mass + i * mw + D.ml_off;
+            const int qo = Y.offQ + i * D.n_lines, po = Y.offP + i * D.P_size;
+            const int mmo = i * Y.mw + D.mm_off, mlo = i * Y.mw + D.ml_off;
             double* out = probs + row * D.R;
-            Walk wk;
-            wk.init(D, lane, 32);
-            for (long long t = lane; t < D.R; t += 32) {
-                out[t] = (Pr[wk.a] * mm[wk.j]) * ml[wk.k];
-                wk.next();
+            Walk w;
+            w.init(D, lane, 32);
+#pragma unroll 4
+            for (int t = lane; t < R; t += 32) {
+                const double p = TAB == TAB_Q ? g_sm[qo + w.L] * g_sm[mlo + w.k]
+                                              : (g_sm[po + w.a] * g_sm[mmo + w.j]) * g_sm[mlo + w.k];
+                __stcs(out + t, p);
+                w.template next<TAB == TAB_P>();
             }
         }
     }
 }
 
-// Stage (ii), on the fly: row groups of tpr threads recompute each row from the
-// staged masses and dot it with V (synthesis.cpp:100-104 + dot_slab :18-47).
-__global__ void __launch_bounds__(kThreads) k_expect_ofa(GmDev D, long long nrows, int rb, int table_in_smem,
+// Stage (i), fused: each CTA batch evaluates its rows' prologue (image, origin,
+// target-hit mass: one thread per row), their per-axis cell masses (one thread
+// per row x cell), the prefix tables, then streams the R products of every row
+// (warp per row, coalesced evict-first stores). The row prologue of one CTA
+// overlaps the store phase of the others on the same SM.
+template <int TAB>
+__global__ void __launch_bounds__(kThreads) k_build(GmDev D, long long row0, long long nrows, int rb,
+                                                   GmFastDiv div_rb, long long* __restrict__ origin_out,
+                                                   double* __restrict__ t0x_out, double* __restrict__ probs,
+                                                   unsigned long long* err) {
+    const Layout Y(D, rb, TAB);
+    // per-row prologue data and the dynamics program after the batch tables
+    const int offMu = Y.offR + kThreads / 32;          // [rb][GMD_MAXD] image
+    const int offX = offMu + rb * GMD_MAXD;             // [rb][GMD_MAXD] state (multiplicative scale)
+    const int offOk = offX + rb * GMD_MAXD;             // [rb] 1.0 = row ok
+    const int offO = offOk + rb;                        // ints: [rb][GMD_MAXD] origin per axis
+    const int offProg = offO + (rb * GMD_MAXD + 1) / 2; // GmIns (8 bytes each), then literals
+    GmIns* sprog = reinterpret_cast<GmIns*>(g_sm + offProg);
+    double* slits = g_sm + offProg + D.n_ins;
+    int* sorg = reinterpret_cast<int*>(g_sm + offO);
+    for (int c = threadIdx.x; c < D.n_ins; c += blockDim.x) sprog[c] = D.prog[c];
+    for (int c = threadIdx.x; c < D.n_lits; c += blockDim.x) slits[c] = D.lits[c];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nwarps = blockDim.x >> 5;
+    const int mw = Y.mw;
+    const int R = static_cast<int>(D.R);
+    const bool reach = D.spec_kind != GM_SPEC_SAFETY;
+    for (long long b0 = static_cast<long long>(blockIdx.x) * rb; b0 < nrows;
+         b0 += static_cast<long long>(gridDim.x) * rb) {
+        __syncthreads();
+        if (threadIdx.x < rb) { // RowKernel::compute (abstraction.cpp:72-121) + box_mass (:187-191)
+            const int i = threadIdx.x;
+            const long long r = b0 + i;
+            double ok = 0.0;
+            if (r < nrows) {
+                double x[GMD_MAXD], u[GMD_MAXD], w[GMD_MAXD], mu[GMD_MAXD];
+                long long ix;
+                decode_row(D, row0 + r, ix, x, u, w);
+                if (run_dynamics(D, sprog, slits, x, u, w, mu)) {
+                    ok = 1.0;
+                    long long flat = 0;
+                    for (int d = 0; d < D.n; ++d) {
+                        const long long o = slab_origin(D, d, mu[d]);
+                        sorg[i * GMD_MAXD + d] = static_cast<int>(o);
+                        flat += o * D.xstride[d];
+                        g_sm[offMu + i * GMD_MAXD + d] = mu[d];
+                        g_sm[offX + i * GMD_MAXD + d] = x[d];
+                    }
+                    origin_out[r] = flat;
+                    if (t0x_out) {
+                        const bool absorbed = reach && D.absorb != nullptr && D.absorb[ix];
+                        double p = 0.0;
+                        bool bok = true;
+                        if (!absorbed) {
+                            p = 1.0;
+                            for (int d = 0; d < D.n; ++d) {
+                                p *= tmass(D, d, D.tlo[d], D.thi[d], mu[d], D.mult ? x[d] : 1.0, bok);
+                                if (p == 0.0) break;
+                            }
+                            p = smin(1.0, smax(0.0, p));
+                        }
+                        if (!bok) record_error(err, row0 + r);
+                        t0x_out[r] = p;
+                    }
+                } else {
+                    record_error(err, row0 + r);
+                }
+            }
+            g_sm[offOk + i] = ok;
+        }
+        __syncthreads();
+        // fill_axis_masses (abstraction.cpp:130-146): thread per (row, cell)
+        for (int c = threadIdx.x; c < rb * mw; c += blockDim.x) {
+            const int q = div_rb.div(c), i = c - q * rb;
+            double v = 1.0;
+            if (q < D.sumW && g_sm[offOk + i] != 0.0) {
+                int d = 0;
+                while (q >= D.mass_off[d + 1]) ++d;
+                const int t = q - D.mass_off[d];
+                const double rep = D.xlb[d] + static_cast<double>(sorg[i * GMD_MAXD + d] + t) * D.xeta[d];
+                const double half = 0.5 * D.xeta[d];
+                bool ok = true;
+                v = tmass(D, d, rep - half, rep + half, g_sm[offMu + i * GMD_MAXD + d],
+                          D.mult ? g_sm[offX + i * GMD_MAXD + d] : 1.0, ok);
+                if (!ok) record_error(err, row0 + b0 + i);
+            }
+            g_sm[i * mw + q] = v;
+        }
+        __syncthreads();
+        stage_tables(D, Y, rb, TAB);
+        __syncthreads();
+        for (int i = warp; i < rb; i += nwarps) { // fill_product (abstraction.cpp:150-159)
+            const long long row = b0 + i;
+            if (row >= nrows) break;
+            const int qo = Y.offQ + i * D.n_lines, po = Y.offP + i * D.P_size;
+            const int mmo = i * mw + D.mm_off, mlo = i * mw + D.ml_off;
+            double* out = probs + row * D.R;
+            Walk wk;
+            wk.init(D, lane, 32);
+#pragma unroll 4
+            for (int t = lane; t < R; t += 32) {
+                const double p = TAB == TAB_Q ? g_sm[qo + wk.L] * g_sm[mlo + wk.k]
+                                              : (g_sm[po + wk.a] * g_sm[mmo + wk.j]) * g_sm[mlo + wk.k];
+                __stcs(out + t, p);
+                wk.template next<TAB == TAB_P>();
+            }
+        }
+    }
+}
+
+// Stage (ii), on the fly (synthesis.cpp:100-104 + dot_slab :18-47): row groups
+// of tpr threads recompute each row from the staged masses and dot it with V.
+template <int TAB, bool LS>
+__global__ void __launch_bounds__(kThreads) k_expect_ofa(GmDev D, long long nrows, int rb, GmFastDiv div_rb,
                                                         const double* __restrict__ mass,
                                                         const long long* __restrict__ origin,
                                                         const double* __restrict__ t0x,
                                                         const uint8_t* __restrict__ rowflag,
                                                         const double* __restrict__ V,
                                                         double* __restrict__ v_in) {
-    const BatchSmem S = carve(D, rb, table_in_smem);
-    stage_table(D, S, table_in_smem);
+    const Layout Y(D, rb, TAB);
+    if (LS) {
+        int* si = reinterpret_cast<int*>(g_sm);
+        for (int c = threadIdx.x; c < D.n_lines; c += blockDim.x) si[Y.offL + c] = D.line_off[c];
+    }
     const int tpr = D.tpr;
     const int groups = kThreads / tpr;
-    const int g = threadIdx.x / tpr, lane = threadIdx.x % tpr;
-    const int mw = D.sumW + 1;
+    const int g = threadIdx.x / tpr, lane = threadIdx.x - g * tpr;
     const bool reach = D.spec_kind != GM_SPEC_SAFETY;
     const int iters = (rb + groups - 1) / groups;
     for (long long b0 = static_cast<long long>(blockIdx.x) * rb; b0 < nrows;
          b0 += static_cast<long long>(gridDim.x) * rb) {
         __syncthreads();
-        stage_rows(D, S, mass, nrows, b0, rb);
+        stage_rows(D, Y, mass, nrows, b0, rb, div_rb, TAB);
         __syncthreads();
         for (int it = 0; it < iters; ++it) {
             const int i = g + it * groups;
@@ -544,22 +745,11 @@ __global__ void __launch_bounds__(kThreads) k_expect_ofa(GmDev D, long long nrow
             const uint8_t fl = valid ? rowflag[row] : RF_ABSORBED;
             double s = 0.0;
             if (!(fl & (RF_ABSORBED | RF_ERROR))) {
-                const double* Pr = S.P + i * D.P_size;
-                const double* mm = S.mass + i * mw + D.mm_off;
-                const double* ml = S.mass + i * mw + D.ml_off;
-                const double* vb = V + origin[row];
-                const int* lines = S.lines;
-                Walk wk;
-                wk.init(D, lane, tpr);
-#pragma unroll 4
-                for (long long t = lane; t < D.R; t += tpr) {
-                    const double p = (Pr[wk.a] * mm[wk.j]) * ml[wk.k];
-                    const double v = __ldg(vb + lines[wk.line()] + wk.k);
-                    s = fma(p, v, s);
-                    wk.next();
-                }
+                s = row_dot<TAB == TAB_Q ? 1 : 2, 4, LS>(D, lane, tpr, nullptr, Y.offQ + i * D.n_lines,
+                                                         Y.offP + i * D.P_size, i * Y.mw + D.mm_off,
+                                                         i * Y.mw + D.ml_off, V + origin[row], D.line_off, Y.offL);
             }
-            s = group_reduce(s, tpr, S, g * tpr);
+            s = group_reduce(s, tpr, Y.offR, g * tpr);
             if (valid && lane == 0) {
                 double r = 0.0;
                 if (!(fl & (RF_ABSORBED | RF_ERROR))) r = reach ? s + t0x[row] : s;
@@ -569,54 +759,43 @@ __global__ void __launch_bounds__(kThreads) k_expect_ofa(GmDev D, long long nrow
     }
 }
 
-// Stage (ii), stored matrix: row groups stream each row (evict-first loads)
-// and gather V at the row's origin (synthesis.cpp:95-99).
+// Stage (ii), stored matrix (synthesis.cpp:95-99): row groups stream each row
+// (evict-first, 8 loads in flight per lane) and gather V at the row's origin.
+template <bool LS>
 __global__ void __launch_bounds__(kThreads) k_expect_matrix(GmDev D, long long row0, long long r_lo,
-                                                           long long r_hi, int table_in_smem,
-                                                           const double* __restrict__ probs,
+                                                           long long r_hi, const double* __restrict__ probs,
                                                            const long long* __restrict__ origins,
                                                            const double* __restrict__ t0x,
                                                            const double* __restrict__ V,
                                                            double* __restrict__ v_in) {
-    const BatchSmem S = carve(D, 0, table_in_smem);
-    stage_table(D, S, table_in_smem);
+    const Layout Y(D, 0, TAB_P);
+    if (LS) {
+        int* si = reinterpret_cast<int*>(g_sm);
+        for (int c = threadIdx.x; c < D.n_lines; c += blockDim.x) si[Y.offL + c] = D.line_off[c];
+    }
     __syncthreads();
     const int tpr = D.tpr;
     const int groups = kThreads / tpr;
-    const int g = threadIdx.x / tpr, lane = threadIdx.x % tpr;
+    const int g = threadIdx.x / tpr, lane = threadIdx.x - g * tpr;
     const bool reach = D.spec_kind != GM_SPEC_SAFETY;
     const long long nrows = r_hi - r_lo;
     const long long total_groups = static_cast<long long>(gridDim.x) * groups;
     const long long iters = (nrows + total_groups - 1) / total_groups;
+    const long long nuw = D.n_u * D.n_w;
     for (long long it = 0; it < iters; ++it) {
         const long long rl = (it * gridDim.x + blockIdx.x) * groups + g; // local row
         const bool valid = rl < nrows;
         const long long r = r_lo + rl; // row inside the matrix
         bool skip = !valid;
-        long long ix = 0;
-        if (valid) {
-            ix = (row0 + r) / (D.n_u * D.n_w);
-            skip = reach && D.absorb != nullptr && D.absorb[ix];
-        }
+        if (valid && reach && D.absorb != nullptr) skip = D.absorb[(row0 + r) / nuw];
         double s = 0.0;
-        if (!skip) {
-            const double* pr = probs + r * D.R;
-            const double* vb = V + origins[r];
-            const int* lines = S.lines;
-            Walk wk;
-            wk.init(D, lane, tpr);
-#pragma unroll 4
-            for (long long t = lane; t < D.R; t += tpr) {
-                const double p = __ldcs(pr + t);
-                const double v = __ldg(vb + lines[wk.line()] + wk.k);
-                s = fma(p, v, s);
-                wk.next();
-            }
-        }
-        s = group_reduce(s, tpr, S, g * tpr);
+        if (!skip)
+            s = row_dot<0, 8, LS>(D, lane, tpr, probs + r * D.R, 0, 0, 0, 0, V + origins[r], D.line_off, Y.offL);
+        s = group_reduce(s, tpr, Y.offR, g * tpr);
         if (valid && lane == 0) v_in[rl] = skip ? 0.0 : (reach ? s + t0x[r] : s);
     }
 }
+
 
 // min over w (strict <, ascending), then max over u (strict >, ascending):
 // lowest-index ties (synthesis.cpp:112-142). L lanes per state.
@@ -713,32 +892,41 @@ __global__ void k_mask(GmDev D, long long r_lo, long long nrows, double* probs,
 // launchers
 // ---------------------------------------------------------------------------
 
+namespace {
+constexpr size_t kSoftSmem = 56 * 1024;   // several CTAs per SM
+constexpr size_t kHardSmem = 200 * 1024;  // one CTA per SM, last resort
+}
+
 BatchPlan plan_batches(const GmDev& D, bool ofa) {
     BatchPlan b;
     b.tpr = ofa ? D.tpr : 32;
     b.groups = kThreads / b.tpr;
-    const size_t per_row = static_cast<size_t>(D.sumW + 1 + D.P_size) * sizeof(double);
+    const size_t mw = static_cast<size_t>(D.sumW + 1);
     const size_t fixed = (kThreads / 32) * sizeof(double);
-    const size_t table = static_cast<size_t>(D.n_lines) * sizeof(int);
-    const size_t soft = 48 * 1024, hard = 200 * 1024;
-    // rows per batch: aim for >= 2 rows per group so each CTA has work while
-    // staging, within a soft budget that allows several CTAs per SM.
-    size_t budget = soft;
-    b.table_in_smem = ofa && (fixed + table + per_row * b.groups <= soft) ? 1 : 0;
-    size_t avail = budget - fixed - (b.table_in_smem ? table : 0);
-    long long rb = per_row ? static_cast<long long>(avail / per_row) : kThreads;
-    if (rb < b.groups) {
-        budget = hard;
-        avail = budget - fixed - (b.table_in_smem ? table : 0);
-        rb = static_cast<long long>(avail / per_row);
+    const size_t table = ofa ? static_cast<size_t>(D.n_lines) * sizeof(int) : 0;
+    const size_t q_row = (mw + D.P_size + D.n_lines) * sizeof(double);
+    const size_t p_row = (mw + D.P_size) * sizeof(double);
+    const long long want = std::max(b.groups, ofa ? 2 : 8);
+    struct Opt { int tab; int lsmem; size_t budget; };
+    const Opt opts[] = {{TAB_Q, 1, kSoftSmem}, {TAB_Q, 0, kSoftSmem}, {TAB_P, 1, kSoftSmem},
+                        {TAB_P, 0, kSoftSmem}, {TAB_P, 0, kHardSmem}};
+    for (const Opt& o : opts) {
+        const size_t per = o.tab == TAB_Q ? q_row : p_row;
+        const size_t tb = (ofa && o.lsmem) ? table : 0;
+        if (!ofa && o.lsmem) continue;
+        if (fixed + tb >= o.budget) continue;
+        long long rb = static_cast<long long>((o.budget - fixed - tb) / per);
+        if (rb < (o.budget == kHardSmem ? 1 : want)) continue;
+        rb = std::min<long long>(rb, kThreads);
+        if (rb >= b.groups) rb -= rb % b.groups;
+        b.rb = static_cast<int>(rb);
+        b.tab = o.tab;
+        b.table_in_smem = (ofa && o.lsmem) ? 1 : 0;
+        b.smem = fixed + per * static_cast<size_t>(b.rb) + tb;
+        return b;
     }
-    if (rb < 1) throw std::runtime_error("row too wide for the device batch layout (" +
-                                         std::to_string(per_row) + " bytes of shared memory per row)");
-    rb = std::min<long long>(rb, kThreads);
-    if (rb >= b.groups) rb -= rb % b.groups;
-    b.rb = static_cast<int>(rb);
-    b.smem = fixed + per_row * static_cast<size_t>(b.rb) + (b.table_in_smem ? table : 0);
-    return b;
+    throw std::runtime_error("row too wide for the device batch layout (" + std::to_string(p_row) +
+                             " bytes of shared memory per row)");
 }
 
 void absorb_flags(const GmDev& D, uint8_t* d_flags, cudaStream_t s) {
@@ -752,18 +940,17 @@ void zero_absorbing(const GmDev& D, double* d_v, cudaStream_t s) {
     check_launch("zero_absorbing");
 }
 
+template <class K>
+static void allow_smem(K kernel, size_t smem) {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
 void prologue(const GmDev& D, long long row0, long long nrows, int flags, long long* origin_out,
               double* t0x_out, uint8_t* rowflag_out, double* mass_out,
               unsigned long long* d_err_row, cudaStream_t s) {
     if (nrows <= 0) return;
     const size_t smem = ((D.n_ins * sizeof(GmIns) + 15) / 16) * 16 + D.n_lits * sizeof(double);
-    if (smem > 48 * 1024) {
-        static bool set = false;
-        if (!set) {
-            cudaFuncSetAttribute(k_prologue, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            set = true;
-        }
-    }
+    allow_smem(k_prologue, smem);
     k_prologue<<<grid_for(nrows, kThreads), kThreads, smem, s>>>(D, row0, nrows, flags, origin_out, t0x_out,
                                                                 rowflag_out, mass_out, d_err_row);
     check_launch("prologue");
@@ -780,10 +967,12 @@ static int num_sms() {
     return sms;
 }
 
+// persistent grids: resident CTAs per SM x SMs, capped by the work
 template <class K>
-static int resident_grid(K kernel, size_t smem, long long batches) {
+static int resident_grid(K kernel, size_t smem, long long batches, int reserve = 0) {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
+    per_sm -= reserve; // slots left for the row prologue running concurrently on the aux stream
     if (per_sm < 1) per_sm = 1;
     long long g = static_cast<long long>(per_sm) * num_sms();
     if (g > batches) g = batches;
@@ -792,12 +981,69 @@ static int resident_grid(K kernel, size_t smem, long long batches) {
 
 void expand(const GmDev& D, long long nrows, const double* mass, double* probs_out, cudaStream_t s) {
     if (nrows <= 0) return;
-    BatchPlan b = plan_batches(D, false);
-    b.smem -= b.table_in_smem ? static_cast<size_t>(D.n_lines) * sizeof(int) : 0;
-    if (b.smem > 48 * 1024) cudaFuncSetAttribute(k_expand, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b.smem);
+    const BatchPlan b = plan_batches(D, false);
     const long long batches = (nrows + b.rb - 1) / b.rb;
-    k_expand<<<resident_grid(k_expand, b.smem, batches), kThreads, b.smem, s>>>(D, nrows, b.rb, 0, mass, probs_out);
+    if (b.tab == TAB_Q) {
+        allow_smem(k_expand<TAB_Q>, b.smem);
+        k_expand<TAB_Q><<<resident_grid(k_expand<TAB_Q>, b.smem, batches, 1), kThreads, b.smem, s>>>(
+            D, nrows, b.rb, gm_fastdiv(b.rb), mass, probs_out);
+    } else {
+        allow_smem(k_expand<TAB_P>, b.smem);
+        k_expand<TAB_P><<<resident_grid(k_expand<TAB_P>, b.smem, batches, 1), kThreads, b.smem, s>>>(
+            D, nrows, b.rb, gm_fastdiv(b.rb), mass, probs_out);
+    }
     check_launch("expand");
+}
+
+// Fused stage (i): rows per batch so that the per-row tables, prologue data and
+// the dynamics program fit the soft shared-memory budget.
+void build(const GmDev& D, long long row0, long long nrows, long long* origin_out, double* t0x_out,
+           double* probs_out, unsigned long long* d_err, cudaStream_t s) {
+    if (nrows <= 0) return;
+    const size_t mw = static_cast<size_t>(D.sumW + 1);
+    const size_t fixed = (kThreads / 32 + D.n_ins + D.n_lits + 2) * sizeof(double);
+    const size_t extra_row = (2 * GMD_MAXD + 1) * sizeof(double) + GMD_MAXD * sizeof(int);
+    const size_t q_row = (mw + D.P_size + D.n_lines) * sizeof(double) + extra_row;
+    const size_t p_row = (mw + D.P_size) * sizeof(double) + extra_row;
+    int tab = -1;
+    long long rb = 0;
+    for (size_t budget : {kSoftSmem, kHardSmem}) {
+        for (int t : {TAB_Q, TAB_P}) {
+            const size_t per = t == TAB_Q ? q_row : p_row;
+            if (fixed >= budget) continue;
+            const long long r = static_cast<long long>((budget - fixed) / per);
+            if (r >= (budget == kSoftSmem ? 8 : 1)) {
+                tab = t;
+                rb = std::min<long long>(r, kThreads);
+                break;
+            }
+        }
+        if (tab >= 0) break;
+    }
+    if (tab < 0) throw std::runtime_error("row too wide for the device build layout");
+    const size_t smem = fixed + (tab == TAB_Q ? q_row : p_row) * static_cast<size_t>(rb);
+    const long long batches = (nrows + rb - 1) / rb;
+    const GmFastDiv drb = gm_fastdiv(static_cast<uint32_t>(rb));
+    if (tab == TAB_Q) {
+        allow_smem(k_build<TAB_Q>, smem);
+        k_build<TAB_Q><<<resident_grid(k_build<TAB_Q>, smem, batches), kThreads, smem, s>>>(
+            D, row0, nrows, static_cast<int>(rb), drb, origin_out, t0x_out, probs_out, d_err);
+    } else {
+        allow_smem(k_build<TAB_P>, smem);
+        k_build<TAB_P><<<resident_grid(k_build<TAB_P>, smem, batches), kThreads, smem, s>>>(
+            D, row0, nrows, static_cast<int>(rb), drb, origin_out, t0x_out, probs_out, d_err);
+    }
+    check_launch("build");
+}
+
+template <int TAB, bool LS>
+static void launch_ofa(const GmDev& D, const BatchPlan& b, long long nrows, const double* mass,
+                       const long long* origin, const double* t0x, const uint8_t* rowflag, const double* V,
+                       double* v_in, cudaStream_t s) {
+    allow_smem(k_expect_ofa<TAB, LS>, b.smem);
+    const long long batches = (nrows + b.rb - 1) / b.rb;
+    k_expect_ofa<TAB, LS><<<resident_grid(k_expect_ofa<TAB, LS>, b.smem, batches), kThreads, b.smem, s>>>(
+        D, nrows, b.rb, gm_fastdiv(b.rb), mass, origin, t0x, rowflag, V, v_in);
 }
 
 void expect_ofa(const GmDev& D, long long nrows, const double* mass, const long long* origin,
@@ -805,11 +1051,13 @@ void expect_ofa(const GmDev& D, long long nrows, const double* mass, const long 
                 cudaStream_t s) {
     if (nrows <= 0) return;
     const BatchPlan b = plan_batches(D, true);
-    if (b.smem > 48 * 1024)
-        cudaFuncSetAttribute(k_expect_ofa, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b.smem);
-    const long long batches = (nrows + b.rb - 1) / b.rb;
-    k_expect_ofa<<<resident_grid(k_expect_ofa, b.smem, batches), kThreads, b.smem, s>>>(
-        D, nrows, b.rb, b.table_in_smem, mass, origin, t0x, rowflag, V, v_in);
+    if (b.tab == TAB_Q) {
+        if (b.table_in_smem) launch_ofa<TAB_Q, true>(D, b, nrows, mass, origin, t0x, rowflag, V, v_in, s);
+        else launch_ofa<TAB_Q, false>(D, b, nrows, mass, origin, t0x, rowflag, V, v_in, s);
+    } else {
+        if (b.table_in_smem) launch_ofa<TAB_P, true>(D, b, nrows, mass, origin, t0x, rowflag, V, v_in, s);
+        else launch_ofa<TAB_P, false>(D, b, nrows, mass, origin, t0x, rowflag, V, v_in, s);
+    }
     check_launch("expect_ofa");
 }
 
@@ -818,12 +1066,17 @@ void expect_matrix(const GmDev& D, long long row0, long long r_lo, long long r_h
                    const double* V, double* v_in, cudaStream_t s) {
     if (r_hi <= r_lo) return;
     const size_t table = static_cast<size_t>(D.n_lines) * sizeof(int);
-    const int in_smem = table <= 32 * 1024 ? 1 : 0;
+    const bool in_smem = table <= 48 * 1024;
     const size_t smem = (kThreads / 32) * sizeof(double) + (in_smem ? table : 0);
     const int groups = kThreads / D.tpr;
     const long long blocks_needed = (r_hi - r_lo + groups - 1) / groups;
-    k_expect_matrix<<<resident_grid(k_expect_matrix, smem, blocks_needed), kThreads, smem, s>>>(
-        D, row0, r_lo, r_hi, in_smem, probs, origins, t0x, V, v_in);
+    if (in_smem) {
+        k_expect_matrix<true><<<resident_grid(k_expect_matrix<true>, smem, blocks_needed), kThreads, smem, s>>>(
+            D, row0, r_lo, r_hi, probs, origins, t0x, V, v_in);
+    } else {
+        k_expect_matrix<false><<<resident_grid(k_expect_matrix<false>, smem, blocks_needed), kThreads, smem, s>>>(
+            D, row0, r_lo, r_hi, probs, origins, t0x, V, v_in);
+    }
     check_launch("expect_matrix");
 }
 

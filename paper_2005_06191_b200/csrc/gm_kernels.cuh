@@ -20,6 +20,7 @@ enum Family { KF_PROLOGUE = 0, KF_EXPAND = 1, KF_MASK = 2, KF_EXPECT_MATRIX = 3,
 
 struct BatchPlan {
     int tpr, groups, rb;     // threads per row, row groups per CTA, rows per CTA batch
+    int tab;                 // 0: line-prefix table per row, 1: leading-prefix table per row
     int table_in_smem;       // line-offset table staged in shared memory
     size_t smem;             // dynamic shared memory bytes
 };
@@ -34,6 +35,11 @@ void zero_absorbing(const GmDev& D, double* d_v, cudaStream_t s);
 void prologue(const GmDev& D, long long row0, long long nrows, int flags, long long* origin_out,
               double* t0x_out, uint8_t* rowflag_out, double* mass_out,
               unsigned long long* d_err_row, cudaStream_t s);
+
+// Fused stage (i) (build_matrix body, abstraction.cpp:211-223): rows
+// [row0, row0+nrows) -> origins, stored rows (and target-hit masses if t0x_out).
+void build(const GmDev& D, long long row0, long long nrows, long long* origin_out, double* t0x_out,
+           double* probs_out, unsigned long long* d_err, cudaStream_t s);
 
 // Outer-product expansion of the prologue's masses into stored rows
 // (fill_product, abstraction.cpp:150-159).

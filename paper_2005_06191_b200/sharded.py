@@ -61,7 +61,7 @@ class DeviceBackend:
         self.stream = stream or torch.cuda.current_stream()
         self.keep = keep_matrix
         self._tm = C.c_void_p()
-        call("gm_model_set_stream", model.handle, C.c_void_p(self.stream.cuda_stream))
+        call("gm_model_set_stream", model.handle, C.c_void_p(self.stream.cuda_stream), 0)
 
     def build(self, x0: int, x1: int):
         """Stage (i) for the shard; with keep_matrix the device buffers are reused

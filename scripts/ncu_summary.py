@@ -1,0 +1,44 @@
+"""Key metrics of an ncu --set full report (+ top SASS stall lines)."""
+import csv
+import io
+import subprocess
+import sys
+
+KEEP = ['Duration', 'DRAM Throughput', 'Memory Throughput', 'L1/TEX Hit Rate', 'L2 Hit Rate', 'Executed Ipc Active',
+        'Issue Slots Busy', 'Warp Cycles Per Issued Instruction', 'Registers Per Thread', 'Achieved Occupancy',
+        'Theoretical Occupancy', 'Executed Instructions', 'Grid Size', 'Dynamic Shared Memory Per Block',
+        'Eligible Warps Per Scheduler', 'Active Warps Per Scheduler', 'L1/TEX Cache Throughput', 'L2 Cache Throughput',
+        'Compute (SM) Throughput', 'Block Limit Registers', 'Block Limit Shared Mem']
+
+
+def run(args):
+    return subprocess.run(["ncu", "-i", *args], capture_output=True, text=True).stdout
+
+
+def main(rep, top=25):
+    rows = list(csv.reader(io.StringIO(run([rep, "--page", "details", "--csv"]))))
+    h = rows[0]
+    for r in rows[1:]:
+        d = dict(zip(h, r))
+        if d["Metric Name"] in KEEP:
+            print(f"{d['Metric Name']:40s} {d['Metric Value']} {d['Metric Unit']}")
+    raw = list(csv.reader(io.StringIO(run([rep, "--page", "raw", "--csv"]))))
+    if len(raw) > 2:
+        hh = raw[0]
+        vals = raw[2]
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            if k in hh:
+                print(f"{k:40s} {vals[hh.index(k)]} {raw[1][hh.index(k)]}")
+    src = list(csv.reader(io.StringIO(run([rep, "--page", "source", "--csv", "--print-source", "sass"]))))
+    hs = src[1]
+    data = [dict(zip(hs, r)) for r in src[2:] if len(r) == len(hs)]
+    tot = sum(int(d["Warp Stall Sampling (All Samples)"]) for d in data) or 1
+    exs = sum(int(d["Instructions Executed"]) for d in data) or 1
+    print("--- top stall lines")
+    for d in sorted(data, key=lambda d: -int(d["Warp Stall Sampling (All Samples)"]))[:top]:
+        print(f"{int(d['Warp Stall Sampling (All Samples)']) / tot * 100:5.1f}% "
+              f"ex={int(d['Instructions Executed']) / exs * 100:5.2f}%  {d['Source'][:80]}")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 25)
