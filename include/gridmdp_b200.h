@@ -84,7 +84,7 @@ typedef struct gm_sizes {
     double gamma;
     int64_t mem_budget;
     int32_t rows_per_thread_group;  /* device reduction width (identical in matrix and OFA) */
-    int32_t reserved;
+    int32_t size_overflow;          /* rows or memory_estimate overflow 64 bits (both set to 0) */
 } gm_sizes;
 
 /* ---------------------------------------------------------------- front end */

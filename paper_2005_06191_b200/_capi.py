@@ -67,7 +67,7 @@ class Sizes(C.Structure):
         ("gamma", C.c_double),
         ("mem_budget", C.c_int64),
         ("rows_per_thread_group", C.c_int32),
-        ("reserved", C.c_int32),
+        ("size_overflow", C.c_int32),
     ]
 
 

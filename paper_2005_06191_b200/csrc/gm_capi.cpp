@@ -620,8 +620,14 @@ gm_code gm_model_sizes(const gm_model* m, gm_sizes* o, gm_status* st) {
         }
         o->row_width = M.R;
         o->rows_per_thread_group = tpr_for_width(M.R);
-        o->rows = M.rows();
-        o->memory_estimate = M.memory_estimate();
+        try { // memory_estimate raises MemoryError only when asked for (abstraction.cpp:37-48)
+            o->rows = M.rows();
+            o->memory_estimate = M.memory_estimate();
+        } catch (const MemoryErr&) {
+            o->rows = 0;
+            o->memory_estimate = 0;
+            o->size_overflow = 1;
+        }
     });
 }
 

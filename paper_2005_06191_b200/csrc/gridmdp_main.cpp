@@ -53,6 +53,11 @@ void print_sizes(const gm_sizes& s) {
     std::cout << "inputs: " << s.n_inputs << "\n";
     std::cout << "disturbances: " << s.n_disturbances << "\n";
     std::cout << "state_input_pairs: " << s.n_states * s.n_inputs << "\n";
+    if (s.size_overflow) { // MemoryError from checked_mul (common.hpp:67-71) -> exit 3
+        std::cout.flush();
+        std::cerr << "error: memory_estimate: size arithmetic overflows 64 bits\n";
+        std::exit(3);
+    }
     std::cout << "rows: " << s.rows << "\n";
     std::cout << "row_width: " << s.row_width << "\n";
     std::cout << "memory_estimate_bytes: " << s.memory_estimate << "\n";
@@ -93,7 +98,9 @@ int cmd_abstract(const Args& a) {
                   << "; use ofa mode\n";
         return 3;
     }
-    if (gm_set_device(a.device, &st) != GM_OK) return fail(st);
+    // device 0 is the default; selecting it eagerly would turn the reference's validation
+    // errors (spec, budget) into device errors on hosts without a GPU
+    if (a.device != 0 && gm_set_device(a.device, &st) != GM_OK) return fail(st);
     const auto t0 = std::chrono::steady_clock::now();
     gm_matrix* tm = nullptr;
     if (gm_build_matrix(m, 0, sz.rows, &tm, &st) != GM_OK) return fail(st);
@@ -118,7 +125,9 @@ int cmd_synthesize(const Args& a) {
     std::cout << "threads: " << resolve_threads(sz.threads) << "\n";
     std::cout << "time_steps: " << sz.horizon << "\n";
     gm_status st;
-    if (gm_set_device(a.device, &st) != GM_OK) return fail(st);
+    // device 0 is the default; selecting it eagerly would turn the reference's validation
+    // errors (spec, budget) into device errors on hosts without a GPU
+    if (a.device != 0 && gm_set_device(a.device, &st) != GM_OK) return fail(st);
     const auto t0 = std::chrono::steady_clock::now();
     gm_result* r = nullptr;
     if (gm_synthesize(m, &r, &st) != GM_OK) return fail(st);

@@ -342,7 +342,10 @@ def window_extents(m: SystemModel) -> list[int]:
 
 
 def memory_estimate(m: SystemModel) -> int:
-    return int(m.sizes().memory_estimate)
+    s = m.sizes()
+    if s.size_overflow:
+        raise MemoryError("memory_estimate: size arithmetic overflows 64 bits")
+    return int(s.memory_estimate)
 
 
 class TransitionMatrix:

@@ -98,6 +98,48 @@ def main() -> None:
         manifest["estimate"][cfg.stem] = {"config": text, "sizes": parse_sizes(ref("estimate", "-c", tmp).stdout)}
         tmp.unlink()
 
+    # front-end error behaviour: rc and message of the reference for bad inputs
+    tiny = (CASES / "tiny.cfg").read_text()
+    bad_inputs = {
+        "no_semicolon": "states.dim = 1\n",
+        "no_equals": "states.dim 1;\n",
+        "empty_key": " = 1;\n",
+        "duplicate": "states.dim = 1;\nstates.dim = 2;\n",
+        "missing_lb": "states.dim = 1;\n",
+        "bad_vector": tiny.replace("states.lb = {-1.0};", "states.lb = -1.0;"),
+        "bad_number": tiny.replace("states.eta = {0.25};", "states.eta = {0.2x5};"),
+        "unknown_key": tiny + "exec.gpus = 8;\n",
+        "unknown_noise": tiny.replace("noise.type = normal;", "noise.type = cauchy;"),
+        "bad_mode": tiny + "noise.mode = both;\n",
+        "vec_size": tiny.replace("noise.sigma = {0.3};", "noise.sigma = {0.3, 0.3};"),
+        "neg_eta": tiny.replace("states.eta = {0.25};", "states.eta = {-0.25};"),
+        "lb_gt_ub": tiny.replace("states.lb = {-1.0};", "states.lb = {2.0};"),
+        "sigma_zero": tiny.replace("noise.sigma = {0.3};", "noise.sigma = {0.0};"),
+        "gamma_range": tiny.replace("noise.cutting_probability = 0.001;", "noise.cutting_probability = 2;"),
+        "parse_ident": tiny.replace("0.7*x0 + 0.4*u0", "0.7*x0 + y0"),
+        "parse_range": tiny.replace("0.7*x0 + 0.4*u0", "x1"),
+        "parse_func": tiny.replace("0.7*x0 + 0.4*u0", "foo(x0)"),
+        "parse_paren": tiny.replace("0.7*x0 + 0.4*u0", "(x0 + 1"),
+        "parse_trailing": tiny.replace("0.7*x0 + 0.4*u0", "x0 1"),
+        "parse_number": tiny.replace("0.7*x0 + 0.4*u0", "1.2.3*x0"),
+        "parse_char": tiny.replace("0.7*x0 + 0.4*u0", "x0 $ 1"),
+        "parse_arity": tiny.replace("0.7*x0 + 0.4*u0", "min(x0)"),
+        "spec_kind": tiny.replace("spec.type = safety;", "spec.type = liveness;"),
+        "spec_box": tiny.replace("spec.type = safety;", "spec.type = reachability;") +
+        "target.lb = {0.5};\ntarget.ub = {3.0};\n",
+        "spec_safety_box": tiny + "target.lb = {0.5};\ntarget.ub = {0.6};\n",
+        "spec_horizon": tiny.replace("spec.time_steps = 3;", "spec.time_steps = 0;"),
+    }
+    manifest["errors"] = {}
+    for name, text in bad_inputs.items():
+        tmp = OUT / f"_bad_{name}.cfg"
+        tmp.write_text(text)
+        p = ref("synthesize", "-c", tmp, "-o", OUT / "_bad.bin", check=False)
+        manifest["errors"][name] = {"config": text, "rc": p.returncode,
+                                    "stderr": p.stderr.strip().replace(str(tmp), "<cfg>")}
+        tmp.unlink()
+        (OUT / "_bad.bin").unlink(missing_ok=True)
+
     cases = sorted(p.stem for p in CASES.glob("*.cfg"))
     rng = np.random.default_rng(20240)  # robot_safety.cfg:34 seed
     for c in cases:

@@ -1,0 +1,142 @@
+"""Host front end and C-ABI boundary (no GPU needed): the shared library loads
+and exports every function include/gridmdp_b200.h declares; sizes, windows and
+memory estimates equal the reference's for every bundled config; config and
+expression errors carry the reference's codes; compute without a device fails
+loudly (no CPU fallback)."""
+import ctypes
+import subprocess
+
+import numpy as np
+import pytest
+
+import golden_io as G
+from paper_2005_06191_b200 import _capi
+from paper_2005_06191_b200 import gridmdp as g
+
+MAN = G.manifest()
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(str(_capi.LIB_PATH))
+    declared = _capi.declared_functions()
+    assert len(declared) >= 35
+    missing = [f for f in declared if not hasattr(lib, f)]
+    assert not missing, missing
+    assert set(declared) == set(_capi.SIGNATURES), set(declared) ^ set(_capi.SIGNATURES)
+
+
+@pytest.mark.parametrize("name", sorted(MAN["estimate"]))
+def test_sizes_match_reference(name):
+    e = MAN["estimate"][name]
+    m = g.parse_config(e["config"], name)
+    s = m.sizes()
+    want = e["sizes"]
+    assert (s.n_states, s.n_inputs, s.n_disturbances, s.rows, s.row_width) == (
+        want["states"], want["inputs"], want["disturbances"], want["rows"], want["row_width"])
+    assert g.window_extents(m) == want["window"]
+    assert g.memory_estimate(m) == want["memory_estimate_bytes"]
+
+
+def test_known_windows():
+    # test_abstraction.cpp:111-122 (degenerate), :212-230 (multiplicative -> full rows)
+    assert g.window_extents(g.load_config(str(G.case_cfg("degenerate")))) == [1]
+    assert g.window_extents(g.load_config(str(G.case_cfg("mult1d")))) == [5]
+    m = g.make_model(g.make_grid([0.0], [1.0], [0.5]), g.make_grid([0.0], [0.0], [1.0]), None, ["x0 + u0"],
+                     g.NoiseSpec.normal([1.0], 1e-3, "multiplicative"))
+    assert g.window_extents(m) == [3] and g.memory_estimate(m) == 3 * 3 * 8 + 3 * 8 + 4096
+
+
+def test_memory_estimate_overflow_is_memory_error():
+    # test_abstraction.cpp:361-366
+    m = g.make_model(g.make_grid([0.0], [1e7], [1.0]), g.make_grid([0.0], [1e6], [1.0]), None, ["x0 + u0"],
+                     g.NoiseSpec.normal([1.0], 0.0))
+    with pytest.raises(g.MemoryError):
+        g.memory_estimate(m)
+
+
+@pytest.mark.parametrize("text,code,needle", [
+    ("states.dim = 1\n", "ConfigError", "statement must end with ';'"),
+    ("states.dim = 1;\nstates.dim = 2;\n", "ConfigError", "duplicate key 'states.dim'"),
+    ("states.dim = 1;\n", "ConfigError", "missing mandatory key 'states.lb'"),
+])
+def test_config_errors(text, code, needle):
+    with pytest.raises(getattr(g, code)) as ei:
+        g.parse_config(text, "bad.cfg")
+    assert needle in str(ei.value)
+
+
+def _tiny(**repl):
+    text = (G.CASES / "tiny.cfg").read_text()
+    for a, b in repl.items():
+        text = text.replace(a, b)
+    return text
+
+
+@pytest.mark.parametrize("name", sorted(MAN["errors"]))
+def test_cli_errors_match_reference(name, tmp_path):
+    """Same exit code and message as the reference CLI for bad configurations
+    (config.cpp, expr.cpp parser, grid/noise/spec validation)."""
+    e = MAN["errors"][name]
+    cfg = tmp_path / "bad.cfg"
+    cfg.write_text(e["config"])
+    r = _cli("synthesize", "-c", cfg, "-o", tmp_path / "r.bin")
+    assert r.returncode == e["rc"]
+    assert r.stderr.strip().replace(str(cfg), "<cfg>") == e["stderr"]
+
+
+def test_dynamics_image_host_evaluator():
+    # test_abstraction.cpp:85-88: robot mu at (x=0, nu=(0.7,0.8), w=0)
+    m = g.load_config(str(G.case_cfg("ref_robot_safety_T2")))
+    # robot_safety input pitch 0.2: nu=(0.6, 0.8) -> indices (8, 9); x=(0,0) -> 20*41+20; w=0 -> 5
+    ix, iu, iw = 20 * 41 + 20, 8 * 11 + 9, 5
+    mu = m.dynamics_image((ix * 121 + iu) * 11 + iw)
+    assert abs(mu[0] - 10 * 0.6 * np.cos(0.8)) <= 1e-12 and abs(mu[1] - 10 * 0.8 * np.sin(0.8)) <= 1e-12
+
+
+def test_compute_without_device_fails_loudly():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a CUDA device is present")
+    m = g.load_config(str(G.case_cfg("tiny")))
+    with pytest.raises(g.CudaError, match="no CPU fallback"):
+        g.synthesize(m)
+
+
+def _cli(*args):
+    return subprocess.run([str(_capi.CLI_PATH), *map(str, args)], capture_output=True, text=True)
+
+
+def test_cli_estimate_mem_matches_reference():
+    for name in ("robot_safety", "bmw7", "traffic5"):
+        cfg = MAN["estimate"][name]["config"]
+        p = G.GOLDEN / "out" / f"_{name}.cfg"
+        p.write_text(cfg)
+        try:
+            r = _cli("estimate-mem", "-c", p)
+        finally:
+            p.unlink()
+        assert r.returncode == 0, r.stderr
+        s = MAN["estimate"][name]["sizes"]
+        for key in ("states", "inputs", "disturbances", "state_input_pairs", "rows", "row_width"):
+            assert f"{key}: {s[key]}\n" in r.stdout
+        assert f"memory_estimate_bytes: {s['memory_estimate_bytes']}\n" in r.stdout
+
+
+def test_cli_exit_codes(tmp_path):
+    # test_cli.cpp:126-174
+    bad = tmp_path / "bad.cfg"
+    bad.write_text("states.dim = 1\n")
+    assert _cli("estimate-mem", "-c", bad).returncode == 2
+    assert _cli("estimate-mem", "-c", "/nonexistent/nope.cfg").returncode == 5
+    t = tmp_path / "t.cfg"
+    t.write_text(_tiny())
+    r = _cli("synthesize", "-c", t, "--mode", "matrix", "--mem-budget", "64")
+    assert r.returncode == 3 and "ofa" in r.stderr
+    r = _cli("synthesize", "-c", t, "--time-steps", "5", "-o", tmp_path / "r.bin")
+    assert "time_steps: 5" in r.stdout
+    d = tmp_path / "d.cfg"
+    d.write_text(_tiny(**{"0.7*x0 + 0.4*u0": "1/x0"}))
+    r = _cli("abstract", "-c", d)
+    import torch
+    assert r.returncode == (4 if torch.cuda.is_available() else 1)

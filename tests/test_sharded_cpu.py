@@ -1,0 +1,91 @@
+"""Multi-process orchestration of the sharded synthesis (paper_2005_06191_b200/
+sharded.py) on CPU with the gloo backend, world_size 2: state shards, one
+all-gather of V per backward step, gathered policies. The per-shard compute
+is the oracle (a CPU backend injected by the test), so the result must be
+bit-identical to the single-process oracle and therefore to the reference."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import golden_io as G
+from oracle import oracle_py as O
+from paper_2005_06191_b200 import sharded as S
+
+
+class OracleBackend:
+    """Shard compute on the CPU oracle (tests only)."""
+
+    def __init__(self, om: O.OracleModel):
+        self.om = om
+
+    def build(self, x0, x1):
+        nuw = self.om.n_u * self.om.n_w
+        o, p = self.om.build_matrix(x0 * nuw, x1 * nuw)
+        t0 = None
+        if self.om.reach:
+            self.om.mask(o, p)
+            t0 = self.om.target_hit(x0 * nuw, x1 * nuw)
+        return (o, p, t0)
+
+    def step(self, tm, x0, x1, v_next, v_out, pol, wst):
+        kw = {}
+        if tm is not None:
+            kw = dict(origins=tm[0], probs=tm[1], t0x=tm[2])
+        vo, p, w, _ = self.om.bellman_step(v_next[: self.om.n_x].numpy(), x0, x1, **kw)
+        n = x1 - x0
+        v_out[:n] = torch.from_numpy(vo)
+        pol[:n] = torch.from_numpy(p.astype(np.int32))
+        wst[:n] = torch.from_numpy(w.astype(np.int32))
+
+
+def _worker(rank, world, port, case, matrix, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    e = G.manifest()["cases"][case]
+    om = O.load(str(G.case_cfg(case)), **G.case_overrides(e))
+    vals, pol, wst = S.synthesize_sharded(OracleBackend(om), om.n_x, om.horizon, om.reach, matrix,
+                                          torch.device("cpu"))
+    if rank == 0:
+        q.put((vals.numpy().copy(), pol.numpy().copy(), wst.numpy().copy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("case,matrix", [("fixture2d_ra", True), ("fixture2d_ra", False),
+                                         ("ref_vehicle3_desk", False), ("exp_dist", True)])
+def test_two_rank_sharded_synthesis_is_bit_identical(case, matrix):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, case, matrix, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    vals, pol, wst = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    ref = G.golden_results(case)
+    assert np.array_equal(vals.T.view(np.uint64), np.ascontiguousarray(ref["values"]).view(np.uint64))
+    assert np.array_equal(pol.T.astype(np.uint32), ref["policy"])
+    assert np.array_equal(wst.T.astype(np.uint32), ref["worst"])
+
+
+def test_shard_plan_covers_states_exactly():
+    for n_x in (1, 7, 81, 741393):
+        for world in (1, 2, 3, 8):
+            plans = [S.ShardPlan(n_x, world, r) for r in range(world)]
+            covered = sum(p.x1 - p.x0 for p in plans)
+            assert covered == n_x
+            assert all(p.x0 == min(n_x, r * p.per) for r, p in enumerate(plans))
+            assert plans[-1].x1 == n_x or n_x < world
