@@ -535,15 +535,18 @@ __device__ __forceinline__ double row_dot(const GmDev& D, int lane, int tpr, con
     Walk w;
     w.init(D, lane, tpr);
     const double* pp = prow + lane;
+    int pi = qo + lane; // MODE 3: stored row staged in shared memory at g_sm[qo]
     const int* si = sm_ints();
     double s = 0.0;
     auto term = [&](double& p, double& v) {
         if (MODE == 0) p = __ldcs(pp);
         else if (MODE == 1) p = g_sm[qo + w.L] * g_sm[mlo + w.k];
-        else p = (g_sm[po + w.a] * g_sm[mmo + w.j]) * g_sm[mlo + w.k];
+        else if (MODE == 2) p = (g_sm[po + w.a] * g_sm[mmo + w.j]) * g_sm[mlo + w.k];
+        else p = g_sm[pi];
         const int off = (LS ? si[lo + w.L] : __ldg(gl + w.L)) + w.k;
         v = ldg_at(vb, off);
         pp += tpr;
+        pi += tpr;
         w.template next<MODE == 2>();
     };
     const int n_full = n_it - n_it % U;
@@ -763,7 +766,7 @@ __global__ void __launch_bounds__(kThreads) k_expect_ofa(GmDev D, long long nrow
 // (evict-first, 8 loads in flight per lane) and gather V at the row's origin.
 template <bool LS>
 __global__ void __launch_bounds__(kThreads) k_expect_matrix(GmDev D, long long row0, long long r_lo,
-                                                           long long r_hi, const double* __restrict__ probs,
+                                                           long long r_hi, int pf, const double* __restrict__ probs,
                                                            const long long* __restrict__ origins,
                                                            const double* __restrict__ t0x,
                                                            const double* __restrict__ V,
@@ -782,7 +785,22 @@ __global__ void __launch_bounds__(kThreads) k_expect_matrix(GmDev D, long long r
     const long long total_groups = static_cast<long long>(gridDim.x) * groups;
     const long long iters = (nrows + total_groups - 1) / total_groups;
     const long long nuw = D.n_u * D.n_w;
+    // L2 prefetch of the CTA's block `pf` iterations ahead (one bulk prefetch per
+    // block of `groups` contiguous rows): the row loads below then hit L2
+    auto prefetch = [&](long long it2) {
+        const long long ra = (it2 * gridDim.x + blockIdx.x) * groups;
+        if (ra >= nrows) return;
+        const long long rz = ra + groups < nrows ? ra + groups : nrows;
+        const uintptr_t a = reinterpret_cast<uintptr_t>(probs + (r_lo + ra) * D.R) & ~uintptr_t(15);
+        const uintptr_t z = reinterpret_cast<uintptr_t>(probs + (r_lo + rz) * D.R) & ~uintptr_t(15);
+        if (z > a)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(static_cast<uint32_t>(z - a))
+                         : "memory");
+    };
+    if (pf > 0 && threadIdx.x == 0)
+        for (int k = 0; k < pf; ++k) prefetch(k);
     for (long long it = 0; it < iters; ++it) {
+        if (pf > 0 && threadIdx.x == 0) prefetch(it + pf);
         const long long rl = (it * gridDim.x + blockIdx.x) * groups + g; // local row
         const bool valid = rl < nrows;
         const long long r = r_lo + rl; // row inside the matrix
@@ -796,6 +814,139 @@ __global__ void __launch_bounds__(kThreads) k_expect_matrix(GmDev D, long long r
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Stage (ii), stored matrix, bulk-async staged (Blackwell TMA bulk copies):
+// each CTA owns a contiguous range of row "stages" (one row per row group);
+// thread 0 streams stage k+NS into a shared-memory ring slot with one
+// cp.async.bulk (mbarrier transaction count) while the groups consume stage k
+// from shared memory and gather V from L2. HBM streaming no longer waits on the
+// V-gather latency. Same canonical per-lane order as every other row kernel.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx_arrive(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+struct BulkPlan {
+    int ns;           // ring slots
+    int slot_dbl;     // doubles per slot (16-byte multiple)
+    int stages_per_cta;
+    long long n_stages;
+};
+
+template <bool LS>
+__global__ void __launch_bounds__(kThreads) k_expect_matrix_bulk(GmDev D, long long row0, long long r_lo,
+                                                                long long r_hi, BulkPlan bp,
+                                                                const double* __restrict__ probs,
+                                                                const long long* __restrict__ origins,
+                                                                const double* __restrict__ t0x,
+                                                                const double* __restrict__ V,
+                                                                double* __restrict__ v_in) {
+    const int tpr = D.tpr;
+    const int groups = kThreads / tpr;
+    const int g = threadIdx.x / tpr, lane = threadIdx.x - g * tpr;
+    const int R = static_cast<int>(D.R);
+    // shared layout (doubles): [ns slots][red 8][mbarriers ns][lines (ints)]
+    const int offRed = bp.ns * bp.slot_dbl;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(g_sm + offRed + kThreads / 32);
+    const int offL = 2 * (offRed + kThreads / 32 + bp.ns);
+    if (LS) {
+        int* si = reinterpret_cast<int*>(g_sm);
+        for (int c = threadIdx.x; c < D.n_lines; c += blockDim.x) si[offL + c] = D.line_off[c];
+    }
+    const bool reach = D.spec_kind != GM_SPEC_SAFETY;
+    const long long nuw = D.n_u * D.n_w;
+    const long long nrows = r_hi - r_lo;
+    const long long s0 = static_cast<long long>(blockIdx.x) * bp.stages_per_cta;
+    const long long s1 = s0 + bp.stages_per_cta < bp.n_stages ? s0 + bp.stages_per_cta : bp.n_stages;
+    const int my = s1 > s0 ? static_cast<int>(s1 - s0) : 0;
+
+    // producer: stage k covers local rows [k*groups, min(nrows, (k+1)*groups)); it is
+    // loaded as the 16-byte aligned superset of its bytes; skipped when every row
+    // of the stage belongs to an absorbing state (those rows are never read)
+    auto issue = [&](int it) {
+        const long long st = s0 + it;
+        const long long ra = st * groups, rz = (ra + groups < nrows ? ra + groups : nrows);
+        uint64_t* bar = bars + (it % bp.ns);
+        bool live = true;
+        if (reach && D.absorb != nullptr) {
+            live = false;
+            for (long long x = (row0 + r_lo + ra) / nuw; x <= (row0 + r_lo + rz - 1) / nuw; ++x)
+                if (!D.absorb[x]) { live = true; break; }
+        }
+        if (!live) { mbar_arrive(bar); return; }
+        const char* src = reinterpret_cast<const char*>(probs + (r_lo + ra) * D.R);
+        const char* a = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15));
+        const char* z = src + (rz - ra) * D.R * 8;
+        const uint32_t bytes = static_cast<uint32_t>(((z - a) + 15) & ~15);
+        mbar_expect_tx_arrive(bar, bytes);
+        bulk_g2s(g_sm + (it % bp.ns) * bp.slot_dbl, a, bytes, bar);
+    };
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < bp.ns; ++s) mbar_init(bars + s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int it = 0; it < bp.ns && it < my; ++it) issue(it);
+    }
+    __syncthreads();
+    for (int it = 0; it < my; ++it) {
+        const int slot = it % bp.ns;
+        mbar_wait(bars + slot, static_cast<uint32_t>((it / bp.ns) & 1));
+        const long long ra = (s0 + it) * groups;
+        const long long rl = ra + g; // local row of this group
+        const bool valid = rl < nrows;
+        const long long r = r_lo + rl;
+        bool skip = !valid;
+        if (valid && reach && D.absorb != nullptr) skip = D.absorb[(row0 + r) / nuw];
+        double s = 0.0;
+        if (!skip) {
+            // offset of the stage's first row inside the aligned superset (0 or 1 double)
+            const int mis = static_cast<int>((reinterpret_cast<uintptr_t>(probs + (r_lo + ra) * D.R) & 15) >> 3);
+            const int base = slot * bp.slot_dbl + mis + g * R;
+            s = row_dot<3, 8, LS>(D, lane, tpr, nullptr, base, 0, 0, 0, V + origins[r], D.line_off, offL);
+        }
+        s = group_reduce(s, tpr, offRed, g * tpr);
+        if (valid && lane == 0) v_in[rl] = skip ? 0.0 : (reach ? s + t0x[r] : s);
+        __syncthreads(); // every group is done with this slot
+        if (threadIdx.x == 0 && it + bp.ns < my) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(it + bp.ns);
+        }
+    }
+}
 
 // min over w (strict <, ascending), then max over u (strict >, ascending):
 // lowest-index ties (synthesis.cpp:112-142). L lanes per state.
@@ -1067,15 +1218,37 @@ void expect_matrix(const GmDev& D, long long row0, long long r_lo, long long r_h
     if (r_hi <= r_lo) return;
     const size_t table = static_cast<size_t>(D.n_lines) * sizeof(int);
     const bool in_smem = table <= 48 * 1024;
-    const size_t smem = (kThreads / 32) * sizeof(double) + (in_smem ? table : 0);
     const int groups = kThreads / D.tpr;
     const long long blocks_needed = (r_hi - r_lo + groups - 1) / groups;
+    // bulk-async staged kernel when a stage (one row per group) fits a 2-slot ring
+    // GM_MATRIX_KERNEL=bulk selects the shared-memory ring variant; the default
+    // streams rows straight to registers with a bulk L2 prefetch GM_PREFETCH blocks ahead
+    static const char* force = std::getenv("GM_MATRIX_KERNEL");
+    static const char* pfs = std::getenv("GM_PREFETCH");
+    const int pf = pfs ? std::atoi(pfs) : 0;
+    const bool allow_bulk = force && std::string(force) == "bulk";
+    const size_t slot = ((static_cast<size_t>(groups) * D.R * 8 + 16) + 15) / 16 * 16;
+    const size_t tail = (kThreads / 32) * sizeof(double) + 4 * sizeof(uint64_t) + (in_smem ? table : 0);
+    if (allow_bulk && in_smem && 2 * slot + tail <= kHardSmem) {
+        BulkPlan bp;
+        bp.ns = (3 * slot + tail <= kHardSmem && 2 * slot + tail > 112 * 1024) ? 3 : 2;
+        bp.slot_dbl = static_cast<int>(slot / 8);
+        const size_t smem = bp.ns * slot + tail;
+        allow_smem(k_expect_matrix_bulk<true>, smem);
+        bp.n_stages = blocks_needed;
+        const int grid = resident_grid(k_expect_matrix_bulk<true>, smem, bp.n_stages);
+        bp.stages_per_cta = static_cast<int>((bp.n_stages + grid - 1) / grid);
+        k_expect_matrix_bulk<true><<<grid, kThreads, smem, s>>>(D, row0, r_lo, r_hi, bp, probs, origins, t0x, V, v_in);
+        check_launch("expect_matrix_bulk");
+        return;
+    }
+    const size_t smem = (kThreads / 32) * sizeof(double) + (in_smem ? table : 0);
     if (in_smem) {
         k_expect_matrix<true><<<resident_grid(k_expect_matrix<true>, smem, blocks_needed), kThreads, smem, s>>>(
-            D, row0, r_lo, r_hi, probs, origins, t0x, V, v_in);
+            D, row0, r_lo, r_hi, pf, probs, origins, t0x, V, v_in);
     } else {
         k_expect_matrix<false><<<resident_grid(k_expect_matrix<false>, smem, blocks_needed), kThreads, smem, s>>>(
-            D, row0, r_lo, r_hi, probs, origins, t0x, V, v_in);
+            D, row0, r_lo, r_hi, pf, probs, origins, t0x, V, v_in);
     }
     check_launch("expect_matrix");
 }
