@@ -151,12 +151,20 @@ gm_code gm_build_target_hit(gm_model* m, int64_t row_begin, int64_t row_end, dou
  * of origins (int64) and probabilities (row-major R doubles) to host memory. */
 gm_code gm_matrix_copy_rows(const gm_matrix* tm, int64_t row_begin, int64_t row_end,
                             int64_t* origins_out, double* probs_out, gm_status* st);
+/* Copies the target-hit vector a shard build fused into the matrix (rows as above);
+ * GM_ERR_CONFIG when the matrix carries none. */
+gm_code gm_matrix_copy_t0x(const gm_matrix* tm, int64_t row_begin, int64_t row_end, double* t0x_out,
+                           gm_status* st);
 /* Device pointers and row range of a matrix (for stream-level callers). */
 gm_code gm_matrix_info(const gm_matrix* tm, int64_t* row_begin, int64_t* row_end,
                        int64_t* row_width, const double** d_probs, const int64_t** d_origins,
                        gm_status* st);
 /* write_matrix (io.hpp:19, io.cpp:236-256): the raw `gridmdp-matrix 1` container. */
 gm_code gm_matrix_write(const gm_matrix* tm, const gm_model* m, const char* path, gm_status* st);
+/* export_prism (io.hpp:21, io.cpp:289-317): PRISM explicit transitions
+ * "n_states n_rows n_transitions" then "src choice dst prob" for prob > 0, streamed
+ * from the device-resident matrix (the nonzero count is reduced on the device). */
+gm_code gm_matrix_write_prism(const gm_matrix* tm, const gm_model* m, const char* path, gm_status* st);
 void gm_matrix_free(gm_matrix* tm);
 
 /* ------------------------------------------------------------ stage (ii) */
@@ -212,6 +220,10 @@ gm_code gm_result_from_tables(const gm_model* m, const double* values, const uin
 /* write_results (io.hpp:13, io.cpp:142-179): the `gridmdp-results 1` container. */
 gm_code gm_result_write(const gm_result* r, const char* path, gm_status* st);
 void gm_result_free(gm_result* r);
+
+/* Large device blocks (>= 64 MB, e.g. stored matrices) are kept for reuse after
+ * release; this returns them to the driver. */
+void gm_release_cached_memory(void);
 
 #ifdef __cplusplus
 }

@@ -94,6 +94,11 @@ int run(const Args& a) {
         write_matrix(tm, a.out);
         return 0;
     }
+    if (a.cmd == "prism") { // export_prism (io.cpp:289-317), like `gridmdp export-prism`
+        const TransitionMatrix tm = build_matrix(m, cfg.threads);
+        export_prism(tm, a.out);
+        return 0;
+    }
     if (a.cmd == "masked-matrix") { // masked as synthesize_with_matrix does
         const Spec spec = build_spec(cfg);
         TransitionMatrix tm = build_matrix(m, cfg.threads);

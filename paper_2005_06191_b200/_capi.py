@@ -100,9 +100,11 @@ SIGNATURES = {
     "gm_mask_absorbing": (C.c_int, [_VP, _VP, _PS]),
     "gm_build_target_hit": (C.c_int, [_VP, _I64, _I64, _VP, _PS]),
     "gm_matrix_copy_rows": (C.c_int, [_VP, _I64, _I64, _VP, _VP, _PS]),
+    "gm_matrix_copy_t0x": (C.c_int, [_VP, _I64, _I64, _VP, _PS]),
     "gm_matrix_info": (C.c_int, [_VP, C.POINTER(_I64), C.POINTER(_I64), C.POINTER(_I64), C.POINTER(_VP),
                                  C.POINTER(_VP), _PS]),
     "gm_matrix_write": (C.c_int, [_VP, _VP, C.c_char_p, _PS]),
+    "gm_matrix_write_prism": (C.c_int, [_VP, _VP, C.c_char_p, _PS]),
     "gm_matrix_free": (None, [_VP]),
     "gm_bellman_step": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _PS]),
     "gm_step_device": (C.c_int, [_VP, _VP, _I64, _I64, _VP, _VP, _VP, _VP, _VP, _PS]),
@@ -118,6 +120,7 @@ SIGNATURES = {
     "gm_result_from_tables": (C.c_int, [_VP, _VP, _VP, _VP, C.POINTER(_VP), _PS]),
     "gm_result_write": (C.c_int, [_VP, C.c_char_p, _PS]),
     "gm_result_free": (None, [_VP]),
+    "gm_release_cached_memory": (None, []),
 }
 
 
@@ -211,4 +214,4 @@ def declared_functions(header: str | os.PathLike | None = None) -> list[str]:
 
     h = Path(header) if header else PKG_DIR.parent / "include" / "gridmdp_b200.h"
     text = h.read_text()
-    return sorted(set(re.findall(r"\b(gm_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(gm_[a-z0-9_]+)\s*\(", text)))

@@ -9,9 +9,11 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <charconv>
 #include <climits>
 #include <cstring>
 #include <fstream>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <sstream>
@@ -88,24 +90,95 @@ void ck(cudaError_t e, const char* what) {
     }
 }
 
+// Large device blocks (stored matrices: tens of GB) are cached on release and
+// reused by the next allocation of a similar size on the same device, so
+// repeated synthesize/build calls do not pay cudaMalloc/cudaFree of the matrix
+// (hundreds of ms at 100 GB). On allocation failure the cache is flushed first.
+constexpr size_t kCacheMin = 64ULL << 20;
+std::mutex g_cache_mu;
+std::multimap<size_t, std::pair<int, void*>> g_cache; // bytes -> (device, ptr)
+
+void flush_cache() {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto& kv : g_cache) {
+        cudaSetDevice(kv.second.first);
+        cudaFree(kv.second.second);
+    }
+    g_cache.clear();
+    cudaSetDevice(cur);
+}
+
+size_t cached_bytes() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    size_t s = 0;
+    for (auto& kv : g_cache)
+        if (kv.second.first == dev) s += kv.first;
+    return s;
+}
+
+void* dev_alloc(size_t bytes, size_t& got, const char* what) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (bytes >= kCacheMin) {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        for (auto it = g_cache.lower_bound(bytes); it != g_cache.end() && it->first <= bytes + bytes / 4; ++it) {
+            if (it->second.first != dev) continue;
+            void* p = it->second.second;
+            got = it->first;
+            g_cache.erase(it);
+            return p;
+        }
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        flush_cache();
+        e = cudaMalloc(&p, bytes);
+    }
+    ck(e, what);
+    got = bytes;
+    return p;
+}
+
+void dev_free(void* p, size_t bytes) {
+    if (!p) return;
+    if (bytes >= kCacheMin) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceSynchronize(); // no queued kernel may still use the block once it is reusable
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        g_cache.emplace(bytes, std::make_pair(dev, p));
+        return;
+    }
+    cudaFree(p);
+}
+
 template <class T>
 struct DevBuf {
     T* p = nullptr;
-    size_t n = 0;
+    size_t n = 0;      // elements usable
+    size_t bytes = 0;  // allocated bytes
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() { release(); }
     void release() {
-        if (p) cudaFree(p);
+        dev_free(p, bytes);
         p = nullptr;
         n = 0;
+        bytes = 0;
     }
     void ensure(size_t count, const char* what) {
         if (count <= n && p) return;
         release();
         if (count == 0) count = 1;
-        ck(cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T)), what);
+        // +16 bytes: bulk async copies may read a 16-byte aligned superset of the last row
+        p = static_cast<T*>(dev_alloc(count * sizeof(T) + 16, bytes, what));
         n = count;
     }
 };
@@ -806,6 +879,18 @@ gm_code gm_matrix_copy_rows(const gm_matrix* tm, int64_t r0, int64_t r1, int64_t
     });
 }
 
+gm_code gm_matrix_copy_t0x(const gm_matrix* tm, int64_t r0, int64_t r1, double* t0x, gm_status* st) {
+    return guarded(st, [&] {
+        if (!tm->has_t0x) throw ConfigErr("matrix carries no target-hit vector");
+        if (r0 < tm->row_begin || r1 > tm->row_end || r0 > r1) throw std::out_of_range("matrix rows out of range");
+        ck(cudaSetDevice(tm->device), "cudaSetDevice");
+        if (r1 > r0)
+            ck(cudaMemcpy(t0x, tm->t0x.p + (r0 - tm->row_begin), static_cast<size_t>(r1 - r0) * 8,
+                          cudaMemcpyDeviceToHost),
+               "t0x");
+    });
+}
+
 gm_code gm_matrix_info(const gm_matrix* tm, int64_t* rb, int64_t* re, int64_t* R, const double** probs,
                        const int64_t** origins, gm_status* st) {
     return guarded(st, [&] {
@@ -850,6 +935,73 @@ gm_code gm_matrix_write(const gm_matrix* tm, const gm_model* m, const char* path
             buf.resize(static_cast<size_t>(n * tm->R));
             ck(cudaMemcpy(buf.data(), tm->probs.p + r * tm->R, buf.size() * 8, cudaMemcpyDeviceToHost), "probs");
             for (double v : buf) put_f64(os, v);
+        }
+        if (!os) throw IoErr(std::string("failed while writing '") + path + "'");
+    });
+}
+
+gm_code gm_matrix_write_prism(const gm_matrix* tm, const gm_model* m, const char* path, gm_status* st) {
+    return guarded(st, [&] {
+        // export_prism, io.cpp:289-317
+        if (tm->row_begin != 0 || tm->row_end != m->M.rows())
+            throw IoErr("export_prism needs the whole matrix (rows 0..rows)");
+        std::ofstream os(path);
+        if (!os) throw IoErr(std::string("cannot open '") + path + "' for writing");
+        ck(cudaSetDevice(tm->device), "cudaSetDevice");
+        const Model& M = m->M;
+        const int64_t rows = tm->row_end - tm->row_begin, R = tm->R;
+        DevBuf<unsigned long long> cnt;
+        cnt.ensure(1, "count");
+        const unsigned long long transitions = gmk::count_positive(tm->probs.p, rows * R, cnt.p, nullptr);
+        const int64_t choices = M.n_u() * M.n_w();
+        os << M.n_x() << ' ' << rows << ' ' << transitions << '\n';
+        const Grid& g = M.X;
+        const int n = g.dim();
+        std::vector<long long> org;
+        std::vector<double> buf;
+        const int64_t blk = std::max<int64_t>(1, (64LL << 20) / 8 / std::max<int64_t>(R, 1));
+        std::string line;
+        char num[64];
+        for (int64_t r0 = 0; r0 < rows; r0 += blk) {
+            const int64_t nb = std::min(blk, rows - r0);
+            org.resize(static_cast<size_t>(nb));
+            buf.resize(static_cast<size_t>(nb * R));
+            ck(cudaMemcpy(org.data(), tm->origins.p + r0, org.size() * 8, cudaMemcpyDeviceToHost), "origins");
+            ck(cudaMemcpy(buf.data(), tm->probs.p + r0 * R, buf.size() * 8, cudaMemcpyDeviceToHost), "probs");
+            for (int64_t i = 0; i < nb; ++i) {
+                const int64_t r = r0 + i, src = r / choices, choice = r % choices;
+                // visit_slab (abstraction.hpp:130-149): row-major over the extents
+                int64_t o[GMD_MAXD], j[GMD_MAXD] = {0}, rem = org[static_cast<size_t>(i)], flat = 0;
+                for (int d = 0; d < n; ++d) {
+                    o[d] = rem / g.stride[d];
+                    rem %= g.stride[d];
+                    flat += o[d] * g.stride[d];
+                }
+                const double* row = buf.data() + i * R;
+                for (int64_t k = 0;; ) {
+                    if (row[k] > 0.0) {
+                        line = std::to_string(src);
+                        line += ' ';
+                        line += std::to_string(choice);
+                        line += ' ';
+                        line += std::to_string(flat);
+                        line += ' ';
+                        auto res = std::to_chars(num, num + sizeof num, row[k]);
+                        line.append(num, res.ptr);
+                        line += '\n';
+                        os << line;
+                    }
+                    ++k;
+                    int d = n - 1;
+                    for (; d >= 0; --d) {
+                        flat += g.stride[d];
+                        if (++j[d] < M.extents[d]) break;
+                        flat -= M.extents[d] * g.stride[d];
+                        j[d] = 0;
+                    }
+                    if (d < 0) break;
+                }
+            }
         }
         if (!os) throw IoErr(std::string("failed while writing '") + path + "'");
     });
@@ -946,6 +1098,7 @@ gm_code gm_synthesize(gm_model* m, gm_result** out, gm_status* st) {
             prepare(m);
             size_t free_b = 0, total_b = 0;
             ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+            free_b += cached_bytes(); // released matrices kept for reuse count as free
             const uint64_t dev_need = need + static_cast<uint64_t>(m->M.rows()) * 16;
             if (dev_need > static_cast<uint64_t>(free_b)) {
                 std::ostringstream os;
@@ -1094,5 +1247,7 @@ gm_code gm_result_write(const gm_result* r, const char* path, gm_status* st) {
 }
 
 void gm_result_free(gm_result* r) { delete r; }
+
+void gm_release_cached_memory(void) { flush_cache(); }
 
 } // extern "C"

@@ -612,8 +612,8 @@ __global__ void __launch_bounds__(kThreads) k_expand(GmDev D, long long nrows, i
 // (warp per row, coalesced evict-first stores). The row prologue of one CTA
 // overlaps the store phase of the others on the same SM.
 template <int TAB>
-__global__ void __launch_bounds__(kThreads) k_build(GmDev D, long long row0, long long nrows, int rb,
-                                                   GmFastDiv div_rb, long long* __restrict__ origin_out,
+__global__ void __launch_bounds__(kThreads, 4) k_build(GmDev D, long long row0, long long nrows, int rb,
+                                                   GmFastDiv div_rb, int rowbuf_off, long long* __restrict__ origin_out,
                                                    double* __restrict__ t0x_out, double* __restrict__ probs,
                                                    unsigned long long* err) {
     const Layout Y(D, rb, TAB);
@@ -633,6 +633,18 @@ __global__ void __launch_bounds__(kThreads) k_build(GmDev D, long long row0, lon
     const int mw = Y.mw;
     const int R = static_cast<int>(D.R);
     const bool reach = D.spec_kind != GM_SPEC_SAFETY;
+    Walk wk0;
+    wk0.init(D, lane, 32);
+    // store-walk table (TAB_Q, W_last <= 64): tab[k0][l] = ((k0 + l) / Wl) | ((k0 + l) % Wl) << 16
+    const bool use_tab = false; // table-driven store walk: measured slower (30.0 vs 25.6 ms on C2b)
+    int* stab = reinterpret_cast<int*>(g_sm + offProg + D.n_ins + D.n_lits);
+    const int c32L = D.div_Wl.div(32), c32k = 32 - c32L * D.Wl;
+    if (TAB == TAB_Q && use_tab)
+        for (int c = threadIdx.x; c < D.Wl * 32; c += blockDim.x) {
+            const int k0 = c >> 5, l = c & 31, e = k0 + l;
+            const int dL = D.div_Wl.div(e);
+            stab[c] = dL | ((e - dL * D.Wl) << 16);
+        }
     for (long long b0 = static_cast<long long>(blockIdx.x) * rb; b0 < nrows;
          b0 += static_cast<long long>(gridDim.x) * rb) {
         __syncthreads();
@@ -697,14 +709,72 @@ __global__ void __launch_bounds__(kThreads) k_build(GmDev D, long long row0, lon
         __syncthreads();
         stage_tables(D, Y, rb, TAB);
         __syncthreads();
+        if (rowbuf_off >= 0) {
+            // fill_product (abstraction.cpp:150-159) into a per-warp shared-memory row,
+            // line by line (q = Q[L], then q*ml[k]); one bulk async store per row
+            const int stride = (R + 3) & ~1; // even: every warp's row starts 16-byte aligned
+            double* buf = g_sm + rowbuf_off + warp * stride;
+            for (int i = warp; i < rb; i += nwarps) {
+                const long long row = b0 + i;
+                if (row >= nrows) break;
+                const int qo = Y.offQ + i * D.n_lines, po = Y.offP + i * D.P_size;
+                const int mmo = i * mw + D.mm_off, mlo = i * mw + D.ml_off;
+                double* out = probs + row * D.R;
+                const int head = (reinterpret_cast<uintptr_t>(out) & 15) ? 1 : 0; // element t at buf[t + head]
+                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                __syncwarp();
+                const int Wl = D.Wl;
+                for (int L = lane; L < D.n_lines; L += 32) {
+                    double q;
+                    if (TAB == TAB_Q) {
+                        q = g_sm[qo + L];
+                    } else {
+                        const int a = D.div_Wm.div(L), j = L - a * D.Wm;
+                        q = g_sm[po + a] * g_sm[mmo + j];
+                    }
+                    double* dst = buf + L * Wl + head;
+                    for (int k = 0; k < Wl; ++k) dst[k] = q * g_sm[mlo + k];
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) {
+                    const int body = (R - head) & ~1;
+                    if (head) __stcs(out, buf[head]);
+                    if (R - head - body) __stcs(out + head + body, buf[2 * head + body]);
+                    if (body > 0) {
+                        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + head),
+                                     "r"(static_cast<uint32_t>(__cvta_generic_to_shared(buf + 2 * head))),
+                                     "r"(static_cast<uint32_t>(body * 8))
+                                     : "memory");
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    }
+                }
+            }
+            continue;
+        }
         for (int i = warp; i < rb; i += nwarps) { // fill_product (abstraction.cpp:150-159)
             const long long row = b0 + i;
             if (row >= nrows) break;
             const int qo = Y.offQ + i * D.n_lines, po = Y.offP + i * D.P_size;
             const int mmo = i * mw + D.mm_off, mlo = i * mw + D.ml_off;
             double* out = probs + row * D.R;
-            Walk wk;
-            wk.init(D, lane, 32);
+            if (TAB == TAB_Q && use_tab) {
+                // warp-uniform walk (L0, k0) over 32-element windows; the lane offsets come
+                // from the per-CTA table tab[k0][lane] = (dL, k) of element k0 + lane
+                int L0 = 0, k0 = 0;
+#pragma unroll 4
+                for (int t0 = 0; t0 < R; t0 += 32) {
+                    const int pk = stab[k0 * 32 + lane];
+                    if (t0 + lane < R)
+                        __stcs(out + t0 + lane, g_sm[qo + L0 + (pk & 0xffff)] * g_sm[mlo + (pk >> 16)]);
+                    k0 += c32k;
+                    const int c = k0 >= D.Wl;
+                    k0 -= c ? D.Wl : 0;
+                    L0 += c32L + c;
+                }
+                continue;
+            }
+            Walk wk = wk0; // the lane's walk is row independent (initialised once per CTA)
 #pragma unroll 4
             for (int t = lane; t < R; t += 32) {
                 const double p = TAB == TAB_Q ? g_sm[qo + wk.L] * g_sm[mlo + wk.k]
@@ -714,6 +784,7 @@ __global__ void __launch_bounds__(kThreads) k_build(GmDev D, long long row0, lon
             }
         }
     }
+    if (rowbuf_off >= 0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // Stage (ii), on the fly (synthesis.cpp:100-104 + dot_slab :18-47): row groups
@@ -1152,18 +1223,19 @@ void build(const GmDev& D, long long row0, long long nrows, long long* origin_ou
            double* probs_out, unsigned long long* d_err, cudaStream_t s) {
     if (nrows <= 0) return;
     const size_t mw = static_cast<size_t>(D.sumW + 1);
-    const size_t fixed = (kThreads / 32 + D.n_ins + D.n_lits + 2) * sizeof(double);
+    const size_t fixed = (kThreads / 32 + D.n_ins + D.n_lits + 2) * sizeof(double) +
+                         (D.Wl <= 64 ? static_cast<size_t>(D.Wl) * 32 * sizeof(int) : 0);
     const size_t extra_row = (2 * GMD_MAXD + 1) * sizeof(double) + GMD_MAXD * sizeof(int);
     const size_t q_row = (mw + D.P_size + D.n_lines) * sizeof(double) + extra_row;
     const size_t p_row = (mw + D.P_size) * sizeof(double) + extra_row;
     int tab = -1;
     long long rb = 0;
-    for (size_t budget : {kSoftSmem, kHardSmem}) {
+    for (size_t budget : {static_cast<size_t>(54 * 1024), kHardSmem}) { // 4 CTAs/SM
         for (int t : {TAB_Q, TAB_P}) {
             const size_t per = t == TAB_Q ? q_row : p_row;
             if (fixed >= budget) continue;
             const long long r = static_cast<long long>((budget - fixed) / per);
-            if (r >= (budget == kSoftSmem ? 8 : 1)) {
+            if (r >= (budget != kHardSmem ? 8 : 1)) {
                 tab = t;
                 rb = std::min<long long>(r, kThreads);
                 break;
@@ -1172,17 +1244,33 @@ void build(const GmDev& D, long long row0, long long nrows, long long* origin_ou
         if (tab >= 0) break;
     }
     if (tab < 0) throw std::runtime_error("row too wide for the device build layout");
-    const size_t smem = fixed + (tab == TAB_Q ? q_row : p_row) * static_cast<size_t>(rb);
+    size_t smem = fixed + (tab == TAB_Q ? q_row : p_row) * static_cast<size_t>(rb);
+    // bulk-store variant: one shared-memory row per warp (+ the tables of >= 16 rows)
+    static const char* bb = std::getenv("GM_BUILD_BULK");
+    const bool want_bulk = bb && bb[0] == '1'; // opt-in: measured slower than direct stores
+    int rowbuf_off = -1;
+    const size_t rowbuf = (kThreads / 32) * static_cast<size_t>((D.R + 3) & ~1LL) * sizeof(double);
+    if (want_bulk && D.R >= 32 && D.R + 2 < (1 << 20)) {
+        const size_t per = tab == TAB_Q ? q_row : p_row;
+        const size_t budget = 110 * 1024;
+        if (fixed + rowbuf + 16 * per <= budget) {
+            rb = std::min<long long>(kThreads, static_cast<long long>((budget - fixed - rowbuf) / per));
+            rb -= rb % 2;
+            const size_t tables = fixed + per * static_cast<size_t>(rb);
+            rowbuf_off = static_cast<int>(((tables + 15) / 16 * 16) / sizeof(double));
+            smem = static_cast<size_t>(rowbuf_off) * sizeof(double) + rowbuf;
+        }
+    }
     const long long batches = (nrows + rb - 1) / rb;
     const GmFastDiv drb = gm_fastdiv(static_cast<uint32_t>(rb));
     if (tab == TAB_Q) {
         allow_smem(k_build<TAB_Q>, smem);
         k_build<TAB_Q><<<resident_grid(k_build<TAB_Q>, smem, batches), kThreads, smem, s>>>(
-            D, row0, nrows, static_cast<int>(rb), drb, origin_out, t0x_out, probs_out, d_err);
+            D, row0, nrows, static_cast<int>(rb), drb, rowbuf_off, origin_out, t0x_out, probs_out, d_err);
     } else {
         allow_smem(k_build<TAB_P>, smem);
         k_build<TAB_P><<<resident_grid(k_build<TAB_P>, smem, batches), kThreads, smem, s>>>(
-            D, row0, nrows, static_cast<int>(rb), drb, origin_out, t0x_out, probs_out, d_err);
+            D, row0, nrows, static_cast<int>(rb), drb, rowbuf_off, origin_out, t0x_out, probs_out, d_err);
     }
     check_launch("build");
 }
@@ -1251,6 +1339,30 @@ void expect_matrix(const GmDev& D, long long row0, long long r_lo, long long r_h
             D, row0, r_lo, r_hi, pf, probs, origins, t0x, V, v_in);
     }
     check_launch("expect_matrix");
+}
+
+namespace {
+__global__ void k_count_positive(const double* __restrict__ p, long long n, unsigned long long* count) {
+    unsigned long long c = 0;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        c += __ldcs(p + i) > 0.0 ? 1 : 0;
+    for (int off = 16; off >= 1; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+} // namespace
+
+unsigned long long count_positive(const double* p, long long n, unsigned long long* d_count, cudaStream_t s) {
+    cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), s);
+    if (n > 0) {
+        k_count_positive<<<std::max(1, std::min(grid_for(n, kThreads), num_sms() * 8)), kThreads, 0, s>>>(p, n,
+                                                                                                       d_count);
+        check_launch("count_positive");
+    }
+    unsigned long long h = 0;
+    cudaMemcpyAsync(&h, d_count, sizeof h, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    return h;
 }
 
 void maxmin(const GmDev& D, long long x0, long long nx, const double* v_in, double* v_out,

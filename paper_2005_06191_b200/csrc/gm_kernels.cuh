@@ -61,6 +61,9 @@ void expect_matrix(const GmDev& D, long long row0, long long r_lo, long long r_h
 void maxmin(const GmDev& D, long long x0, long long nx, const double* v_in, double* v_out,
             uint32_t* pol, uint32_t* wst, cudaStream_t s);
 
+// Number of stored probabilities > 0 in n doubles (export_prism header, io.cpp:296-298).
+unsigned long long count_positive(const double* p, long long n, unsigned long long* d_count, cudaStream_t s);
+
 // mask_absorbing (abstraction.cpp:273-344) over stored rows.
 void mask(const GmDev& D, long long r_lo, long long nrows, double* probs, const long long* origins,
           const uint8_t* inT, const uint8_t* inA, const long long* axis_off, cudaStream_t s);

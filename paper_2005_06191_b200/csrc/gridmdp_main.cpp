@@ -142,6 +142,31 @@ int cmd_synthesize(const Args& a) {
     return 0;
 }
 
+int cmd_export_prism(const Args& a) {
+    // tools/gridmdp_main.cpp:142-152
+    gm_model* m = nullptr;
+    gm_sizes sz;
+    if (int rc = load(a, &m, &sz)) return rc;
+    const std::string out = gm_model_output_path(m);
+    gm_status st;
+    if (out.empty()) {
+        std::cerr << "error: export-prism needs --output or exec.output\n";
+        return 2;
+    }
+    if (sz.mem_budget != 0 && sz.memory_estimate > static_cast<uint64_t>(sz.mem_budget)) {
+        std::cerr << "error: matrix exceeds the configured budget; export needs matrix mode\n";
+        return 3;
+    }
+    if (a.device != 0 && gm_set_device(a.device, &st) != GM_OK) return fail(st);
+    gm_matrix* tm = nullptr;
+    if (gm_build_matrix(m, 0, sz.rows, &tm, &st) != GM_OK) return fail(st);
+    if (gm_matrix_write_prism(tm, m, out.c_str(), &st) != GM_OK) return fail(st);
+    std::cout << "output: " << out << "\n";
+    gm_matrix_free(tm);
+    gm_model_free(m);
+    return 0;
+}
+
 int not_in_engine(const std::string& verb) {
     std::cerr << "error: '" << verb
               << "' is outside the B200 engine's hot path (MDP construction + synthesis); use the reference CLI\n";
@@ -237,6 +262,7 @@ int main(int argc, char** argv) {
         case 0: return cmd_estimate(a);
         case 1: return cmd_abstract(a);
         case 2: return cmd_synthesize(a);
+        case 4: return cmd_export_prism(a);
         default: return not_in_engine(a.verb);
     }
 }

@@ -176,6 +176,9 @@ def main() -> None:
             f = OUT / f"{c}.matrix.bin"
             ref("matrix", "-c", cfgp, "-o", f, *extra)
             entry["files"]["matrix"] = f.name
+            f = OUT / f"{c}.prism.tra"
+            ref("prism", "-c", cfgp, "-o", f, *extra)
+            entry["files"]["prism"] = f.name
             if "spec.type = safety" not in cfgp.read_text():
                 f = OUT / f"{c}.masked.bin"
                 ref("masked-matrix", "-c", cfgp, "-o", f, *extra)
