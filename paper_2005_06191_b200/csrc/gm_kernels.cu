@@ -1019,6 +1019,180 @@ __global__ void __launch_bounds__(kThreads) k_expect_matrix_bulk(GmDev D, long l
     }
 }
 
+// ---------------------------------------------------------------------------
+// Stage (ii), stored matrix, warp-specialised: warp 8 of the CTA is a producer
+// that streams the CTA's contiguous rows, one row per ring slot, with
+// cp.async.bulk (mbarrier complete_tx); warps 0-7 form the usual row groups and
+// consume slots in order. Per-slot full/empty mbarriers replace CTA barriers,
+// so HBM streaming runs up to `ns` rows ahead of the V-gather-bound consumers.
+// ---------------------------------------------------------------------------
+
+constexpr int kWsThreads = kThreads + 32;
+
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) { mbar_wait(bar, parity); }
+
+template <bool LS>
+__global__ void __launch_bounds__(kWsThreads) k_expect_matrix_ws(GmDev D, long long row0, long long r_lo,
+                                                                long long r_hi, int ns, int slot_dbl,
+                                                                long long rows_per_cta,
+                                                                const double* __restrict__ probs,
+                                                                const long long* __restrict__ origins,
+                                                                const double* __restrict__ t0x,
+                                                                const double* __restrict__ V,
+                                                                double* __restrict__ v_in) {
+    const int tpr = D.tpr;
+    const int groups = kThreads / tpr;
+    const int R = static_cast<int>(D.R);
+    // shared layout (doubles): [ns slots][red 8][full ns][empty ns][lines (ints)]
+    const int offRed = ns * slot_dbl;
+    uint64_t* full = reinterpret_cast<uint64_t*>(g_sm + offRed + kThreads / 32);
+    uint64_t* empty = full + ns;
+    const int offL = 2 * (offRed + kThreads / 32 + 2 * ns);
+    if (LS) {
+        int* si = reinterpret_cast<int*>(g_sm);
+        for (int c = threadIdx.x; c < D.n_lines; c += blockDim.x) si[offL + c] = D.line_off[c];
+    }
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < ns; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const bool reach = D.spec_kind != GM_SPEC_SAFETY;
+    const long long nuw = D.n_u * D.n_w;
+    const long long nrows = r_hi - r_lo;
+    const long long ra = static_cast<long long>(blockIdx.x) * rows_per_cta;
+    const long long rz = ra + rows_per_cta < nrows ? ra + rows_per_cta : nrows;
+    const long long my = rz > ra ? rz - ra : 0;
+    auto absorbed = [&](long long rl) {
+        return reach && D.absorb != nullptr && D.absorb[(row0 + r_lo + rl) / nuw];
+    };
+
+    if (threadIdx.x >= kThreads) { // producer warp: flags of 32 rows at a time, lane 0 issues
+        const int pl = threadIdx.x - kThreads;
+        for (long long i0 = 0; i0 < my; i0 += 32) {
+            const bool ab = i0 + pl < my ? absorbed(ra + i0 + pl) : true;
+            const unsigned mask = __ballot_sync(0xffffffffu, ab);
+            if (pl == 0) {
+                for (int k = 0; k < 32 && i0 + k < my; ++k) {
+                    const long long i = i0 + k;
+                    const int s = static_cast<int>(i % ns);
+                    if (i >= ns) mbar_wait(empty + s, static_cast<uint32_t>(((i / ns) - 1) & 1));
+                    if ((mask >> k) & 1u) { // never read (synthesis.cpp:86-89): complete without data
+                        mbar_arrive(full + s);
+                        continue;
+                    }
+                    const long long rl = ra + i;
+                    const char* src = reinterpret_cast<const char*>(probs + (r_lo + rl) * D.R);
+                    const char* a =
+                        reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15));
+                    const uint32_t bytes = static_cast<uint32_t>(((src + R * 8 - a) + 15) & ~15);
+                    mbar_expect_tx_arrive(full + s, bytes);
+                    bulk_g2s(g_sm + s * slot_dbl, a, bytes, full + s);
+                }
+            }
+            __syncwarp();
+        }
+        return;
+    }
+
+    const int g = threadIdx.x / tpr, lane = threadIdx.x - g * tpr;
+    const long long iters = (my + groups - 1) / groups;
+    for (long long it = 0; it < iters; ++it) {
+        const long long i = it * groups + g; // row of the CTA range handled by this group
+        const bool valid = i < my;
+        double s = 0.0;
+        bool skip = true;
+        int slot = 0;
+        if (valid) {
+            slot = static_cast<int>(i % ns);
+            mbar_wait(full + slot, static_cast<uint32_t>((i / ns) & 1));
+            skip = absorbed(ra + i);
+            if (!skip) {
+                const long long r = r_lo + ra + i;
+                const int mis = static_cast<int>((reinterpret_cast<uintptr_t>(probs + r * D.R) & 15) >> 3);
+                s = row_dot<3, 8, LS>(D, lane, tpr, nullptr, slot * slot_dbl + mis, 0, 0, 0, V + origins[r],
+                                      D.line_off, offL);
+            }
+        }
+        s = group_reduce(s, tpr, offRed, g * tpr);
+        if (valid && lane == 0) {
+            const long long r = r_lo + ra + i;
+            v_in[ra + i] = skip ? 0.0 : (reach ? s + t0x[r] : s);
+            mbar_arrive(empty + slot); // the group has finished reading this slot
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Stage (ii), stored matrix, per-warp cp.async double buffer (tpr == 32): each
+// warp copies its NEXT row into shared memory with 16-byte cp.async (no register
+// staging) while it reduces the current row from shared memory. Opt-in.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_expect_matrix_cp(GmDev D, long long row0, long long r_lo,
+                                                              long long r_hi, int buf_dbl,
+                                                              const double* __restrict__ probs,
+                                                              const long long* __restrict__ origins,
+                                                              const double* __restrict__ t0x,
+                                                              const double* __restrict__ V,
+                                                              double* __restrict__ v_in) {
+    const int nw = kThreads / 32;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int offRed = nw * 2 * buf_dbl;
+    const int offL = 2 * (offRed + kThreads / 32);
+    {
+        int* si = reinterpret_cast<int*>(g_sm);
+        for (int c = threadIdx.x; c < D.n_lines; c += blockDim.x) si[offL + c] = D.line_off[c];
+    }
+    __syncthreads();
+    const bool reach = D.spec_kind != GM_SPEC_SAFETY;
+    const long long nuw = D.n_u * D.n_w;
+    const long long nrows = r_hi - r_lo;
+    const int R = static_cast<int>(D.R);
+    const long long step = static_cast<long long>(gridDim.x) * nw;
+    auto row_of = [&](long long it) { return (it * gridDim.x + blockIdx.x) * nw + warp; };
+    auto live = [&](long long rl) {
+        return rl < nrows && !(reach && D.absorb != nullptr && D.absorb[(row0 + r_lo + rl) / nuw]);
+    };
+    auto fetch = [&](long long rl, int b) { // aligned superset of the row -> buffer b
+        const char* src = reinterpret_cast<const char*>(probs + (r_lo + rl) * D.R);
+        const char* a = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15));
+        const int chunks = static_cast<int>(((src + R * 8 - a) + 15) >> 4);
+        const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(g_sm + (warp * 2 + b) * buf_dbl));
+        for (int c = lane; c < chunks; c += 32)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + c * 16), "l"(a + c * 16) : "memory");
+    };
+    (void)step;
+    long long it = 0;
+    long long rl = row_of(0);
+    if (live(rl)) fetch(rl, 0);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    for (; rl < nrows || __any_sync(0xffffffffu, rl < nrows); ++it) {
+        const long long nxt = row_of(it + 1);
+        const int b = static_cast<int>(it & 1);
+        if (live(nxt)) fetch(nxt, b ^ 1);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        __syncwarp();
+        double s = 0.0;
+        const bool ok = live(rl);
+        if (ok) {
+            const long long r = r_lo + rl;
+            const int mis = static_cast<int>((reinterpret_cast<uintptr_t>(probs + r * D.R) & 15) >> 3);
+            s = row_dot<3, 8, true>(D, lane, 32, nullptr, (warp * 2 + b) * buf_dbl + mis, 0, 0, 0, V + origins[r],
+                                    D.line_off, offL);
+        }
+        s = group_reduce(s, 32, offRed, warp * 32);
+        if (rl < nrows && lane == 0) v_in[rl] = ok ? (reach ? s + t0x[r_lo + rl] : s) : 0.0;
+        __syncwarp(); // buffer b is refilled next iteration
+        rl = nxt;
+        if (rl >= nrows) break;
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
 // min over w (strict <, ascending), then max over u (strict >, ascending):
 // lowest-index ties (synthesis.cpp:112-142). L lanes per state.
 template <int L>
@@ -1315,6 +1489,47 @@ void expect_matrix(const GmDev& D, long long row0, long long r_lo, long long r_h
     static const char* pfs = std::getenv("GM_PREFETCH");
     const int pf = pfs ? std::atoi(pfs) : 0;
     const bool allow_bulk = force && std::string(force) == "bulk";
+    // opt-in variants: GM_MATRIX_KERNEL=ws (warp-specialised bulk ring, 28 ms on C2b),
+    // bulk (CTA-synchronised ring, 25.6 ms), cp (per-warp cp.async double buffer); the
+    // default register-streaming kernel measured 20.8 ms.
+    const bool allow_ws = force && std::string(force) == "ws";
+    if (force && std::string(force) == "cp" && D.tpr == 32 && in_smem) {
+        const size_t buf = ((static_cast<size_t>(D.R) * 8 + 16) + 15) / 16 * 16;
+        const size_t smem = (kThreads / 32) * 2 * buf + (kThreads / 32) * sizeof(double) + table;
+        if (smem <= 110 * 1024) {
+            allow_smem(k_expect_matrix_cp, smem);
+            const int grid = resident_grid(k_expect_matrix_cp, smem, blocks_needed);
+            k_expect_matrix_cp<<<grid, kThreads, smem, s>>>(D, row0, r_lo, r_hi, static_cast<int>(buf / 8), probs,
+                                                            origins, t0x, V, v_in);
+            check_launch("expect_matrix_cp");
+            return;
+        }
+    }
+    {
+        static const char* cs = std::getenv("GM_WS_CTAS");
+        const int ctas = cs ? std::max(1, std::atoi(cs)) : 2;
+        const size_t slot_b = ((static_cast<size_t>(D.R) * 8 + 16) + 15) / 16 * 16;
+        const size_t tail_b = (kThreads / 32) * sizeof(double) + (in_smem ? table : 0);
+        const size_t budget = (ctas >= 2 ? 110 * 1024 : 220 * 1024);
+        long long ns = slot_b ? static_cast<long long>((budget - tail_b) / (slot_b + 16)) : 0;
+        ns = std::min<long long>(ns, std::max(64, groups));
+        // a multiple of the group count: slot s is always consumed by group s % groups, so
+        // a consumer is never more than one phase ahead of a slot's mbarrier (parity waits)
+        ns -= ns % groups;
+        if (allow_ws && in_smem && ns >= groups && ns >= 4) {
+            const size_t smem = static_cast<size_t>(ns) * slot_b + tail_b + 2 * ns * sizeof(uint64_t) + 16;
+            allow_smem(k_expect_matrix_ws<true>, smem);
+            const long long nrows = r_hi - r_lo;
+            int grid = num_sms() * ctas;
+            const long long per = (nrows + grid - 1) / grid;
+            grid = static_cast<int>((nrows + per - 1) / per);
+            k_expect_matrix_ws<true><<<grid, kWsThreads, smem, s>>>(D, row0, r_lo, r_hi, static_cast<int>(ns),
+                                                                    static_cast<int>(slot_b / 8), per, probs,
+                                                                    origins, t0x, V, v_in);
+            check_launch("expect_matrix_ws");
+            return;
+        }
+    }
     const size_t slot = ((static_cast<size_t>(groups) * D.R * 8 + 16) + 15) / 16 * 16;
     const size_t tail = (kThreads / 32) * sizeof(double) + 4 * sizeof(uint64_t) + (in_smem ? table : 0);
     if (allow_bulk && in_smem && 2 * slot + tail <= kHardSmem) {
