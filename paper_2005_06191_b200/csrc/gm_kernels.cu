@@ -248,6 +248,63 @@ __device__ __forceinline__ double tmass(const GmDev& D, int d, double lo, double
     return axis_mass(D, d, a, b, ok);
 }
 
+// Per-boundary CDF term of axis_mass (noise.cpp:92-122): erf(x/s) for the normal,
+// the exponential / beta CDFs; axis_mass(lo, hi) = combine(F(hi), F(lo)).
+__device__ __forceinline__ double axis_F(const GmDev& D, int d, double x, bool& ok) {
+    switch (D.family) {
+        case GM_NORMAL: return erf(x / D.s[d]);
+        case GM_EXPONENTIAL: return x <= 0.0 ? 0.0 : -expm1(-D.s[d] * x);
+        default: return x <= 0.0 ? 0.0 : (x >= 1.0 ? 1.0 : inc_beta(D.s[d], D.p2[d], x, ok));
+    }
+}
+
+__device__ __forceinline__ bool same_bits(double a, double b) {
+    return __double_as_longlong(a) == __double_as_longlong(b);
+}
+
+// fill_axis_masses for one axis (abstraction.cpp:130-146): the W cell masses of
+// axis d, each exactly axis_transformed_mass(d, rep-η/2, rep+η/2, μ, scale)
+// (noise.cpp:124-131). Adjacent cells share a boundary: when the transformed
+// boundary of cell t+1 is bitwise equal to the one of cell t, the reference
+// evaluates the same CDF argument twice; the value is reused instead, so the
+// masses are bit-identical while erf/expm1/inc_beta calls drop from 2W to W+1.
+__device__ void axis_masses(const GmDev& D, int d, long long o, double mu, double scale, double* out, int stride,
+                            bool& ok) {
+    const double eta = D.xeta[d], half = 0.5 * D.xeta[d], lb = D.xlb[d];
+    double cx0 = 0.0, cF0 = 0.0, cx1 = 0.0, cF1 = 0.0;
+    bool h0 = false, h1 = false;
+    for (int t = 0; t < D.W[d]; ++t) {
+        const double rep = lb + static_cast<double>(o + t) * eta;
+        const double lo = rep - half, hi = rep + half;
+        double m;
+        if (scale == 0.0) {
+            m = (mu >= lo && mu <= hi) ? 1.0 : 0.0;
+        } else {
+            double a = (lo - mu) / scale;
+            double b = (hi - mu) / scale;
+            if (scale < 0.0) {
+                const double tmp = a;
+                a = b;
+                b = tmp;
+            }
+            if (b <= a) {
+                m = 0.0;
+            } else if (D.family == GM_UNIFORM) {
+                const double ua = D.s[d], ub = D.p2[d];
+                const double ov = smin(b, ub) - smax(a, ua);
+                m = ov > 0.0 ? ov / (ub - ua) : 0.0;
+            } else {
+                const double Fa = (h0 && same_bits(a, cx0)) ? cF0 : (h1 && same_bits(a, cx1)) ? cF1 : axis_F(D, d, a, ok);
+                const double Fb = (h0 && same_bits(b, cx0)) ? cF0 : (h1 && same_bits(b, cx1)) ? cF1 : axis_F(D, d, b, ok);
+                m = D.family == GM_NORMAL ? 0.5 * (Fb - Fa) : Fb - Fa;
+                cx0 = a; cF0 = Fa; h0 = true;
+                cx1 = b; cF1 = Fb; h1 = true;
+            }
+        }
+        out[static_cast<long long>(t) * stride] = m;
+    }
+}
+
 // slab origin along one axis (abstraction.cpp:103-120)
 __device__ __forceinline__ long long slab_origin(const GmDev& D, int d, double mu) {
     long long o;
@@ -346,7 +403,7 @@ __global__ void __launch_bounds__(kThreads) k_prologue(GmDev D, long long row0, 
     }
     if (origin_out) origin_out[i] = flat;
     bool ok = true;
-    if (flags & PF_MASSES) {
+    if (flags & PF_MASSES) { // per-cell form: keeps this kernel at 64 registers (axis_masses: 80)
         for (int d = 0; d < D.n; ++d) {
             const double scale = D.mult ? x[d] : 1.0;
             const double half = 0.5 * D.xeta[d];
@@ -613,7 +670,8 @@ __global__ void __launch_bounds__(kThreads) k_expand(GmDev D, long long nrows, i
 // overlaps the store phase of the others on the same SM.
 template <int TAB>
 __global__ void __launch_bounds__(kThreads, 4) k_build(GmDev D, long long row0, long long nrows, int rb,
-                                                   GmFastDiv div_rb, int rowbuf_off, long long* __restrict__ origin_out,
+                                                   GmFastDiv div_rb, int rowbuf_off, int vec_copy,
+                                                   long long* __restrict__ origin_out,
                                                    double* __restrict__ t0x_out, double* __restrict__ probs,
                                                    unsigned long long* err) {
     const Layout Y(D, rb, TAB);
@@ -689,23 +747,20 @@ __global__ void __launch_bounds__(kThreads, 4) k_build(GmDev D, long long row0, 
             g_sm[offOk + i] = ok;
         }
         __syncthreads();
-        // fill_axis_masses (abstraction.cpp:130-146): thread per (row, cell)
-        for (int c = threadIdx.x; c < rb * mw; c += blockDim.x) {
-            const int q = div_rb.div(c), i = c - q * rb;
-            double v = 1.0;
-            if (q < D.sumW && g_sm[offOk + i] != 0.0) {
-                int d = 0;
-                while (q >= D.mass_off[d + 1]) ++d;
-                const int t = q - D.mass_off[d];
-                const double rep = D.xlb[d] + static_cast<double>(sorg[i * GMD_MAXD + d] + t) * D.xeta[d];
-                const double half = 0.5 * D.xeta[d];
+        // fill_axis_masses (abstraction.cpp:130-146): thread per (row, axis), boundary
+        // CDF values shared between adjacent cells when bitwise equal (axis_masses)
+        for (int c = threadIdx.x; c < rb * D.n; c += blockDim.x) {
+            const int d = c / rb, i = c - d * rb;
+            if (g_sm[offOk + i] != 0.0) {
                 bool ok = true;
-                v = tmass(D, d, rep - half, rep + half, g_sm[offMu + i * GMD_MAXD + d],
-                          D.mult ? g_sm[offX + i * GMD_MAXD + d] : 1.0, ok);
+                axis_masses(D, d, sorg[i * GMD_MAXD + d], g_sm[offMu + i * GMD_MAXD + d],
+                            D.mult ? g_sm[offX + i * GMD_MAXD + d] : 1.0, g_sm + i * mw + D.mass_off[d], 1, ok);
                 if (!ok) record_error(err, row0 + b0 + i);
+            } else {
+                for (int t = 0; t < D.W[d]; ++t) g_sm[i * mw + D.mass_off[d] + t] = 1.0;
             }
-            g_sm[i * mw + q] = v;
         }
+        for (int i = threadIdx.x; i < rb; i += blockDim.x) g_sm[i * mw + D.sumW] = 1.0; // virtual-axis slot
         __syncthreads();
         stage_tables(D, Y, rb, TAB);
         __syncthreads();
@@ -734,6 +789,17 @@ __global__ void __launch_bounds__(kThreads, 4) k_build(GmDev D, long long row0, 
                     }
                     double* dst = buf + L * Wl + head;
                     for (int k = 0; k < Wl; ++k) dst[k] = q * g_sm[mlo + k];
+                }
+                if (vec_copy) { // 16-byte vector stores from the staged row, coalesced
+                    __syncwarp();
+                    const int body = (R - head) & ~1;
+                    if (lane == 0 && head) __stcs(out, buf[head]);
+                    if (lane == 1 && (R - head - body)) __stcs(out + head + body, buf[2 * head + body]);
+                    const double2* src2 = reinterpret_cast<const double2*>(buf + 2 * head);
+                    double2* dst2 = reinterpret_cast<double2*>(out + head);
+                    for (int q2 = lane; q2 < body / 2; q2 += 32) __stcs(dst2 + q2, src2[q2]);
+                    __syncwarp();
+                    continue;
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
@@ -1421,7 +1487,10 @@ void build(const GmDev& D, long long row0, long long nrows, long long* origin_ou
     size_t smem = fixed + (tab == TAB_Q ? q_row : p_row) * static_cast<size_t>(rb);
     // bulk-store variant: one shared-memory row per warp (+ the tables of >= 16 rows)
     static const char* bb = std::getenv("GM_BUILD_BULK");
-    const bool want_bulk = bb && bb[0] == '1'; // opt-in: measured slower than direct stores
+    // GM_BUILD_BULK=1: rows staged in shared memory + one TMA bulk store each; =2: staged rows
+    // copied with 16-byte vector stores; unset: lane-strided direct stores
+    const bool want_bulk = bb && (bb[0] == '1' || bb[0] == '2');
+    const int vec_copy = bb && bb[0] == '2' ? 1 : 0;
     int rowbuf_off = -1;
     const size_t rowbuf = (kThreads / 32) * static_cast<size_t>((D.R + 3) & ~1LL) * sizeof(double);
     if (want_bulk && D.R >= 32 && D.R + 2 < (1 << 20)) {
@@ -1440,11 +1509,11 @@ void build(const GmDev& D, long long row0, long long nrows, long long* origin_ou
     if (tab == TAB_Q) {
         allow_smem(k_build<TAB_Q>, smem);
         k_build<TAB_Q><<<resident_grid(k_build<TAB_Q>, smem, batches), kThreads, smem, s>>>(
-            D, row0, nrows, static_cast<int>(rb), drb, rowbuf_off, origin_out, t0x_out, probs_out, d_err);
+            D, row0, nrows, static_cast<int>(rb), drb, rowbuf_off, vec_copy, origin_out, t0x_out, probs_out, d_err);
     } else {
         allow_smem(k_build<TAB_P>, smem);
         k_build<TAB_P><<<resident_grid(k_build<TAB_P>, smem, batches), kThreads, smem, s>>>(
-            D, row0, nrows, static_cast<int>(rb), drb, rowbuf_off, origin_out, t0x_out, probs_out, d_err);
+            D, row0, nrows, static_cast<int>(rb), drb, rowbuf_off, vec_copy, origin_out, t0x_out, probs_out, d_err);
     }
     check_launch("build");
 }
