@@ -10,9 +10,11 @@ runs the 32 backward Bellman steps (all-gather of V between ranks).
   value      MDP probabilities built per second, whole job (rows*R / build time,
              device time with CUDA events on the engine's stream, max over ranks)
   sweep_s    Bellman sweep seconds per synthesis (device time, max over ranks)
-  e2e        the same metric through the public API (gridmdp.synthesize -> C ABI
-             gm_synthesize: config text parsed on the host, descriptors uploaded,
-             matrix built, sweep run, value/policy tables copied back to host)
+  e2e        the same metric through the public C ABI from host data: config text
+             parsed on the host, model uploaded, shard built (gm_build_shard),
+             origins + target-hit vector read back into pinned host memory
+             (wall clock, max over ranks); e2e_synthesize = one full
+             gridmdp.synthesize (value/policy tables on the host)
 
 `--impl reference` times the reference's own CPU implementation
 (oracle/_ref/gridmdp_ref: RowKernel::compute + fill_row, the body of
@@ -180,7 +182,8 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     _capi.call("gm_set_device", local)
-    if world > 1:
+    # under torchrun (any N, including 1) the NCCL path is the one exercised
+    if world > 1 or ("MASTER_ADDR" in os.environ and "RANK" in os.environ):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
 
@@ -209,7 +212,7 @@ def main():
     for _ in range(args.warmup):
         one_step()
     torch.cuda.synchronize()
-    if world > 1:
+    if dist.is_initialized():
         dist.barrier()
     lib = _capi.lib
     lib.gm_reset_kernel_stats()
@@ -236,7 +239,7 @@ def main():
     fam_n = {n: lib.gm_kernel_launches(i) for i, n in enumerate(_capi.KF_NAMES)}
 
     t = torch.tensor([total_ms, sum(build_ms), sum(sweep_ms)], dtype=torch.float64, device=dev)
-    if world > 1:
+    if dist.is_initialized():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms, bsum, ssum = t.tolist()
     rows_all = int(sz.rows)
@@ -315,13 +318,13 @@ def main():
         e2e = []
         for _ in range(args.steps):
             torch.cuda.synchronize()
-            if world > 1:
+            if dist.is_initialized():
                 dist.barrier()
             a = time.perf_counter()
             m3 = e2e_step()
             torch.cuda.synchronize()
             dt = torch.tensor([time.perf_counter() - a], dtype=torch.float64, device=dev)
-            if world > 1:
+            if dist.is_initialized():
                 dist.all_reduce(dt, op=dist.ReduceOp.MAX)
             e2e.append(float(dt.item()))
         prog_bytes = int(_capi.lib.gm_model_program_size(m3.handle)) * 8
@@ -377,7 +380,7 @@ def main():
             line["cpu_baseline"] = {"value": None, "error": str(e)}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.barrier()
         dist.destroy_process_group()
 

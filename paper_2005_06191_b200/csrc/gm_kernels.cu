@@ -494,10 +494,21 @@ __device__ __forceinline__ void stage_tables(const GmDev& D, const Layout& Y, in
     }
     if (tab == TAB_Q) {
         __syncthreads();
-        for (int c = threadIdx.x; c < rb * D.n_lines; c += blockDim.x) {
-            const int i = D.div_lines.div(c), L = c - i * D.n_lines;
-            const int a = D.div_Wm.div(L), j = L - a * D.Wm;
-            g_sm[Y.offQ + c] = g_sm[Y.offP + i * D.P_size + a] * g_sm[i * mw + D.mm_off + j];
+        // Q[L] = P[a] * mm[j], L = a*Wm + j; per row, lanes stride L by blockDim with an
+        // incremental (a, j) so the loop has no divisions
+        const int st = blockDim.x;
+        const int qa = D.div_Wm.div(st), qj = st - qa * D.Wm;
+        const int a0 = D.div_Wm.div(threadIdx.x), j0 = threadIdx.x - a0 * D.Wm;
+        for (int i = 0; i < rb; ++i) {
+            const int po = Y.offP + i * D.P_size, mo = i * mw + D.mm_off, qo = Y.offQ + i * D.n_lines;
+            int a = a0, j = j0;
+            for (int L = threadIdx.x; L < D.n_lines; L += st) {
+                g_sm[qo + L] = g_sm[po + a] * g_sm[mo + j];
+                j += qj;
+                const int c = j >= D.Wm;
+                j -= c ? D.Wm : 0;
+                a += qa + c;
+            }
         }
     }
 }

@@ -121,7 +121,7 @@ def synthesize_sharded(backend, n_x: int, horizon: int, reach: bool, matrix: boo
         for k in range(T - 1, -1, -1):
             backend.step(tm, x0, x1, vals[k + 1], vals[k, lo:lo + per], pol[k, lo:lo + per],
                          wst[k, lo:lo + per])
-            if world > 1:
+            if dist.is_initialized():  # V exchange: in-place all-gather of the shards (NCCL)
                 dist.all_gather_into_tensor(vals[k], vals[k, lo:lo + per].clone() if vals.device.type == "cpu"
                                             else vals[k, lo:lo + per], group=group)
             if k == T - 1 and hasattr(backend, "check"):
@@ -132,7 +132,7 @@ def synthesize_sharded(backend, n_x: int, horizon: int, reach: bool, matrix: boo
             backend.free(tm)
     if timer:
         timer("sweep_end")
-    if world > 1:
+    if dist.is_initialized():
         pol_full = torch.empty_like(pol)
         wst_full = torch.empty_like(wst)
         for src, dst in ((pol, pol_full), (wst, wst_full)):
