@@ -72,6 +72,7 @@ struct GmDev {
 
     double radius[GMD_MAXD];
     double s[GMD_MAXD];      // normal: sigma*sqrt(2) (noise.cpp:96); else param1
+    double inv_s[GMD_MAXD];  // normal: 1 / s (the device scales erf arguments by a multiply)
     double p2[GMD_MAXD];     // uniform b / beta beta
     double tlo[GMD_MAXD], thi[GMD_MAXD], alo[GMD_MAXD], ahi[GMD_MAXD];
     int W[GMD_MAXD];
@@ -88,6 +89,9 @@ struct GmDev {
     int mm_off, ml_off;      // offsets of the last two axes' masses (n == 1: mm_off = sumW, a 1.0 slot)
     GmFastDiv div_Wm, div_Wl, div_lines, div_P, div_mw; // n / d for n < 2^31 by multiply-shift
     GmFastDiv div_W[GMD_MAXD];
+    // row decode by multiply-shift when every row index is < 2^31 (idx32)
+    int idx32;
+    GmFastDiv div_nw, div_nu, div_xs[GMD_MAXD], div_us[GMD_MAXD], div_ws[GMD_MAXD];
 
     int entry[GMD_MAXD + 1]; // bytecode offsets of the n dynamics expressions
     const GmIns* prog;

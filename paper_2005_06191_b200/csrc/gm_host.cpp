@@ -1155,6 +1155,7 @@ GmDev Model::device_descriptor() const {
         D.xeta[d] = X.eta[d];
         D.radius[d] = radius ? (*radius)[d] : 0.0;
         D.s[d] = noise.family == GM_NORMAL ? noise.p1[d] * kRoot2 : noise.p1[d];
+        D.inv_s[d] = 1.0 / D.s[d];
         D.p2[d] = noise.p2.empty() ? 0.0 : noise.p2[d];
         D.W[d] = static_cast<int>(extents[d]);
         if (spec.target.dim() == n) { D.tlo[d] = spec.target.lo[d]; D.thi[d] = spec.target.hi[d]; }
@@ -1190,6 +1191,14 @@ GmDev Model::device_descriptor() const {
     D.div_P = gm_fastdiv(static_cast<uint32_t>(D.P_size));
     D.div_mw = gm_fastdiv(static_cast<uint32_t>(D.sumW + 1));
     for (int d = 0; d < n; ++d) D.div_W[d] = gm_fastdiv(static_cast<uint32_t>(D.W[d]));
+    D.idx32 = rows() < (int64_t(1) << 31) ? 1 : 0;
+    if (D.idx32) {
+        D.div_nw = gm_fastdiv(static_cast<uint32_t>(D.n_w));
+        D.div_nu = gm_fastdiv(static_cast<uint32_t>(D.n_u));
+        for (int d = 0; d < n; ++d) D.div_xs[d] = gm_fastdiv(static_cast<uint32_t>(D.xstride[d]));
+        for (int d = 0; d < D.m; ++d) D.div_us[d] = gm_fastdiv(static_cast<uint32_t>(D.ustride[d]));
+        for (int d = 0; d < D.p; ++d) D.div_ws[d] = gm_fastdiv(static_cast<uint32_t>(D.wstride[d]));
+    }
     for (size_t i = 0; i < prog.entry.size() && i <= GMD_MAXD; ++i) D.entry[i] = prog.entry[i];
     return D;
 }

@@ -58,6 +58,31 @@ __device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b 
 
 __device__ void decode_row(const GmDev& D, long long row, long long& ix, double* x, double* u,
                            double* w) {
+    if (D.idx32) { // same integers by multiply-shift division
+        const int r32 = static_cast<int>(row);
+        const int pr = D.div_nw.div(r32), iw = r32 - pr * static_cast<int>(D.n_w);
+        const int x32 = D.div_nu.div(pr), iu = pr - x32 * static_cast<int>(D.n_u);
+        ix = x32;
+        int rem = x32;
+        for (int d = 0; d < D.n; ++d) {
+            const int j = D.div_xs[d].div(rem);
+            rem -= j * static_cast<int>(D.xstride[d]);
+            x[d] = D.xlb[d] + static_cast<double>(j) * D.xeta[d];
+        }
+        rem = iu;
+        for (int d = 0; d < D.m; ++d) {
+            const int j = D.div_us[d].div(rem);
+            rem -= j * static_cast<int>(D.ustride[d]);
+            u[d] = D.ulb[d] + static_cast<double>(j) * D.ueta[d];
+        }
+        rem = iw;
+        for (int d = 0; d < D.p; ++d) {
+            const int j = D.div_ws[d].div(rem);
+            rem -= j * static_cast<int>(D.wstride[d]);
+            w[d] = D.wlb[d] + static_cast<double>(j) * D.weta[d];
+        }
+        return;
+    }
     const long long iw = row % D.n_w;
     const long long pr = row / D.n_w;
     const long long iu = pr % D.n_u;
@@ -211,8 +236,8 @@ __device__ double axis_mass(const GmDev& D, int d, double lo, double hi, bool& o
     if (hi <= lo) return 0.0;
     switch (D.family) {
         case GM_NORMAL: {
-            const double s = D.s[d];
-            return 0.5 * (erf(hi / s) - erf(lo / s));
+            const double is = D.inv_s[d];
+            return 0.5 * (erf(hi * is) - erf(lo * is));
         }
         case GM_UNIFORM: {
             const double a = D.s[d], b = D.p2[d];
@@ -238,8 +263,8 @@ __device__ double axis_mass(const GmDev& D, int d, double lo, double hi, bool& o
 __device__ __forceinline__ double tmass(const GmDev& D, int d, double lo, double hi, double mean,
                                         double scale, bool& ok) {
     if (scale == 0.0) return (mean >= lo && mean <= hi) ? 1.0 : 0.0;
-    double a = (lo - mean) / scale;
-    double b = (hi - mean) / scale;
+    double a = scale == 1.0 ? lo - mean : (lo - mean) / scale; // x / 1.0 == x exactly
+    double b = scale == 1.0 ? hi - mean : (hi - mean) / scale;
     if (scale < 0.0) {
         const double t = a;
         a = b;
@@ -252,7 +277,7 @@ __device__ __forceinline__ double tmass(const GmDev& D, int d, double lo, double
 // the exponential / beta CDFs; axis_mass(lo, hi) = combine(F(hi), F(lo)).
 __device__ __forceinline__ double axis_F(const GmDev& D, int d, double x, bool& ok) {
     switch (D.family) {
-        case GM_NORMAL: return erf(x / D.s[d]);
+        case GM_NORMAL: return erf(x * D.inv_s[d]);
         case GM_EXPONENTIAL: return x <= 0.0 ? 0.0 : -expm1(-D.s[d] * x);
         default: return x <= 0.0 ? 0.0 : (x >= 1.0 ? 1.0 : inc_beta(D.s[d], D.p2[d], x, ok));
     }
@@ -280,8 +305,8 @@ __device__ void axis_masses(const GmDev& D, int d, long long o, double mu, doubl
         if (scale == 0.0) {
             m = (mu >= lo && mu <= hi) ? 1.0 : 0.0;
         } else {
-            double a = (lo - mu) / scale;
-            double b = (hi - mu) / scale;
+            double a = scale == 1.0 ? lo - mu : (lo - mu) / scale; // x / 1.0 == x exactly
+            double b = scale == 1.0 ? hi - mu : (hi - mu) / scale;
             if (scale < 0.0) {
                 const double tmp = a;
                 a = b;
@@ -494,8 +519,20 @@ __device__ __forceinline__ void stage_tables(const GmDev& D, const Layout& Y, in
     }
     if (tab == TAB_Q) {
         __syncthreads();
-        // Q[L] = P[a] * mm[j], L = a*Wm + j; per row, lanes stride L by blockDim with an
-        // incremental (a, j) so the loop has no divisions
+        const int nl = D.n_lines;
+        if (nl <= static_cast<int>(blockDim.x)) {
+            // Q[L] = P[a] * mm[j], L = a*Wm + j: each thread owns one line L of rows
+            // ri, ri+rp, ... (rp = rows per pass), so (a, j) are fixed per thread
+            const int rp = D.div_lines.div(blockDim.x);
+            const int ri = D.div_lines.div(threadIdx.x), L = threadIdx.x - ri * nl;
+            if (ri < rp) {
+                const int a = D.div_Wm.div(L), j = L - a * D.Wm;
+                for (int i = ri; i < rb; i += rp)
+                    g_sm[Y.offQ + i * nl + L] = g_sm[Y.offP + i * D.P_size + a] * g_sm[i * mw + D.mm_off + j];
+            }
+            return;
+        }
+        // wide rows: per row, lanes stride L by blockDim with an incremental (a, j)
         const int st = blockDim.x;
         const int qa = D.div_Wm.div(st), qj = st - qa * D.Wm;
         const int a0 = D.div_Wm.div(threadIdx.x), j0 = threadIdx.x - a0 * D.Wm;
@@ -864,6 +901,218 @@ __global__ void __launch_bounds__(kThreads, 4) k_build(GmDev D, long long row0, 
     if (rowbuf_off >= 0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// ---------------------------------------------------------------------------
+// Stage (i), fused and warp-specialised. The row prologue (decode, dynamics
+// bytecode, slab origin, target-hit mass: one thread per row, a long serial
+// chain) of batch k+1 runs on the `npw` producer warps while the consumer
+// warps build batch k (cell masses, prefix tables); then every warp, producers
+// included once their prologue is done, claims rows of batch k to expand.
+// Barriers: 0 = whole CTA (batch boundary), 1 = consumer warps, 2 = "tables of
+// batch k ready" (consumers arrive, producers wait).
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ void named_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+struct ProBuf { // one batch's prologue results in shared memory
+    double* mu;  // [rb][GMD_MAXD]
+    double* x;   // [rb][GMD_MAXD]
+    double* ok;  // [rb]
+    int* org;    // [rb][GMD_MAXD]
+};
+
+__device__ __forceinline__ int pro_doubles(int rb) { return 2 * rb * GMD_MAXD + rb + (rb * GMD_MAXD + 1) / 2; }
+
+__device__ __forceinline__ ProBuf pro_buf(int base, int rb) {
+    ProBuf p;
+    p.mu = g_sm + base;
+    p.x = p.mu + rb * GMD_MAXD;
+    p.ok = p.x + rb * GMD_MAXD;
+    p.org = reinterpret_cast<int*>(p.ok + rb);
+    return p;
+}
+
+// RowKernel::compute (abstraction.cpp:72-121) + box_mass (:187-191) for rows
+// b0 + [ti, ti+nt, ...) of a batch
+__device__ __forceinline__ void build_prologue(const GmDev& D, const GmIns* sprog, const double* slits,
+                                               long long row0, long long nrows, long long b0, int rb, int ti,
+                                               int nt, const ProBuf& pb, long long* __restrict__ origin_out,
+                                               double* __restrict__ t0x_out, unsigned long long* err) {
+    const bool reach = D.spec_kind != GM_SPEC_SAFETY;
+    for (int i = ti; i < rb; i += nt) {
+        const long long r = b0 + i;
+        double ok = 0.0;
+        if (r < nrows) {
+            double x[GMD_MAXD], u[GMD_MAXD], w[GMD_MAXD], mu[GMD_MAXD];
+            long long ix;
+            decode_row(D, row0 + r, ix, x, u, w);
+            if (run_dynamics(D, sprog, slits, x, u, w, mu)) {
+                ok = 1.0;
+                long long flat = 0;
+                for (int d = 0; d < D.n; ++d) {
+                    const long long o = slab_origin(D, d, mu[d]);
+                    pb.org[i * GMD_MAXD + d] = static_cast<int>(o);
+                    flat += o * D.xstride[d];
+                    pb.mu[i * GMD_MAXD + d] = mu[d];
+                    pb.x[i * GMD_MAXD + d] = x[d];
+                }
+                origin_out[r] = flat;
+                if (t0x_out) {
+                    const bool absorbed = reach && D.absorb != nullptr && D.absorb[ix];
+                    double p = 0.0;
+                    bool bok = true;
+                    if (!absorbed) {
+                        p = 1.0;
+                        for (int d = 0; d < D.n; ++d) {
+                            p *= tmass(D, d, D.tlo[d], D.thi[d], mu[d], D.mult ? x[d] : 1.0, bok);
+                            if (p == 0.0) break;
+                        }
+                        p = smin(1.0, smax(0.0, p));
+                    }
+                    if (!bok) record_error(err, row0 + r);
+                    t0x_out[r] = p;
+                }
+            } else {
+                record_error(err, row0 + r);
+            }
+        }
+        pb.ok[i] = ok;
+    }
+}
+
+template <int TAB>
+__global__ void __launch_bounds__(kThreads, 4) k_build_ws(GmDev D, long long row0, long long nrows, int rb,
+                                                      int npw, int opts, long long* __restrict__ origin_out,
+                                                      double* __restrict__ t0x_out, double* __restrict__ probs,
+                                                      unsigned long long* err) {
+    const Layout Y(D, rb, TAB);
+    const int offPro = Y.offR + kThreads / 32;
+    const int psz = pro_doubles(rb);
+    const int offProg = offPro + 2 * psz;
+    GmIns* sprog = reinterpret_cast<GmIns*>(g_sm + offProg);
+    double* slits = g_sm + offProg + D.n_ins;
+    int* claim = reinterpret_cast<int*>(slits + D.n_lits); // two fill-row counters (batch parity)
+    for (int c = threadIdx.x; c < D.n_ins; c += blockDim.x) sprog[c] = D.prog[c];
+    for (int c = threadIdx.x; c < D.n_lits; c += blockDim.x) slits[c] = D.lits[c];
+    if (threadIdx.x < 2) claim[threadIdx.x] = 0;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int mw = Y.mw;
+    const int R = static_cast<int>(D.R);
+    const int np = npw * 32;               // producer threads
+    const int nc = kThreads - np;          // consumer threads
+    const bool producer = warp < npw;
+    const int ct = threadIdx.x - np;       // consumer thread index
+    Walk wk0;
+    wk0.init(D, lane, 32);
+    // fill: opts bit 3 = element table ET[t] = byte offsets of (Q[L], ml[k]) in the row's
+    // tables (TAB_Q; 5% faster than the incremental slab walk on C2b)
+    int* ET = claim + 2;
+    const bool use_et = TAB == TAB_Q && (opts & 8);
+    if (use_et)
+        for (int t = threadIdx.x; t < R; t += blockDim.x) {
+            const int L = D.div_Wl.div(t);
+            ET[t] = (L * 8) | ((t - L * D.Wl) * 8) << 16;
+        }
+    const long long stride = static_cast<long long>(gridDim.x) * rb;
+    long long b0 = static_cast<long long>(blockIdx.x) * rb;
+    __syncthreads();
+    if (producer && b0 < nrows)
+        build_prologue(D, sprog, slits, row0, nrows, b0, rb, threadIdx.x, np, pro_buf(offPro, rb), origin_out,
+                       t0x_out, err);
+    __syncthreads();
+    for (int par = 0; b0 < nrows; b0 += stride, par ^= 1) {
+        const ProBuf cur = pro_buf(offPro + par * psz, rb);
+        if (producer) {
+            if (threadIdx.x == 0) claim[par ^ 1] = 0; // next batch's counter (unused in this one)
+            if (b0 + stride < nrows)
+                build_prologue(D, sprog, slits, row0, nrows, b0 + stride, rb, threadIdx.x, np,
+                               pro_buf(offPro + (par ^ 1) * psz, rb), origin_out, t0x_out, err);
+            named_sync(2, kThreads); // the consumers have built this batch's tables
+        } else {
+            // fill_axis_masses (abstraction.cpp:130-146): thread per (row, axis)
+            for (int c = ct; c < rb * D.n; c += nc) {
+                const int d = c / rb, i = c - d * rb;
+                if (cur.ok[i] != 0.0) {
+                    bool ok = true;
+                    axis_masses(D, d, cur.org[i * GMD_MAXD + d], cur.mu[i * GMD_MAXD + d],
+                                D.mult ? cur.x[i * GMD_MAXD + d] : 1.0, g_sm + i * mw + D.mass_off[d], 1, ok);
+                    if (!ok) record_error(err, row0 + b0 + i);
+                } else {
+                    for (int t = 0; t < D.W[d]; ++t) g_sm[i * mw + D.mass_off[d] + t] = 1.0;
+                }
+            }
+            for (int i = ct; i < rb; i += nc) g_sm[i * mw + D.sumW] = 1.0; // virtual-axis slot
+            named_sync(1, nc);
+            // prefix tables P (and Q)
+            for (int c = ct; c < rb * D.P_size; c += nc) {
+                const int i = D.div_P.div(c), a = c - i * D.P_size;
+                const int mrow = i * mw;
+                int jv[GMD_MAXD];
+                int rem = a;
+#pragma unroll
+                for (int d = GMD_MAXD - 1; d >= 0; --d) {
+                    if (d < D.s_axes) {
+                        const int q = D.div_W[d].div(rem);
+                        jv[d] = rem - q * D.W[d];
+                        rem = q;
+                    }
+                }
+                double acc = 1.0;
+#pragma unroll
+                for (int d = 0; d < GMD_MAXD; ++d)
+                    if (d < D.s_axes) acc *= g_sm[mrow + D.mass_off[d] + jv[d]];
+                g_sm[Y.offP + c] = acc;
+            }
+            if (TAB == TAB_Q) {
+                named_sync(1, nc);
+                const int nl = D.n_lines;
+                for (int c = ct; c < rb * nl; c += nc) {
+                    const int i = D.div_lines.div(c), L = c - i * nl;
+                    const int a = D.div_Wm.div(L), j = L - a * D.Wm;
+                    g_sm[Y.offQ + c] = g_sm[Y.offP + i * D.P_size + a] * g_sm[i * mw + D.mm_off + j];
+                }
+            }
+            named_sync(1, nc);
+            named_arrive(2, kThreads);
+        }
+        // fill_product (abstraction.cpp:150-159): warps claim rows of this batch
+        for (;;) {
+            int i = 0;
+            if (lane == 0) i = atomicAdd(&claim[par], 1);
+            i = __shfl_sync(0xffffffffu, i, 0);
+            const long long row = b0 + i;
+            if (i >= rb || row >= nrows) break;
+            const int qo = Y.offQ + i * D.n_lines, po = Y.offP + i * D.P_size;
+            const int mmo = i * mw + D.mm_off, mlo = i * mw + D.ml_off;
+            double* out = probs + row * D.R;
+            if (use_et) {
+                const char* qb = reinterpret_cast<const char*>(g_sm + qo);
+                const char* mb = reinterpret_cast<const char*>(g_sm + mlo);
+#pragma unroll 4
+                for (int t = lane; t < R; t += 32) {
+                    const int e = ET[t];
+                    __stcs(out + t, *reinterpret_cast<const double*>(qb + (e & 0xffff)) *
+                                        *reinterpret_cast<const double*>(mb + (e >> 16)));
+                }
+                continue;
+            }
+            Walk wk = wk0;
+#pragma unroll 4
+            for (int t = lane; t < R; t += 32) {
+                const double p = TAB == TAB_Q ? g_sm[qo + wk.L] * g_sm[mlo + wk.k]
+                                              : (g_sm[po + wk.a] * g_sm[mmo + wk.j]) * g_sm[mlo + wk.k];
+                __stcs(out + t, p);
+                wk.template next<TAB == TAB_P>();
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // Stage (ii), on the fly (synthesis.cpp:100-104 + dot_slab :18-47): row groups
 // of tpr threads recompute each row from the staged masses and dot it with V.
 template <int TAB, bool LS>
@@ -962,6 +1211,106 @@ __global__ void __launch_bounds__(kThreads) k_expect_matrix(GmDev D, long long r
     }
 }
 
+// Stage (ii), stored matrix, element-offset table: the slab walk of a lane is the
+// same for every row, so the CTA tabulates E[t] = line_off[L(t)] + k(t) once in
+// shared memory and each term costs one LDS + the two loads + one fma (the walk
+// kernel above spends ~19 instructions per term). Same canonical per-lane order
+// (t = lane, lane+TPR, ...; batches of 8 with zero padding), so the result is
+// bitwise that of every other row kernel.
+//
+// Row schedule (flags bit 1 clear): CTA-interleaved groups of `groups` rows;
+// (bit 1 set) each CTA owns one contiguous range of rows, so consecutive states
+// (whose slabs overlap) run back to back on one SM and reuse V lines in L1.
+// flags bit 0: row / (n_u n_w) fits the 32-bit multiply-shift division.
+struct RowSched {
+    long long per_cta, iters, stride;
+    bool contig;
+    __device__ __forceinline__ RowSched(long long nrows, int groups, int flags) {
+        contig = flags & 2;
+        if (contig) {
+            per_cta = ((nrows + gridDim.x - 1) / gridDim.x + groups - 1) / groups * groups;
+            iters = per_cta / groups;
+        } else {
+            const long long total = static_cast<long long>(gridDim.x) * groups;
+            per_cta = 0;
+            iters = (nrows + total - 1) / total;
+        }
+    }
+    __device__ __forceinline__ long long row(long long it, int groups, int g) const {
+        return contig ? blockIdx.x * per_cta + it * groups + g : (it * gridDim.x + blockIdx.x) * groups + g;
+    }
+};
+
+template <int TPR>
+__global__ void __launch_bounds__(kThreads) k_expect_matrix_et(GmDev D, long long row0, long long r_lo,
+                                                              long long r_hi, GmFastDiv div_nuw, int flags,
+                                                              const double* __restrict__ probs,
+                                                              const long long* __restrict__ origins,
+                                                              const double* __restrict__ t0x,
+                                                              const double* __restrict__ V,
+                                                              double* __restrict__ v_in) {
+    constexpr int U = 8;
+    constexpr int groups = kThreads / TPR;
+    const int R = static_cast<int>(D.R);
+    int* E = reinterpret_cast<int*>(g_sm + kThreads / 32); // after the group partials
+    for (int t = threadIdx.x; t < R; t += kThreads) {
+        const int L = D.div_Wl.div(t);
+        E[t] = D.line_off[L] + (t - L * D.Wl);
+    }
+    __syncthreads();
+    const int g = threadIdx.x / TPR, lane = threadIdx.x % TPR;
+    const bool reach = D.spec_kind != GM_SPEC_SAFETY;
+    const long long nrows = r_hi - r_lo;
+    const RowSched rs(nrows, groups, flags);
+    const long long nuw = D.n_u * D.n_w;
+    const int n_it = lane < R ? (R - lane + TPR - 1) / TPR : 0;
+    const int n_full = n_it - n_it % U;
+    const int rem = n_it - n_full;
+    for (long long it = 0; it < rs.iters; ++it) {
+        const long long rl = rs.row(it, groups, g);
+        const bool valid = rl < nrows;
+        const long long r = r_lo + rl;
+        bool skip = !valid;
+        if (valid && reach && D.absorb != nullptr) {
+            const long long row = row0 + r;
+            skip = D.absorb[(flags & 1) ? static_cast<long long>(div_nuw.div(static_cast<int>(row))) : row / nuw];
+        }
+        double s = 0.0;
+        if (!skip) {
+            const double* pr = probs + r * R + lane;
+            const double* vb = V + origins[r];
+            const int* e = E + lane;
+            for (int b = 0; b < n_full; b += U) {
+                double p[U], v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    p[u] = __ldcs(pr + u * TPR);
+                    v[u] = ldg_at(vb, e[u * TPR]);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) s = fma(p[u], v[u], s);
+                pr += U * TPR;
+                e += U * TPR;
+            }
+            if (rem) {
+                double p[U], v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    p[u] = 0.0;
+                    v[u] = 0.0;
+                    if (u < rem) {
+                        p[u] = __ldcs(pr + u * TPR);
+                        v[u] = ldg_at(vb, e[u * TPR]);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) s = fma(p[u], v[u], s);
+            }
+        }
+        s = group_reduce(s, TPR, 0, g * TPR);
+        if (valid && lane == 0) v_in[rl] = skip ? 0.0 : (reach ? s + t0x[r] : s);
+    }
+}
 
 // ---------------------------------------------------------------------------
 // Stage (ii), stored matrix, bulk-async staged (Blackwell TMA bulk copies):
@@ -1474,6 +1823,38 @@ void build(const GmDev& D, long long row0, long long nrows, long long* origin_ou
            double* probs_out, unsigned long long* d_err, cudaStream_t s) {
     if (nrows <= 0) return;
     const size_t mw = static_cast<size_t>(D.sumW + 1);
+    static const char* bw = std::getenv("GM_BUILD_WS"); // 0: single-role k_build
+    if (!(bw && bw[0] == '0')) {
+        // warp-specialised build: layout of k_build_ws in doubles
+        static const char* bo2 = std::getenv("GM_BUILD_OPTS");
+        const int wopts = bo2 ? std::atoi(bo2) : 8; // default: element-table fill
+        // + two claim counters, + the element table (R ints) when selected
+        const bool et = (wopts & 8) && D.n_lines * 8 < 65536 && D.Wl * 8 < 32768;
+        const size_t fixed_d = kThreads / 32 + D.n_ins + D.n_lits + 1 + (et ? (D.R + 1) / 2 : 0);
+        for (int t : {TAB_Q, TAB_P}) {
+            const size_t per_d = mw + D.P_size + (t == TAB_Q ? D.n_lines : 0) + 42; // + 2 prologue buffers
+            const size_t budget_d = 54 * 1024 / sizeof(double);                     // 4 CTAs/SM
+            if (fixed_d >= budget_d) break;
+            long long rb = std::min<long long>(96, static_cast<long long>((budget_d - fixed_d) / per_d));
+            if (rb < 16) continue;
+            const int npw = static_cast<int>((rb + 31) / 32);
+            const size_t smem = (fixed_d + per_d * static_cast<size_t>(rb)) * sizeof(double);
+            const long long batches = (nrows + rb - 1) / rb;
+            if (t == TAB_Q) {
+                allow_smem(k_build_ws<TAB_Q>, smem);
+                k_build_ws<TAB_Q><<<resident_grid(k_build_ws<TAB_Q>, smem, batches), kThreads, smem, s>>>(
+                    D, row0, nrows, static_cast<int>(rb), npw, et ? wopts : (wopts & ~8), origin_out, t0x_out,
+                    probs_out, d_err);
+            } else {
+                allow_smem(k_build_ws<TAB_P>, smem);
+                k_build_ws<TAB_P><<<resident_grid(k_build_ws<TAB_P>, smem, batches), kThreads, smem, s>>>(
+                    D, row0, nrows, static_cast<int>(rb), npw, et ? wopts : (wopts & ~8), origin_out, t0x_out,
+                    probs_out, d_err);
+            }
+            check_launch("build");
+            return;
+        }
+    }
     const size_t fixed = (kThreads / 32 + D.n_ins + D.n_lits + 2) * sizeof(double) +
                          (D.Wl <= 64 ? static_cast<size_t>(D.Wl) * 32 * sizeof(int) : 0);
     const size_t extra_row = (2 * GMD_MAXD + 1) * sizeof(double) + GMD_MAXD * sizeof(int);
@@ -1569,9 +1950,12 @@ void expect_matrix(const GmDev& D, long long row0, long long r_lo, long long r_h
     static const char* pfs = std::getenv("GM_PREFETCH");
     const int pf = pfs ? std::atoi(pfs) : 0;
     const bool allow_bulk = force && std::string(force) == "bulk";
-    // opt-in variants: GM_MATRIX_KERNEL=ws (warp-specialised bulk ring, 28 ms on C2b),
-    // bulk (CTA-synchronised ring, 25.6 ms), cp (per-warp cp.async double buffer); the
-    // default register-streaming kernel measured 20.8 ms.
+    // default: element-offset-table kernel k_expect_matrix_et (18.2-19.8 ms on C2b,
+    // L1 data-pipe bound). Opt-in variants, all slower on C2b: GM_MATRIX_KERNEL=walk
+    // (per-term slab walk, 23 ms), ws (warp-specialised bulk ring, 28 ms), bulk
+    // (CTA-synchronised ring, 25.6 ms), cp (per-warp cp.async double buffer, 32.8 ms).
+    // Offsets held in registers instead of the table: 21.3 ms (92 registers) / equal
+    // (64 registers, spills); GM_CONTIG=1 (contiguous rows per CTA): equal.
     const bool allow_ws = force && std::string(force) == "ws";
     if (force && std::string(force) == "cp" && D.tpr == 32 && in_smem) {
         const size_t buf = ((static_cast<size_t>(D.R) * 8 + 16) + 15) / 16 * 16;
@@ -1624,6 +2008,26 @@ void expect_matrix(const GmDev& D, long long row0, long long r_lo, long long r_h
         k_expect_matrix_bulk<true><<<grid, kThreads, smem, s>>>(D, row0, r_lo, r_hi, bp, probs, origins, t0x, V, v_in);
         check_launch("expect_matrix_bulk");
         return;
+    }
+    const size_t et_smem = (kThreads / 32) * sizeof(double) + static_cast<size_t>(D.R) * sizeof(int);
+    if (!(force && std::string(force) == "walk") && et_smem <= kHardSmem) {
+        const long long nuw = D.n_u * D.n_w;
+        const int div32 = (row0 + r_hi <= INT_MAX && nuw <= INT_MAX) ? 1 : 0;
+        const GmFastDiv dn = gm_fastdiv(static_cast<uint32_t>(div32 ? nuw : 1));
+        static const char* cg = std::getenv("GM_CONTIG");
+        const int flags = div32 | ((cg && std::atoi(cg)) ? 2 : 0);
+        switch (D.tpr) {
+#define GM_ET(T)                                                                                          \
+    case T:                                                                                               \
+        allow_smem(k_expect_matrix_et<T>, et_smem);                                                       \
+        k_expect_matrix_et<T><<<resident_grid(k_expect_matrix_et<T>, et_smem, blocks_needed), kThreads,   \
+                                et_smem, s>>>(D, row0, r_lo, r_hi, dn, flags, probs, origins, t0x, V, v_in); \
+        check_launch("expect_matrix");                                                                    \
+        return;
+            GM_ET(1) GM_ET(2) GM_ET(4) GM_ET(8) GM_ET(16) GM_ET(32) GM_ET(64) GM_ET(128)
+#undef GM_ET
+        default: break;
+        }
     }
     const size_t smem = (kThreads / 32) * sizeof(double) + (in_smem ? table : 0);
     if (in_smem) {
