@@ -47,6 +47,16 @@ def peaks():
     return 6650.0, "fallback"
 
 
+def ncu_traffic(kernel: str, workload: str):
+    """DRAM bytes per launch of `kernel` from the newest committed ncu --set full capture
+    (profiles/*/ncu_traffic.json, written by scripts/ncu_summary.py --traffic), else None."""
+    for f in sorted(REPO.glob("profiles/*/ncu_traffic.json"), reverse=True):
+        e = json.loads(f.read_text()).get(kernel)
+        if e and e.get("workload") == workload:
+            return e["dram_bytes_per_launch"]
+    return None
+
+
 class Clocks:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
 
@@ -259,7 +269,7 @@ def main():
         live_rows = int((ab == 0).sum()) * nuw
     dom_bytes = live_rows * (R * 8 + 8 + (8 if reach else 0))
     roofline = {"kernel": dom, "bound": "hbm", "achieved": dom_bytes / (dom_ms / 1e3) / 1e9, "peak": hbm,
-                "peak_kind": peak_kind, "unit": "GB/s", "traffic": None,
+                "peak_kind": peak_kind, "unit": "GB/s", "traffic": ncu_traffic(dom, args.workload),
                 "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_ms": dom_ms, "launches": fam_n[dom]}
     roofline["frac"] = roofline["achieved"] / hbm
     if not matrix:
@@ -268,7 +278,8 @@ def main():
     build_bytes = my_rows * (R * 8 + 8 + (8 if reach else 0))  # rows written + origins (+ T0x)
     roofline_build = {"kernel": "k_build", "bound": "hbm",
                       "achieved": build_bytes / (exp_ms / 1e3) / 1e9 if exp_ms > 0 else None, "peak": hbm,
-                      "unit": "GB/s", "algorithmic_bytes_per_launch": build_bytes, "avg_launch_ms": exp_ms}
+                      "unit": "GB/s", "algorithmic_bytes_per_launch": build_bytes, "avg_launch_ms": exp_ms,
+                      "traffic": ncu_traffic("k_build", args.workload)}
     if roofline_build["achieved"]:
         roofline_build["frac"] = roofline_build["achieved"] / hbm
 

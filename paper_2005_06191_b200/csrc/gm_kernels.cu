@@ -1019,6 +1019,15 @@ __global__ void __launch_bounds__(kThreads, 4) k_build_ws(GmDev D, long long row
         }
     const long long stride = static_cast<long long>(gridDim.x) * rb;
     long long b0 = static_cast<long long>(blockIdx.x) * rb;
+    // opts bit 4: cycle totals of thread 0 (producer) and thread np (consumer), CTA 0
+    const bool prof = (opts & 16) && blockIdx.x == 0 && (threadIdx.x == 0 || threadIdx.x == np);
+    long long tp[4] = {0, 0, 0, 0}, tl = clock64();
+#define GM_TP(k)                          \
+    if (prof) {                           \
+        const long long n_ = clock64();   \
+        tp[k] += n_ - tl;                 \
+        tl = n_;                          \
+    }
     __syncthreads();
     if (producer && b0 < nrows)
         build_prologue(D, sprog, slits, row0, nrows, b0, rb, threadIdx.x, np, pro_buf(offPro, rb), origin_out,
@@ -1031,7 +1040,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_build_ws(GmDev D, long long row
             if (b0 + stride < nrows)
                 build_prologue(D, sprog, slits, row0, nrows, b0 + stride, rb, threadIdx.x, np,
                                pro_buf(offPro + (par ^ 1) * psz, rb), origin_out, t0x_out, err);
+            GM_TP(0)
             named_sync(2, kThreads); // the consumers have built this batch's tables
+            GM_TP(1)
         } else {
             // fill_axis_masses (abstraction.cpp:130-146): thread per (row, axis)
             for (int c = ct; c < rb * D.n; c += nc) {
@@ -1047,6 +1058,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_build_ws(GmDev D, long long row
             }
             for (int i = ct; i < rb; i += nc) g_sm[i * mw + D.sumW] = 1.0; // virtual-axis slot
             named_sync(1, nc);
+            GM_TP(0)
             // prefix tables P (and Q)
             for (int c = ct; c < rb * D.P_size; c += nc) {
                 const int i = D.div_P.div(c), a = c - i * D.P_size;
@@ -1078,6 +1090,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_build_ws(GmDev D, long long row
             }
             named_sync(1, nc);
             named_arrive(2, kThreads);
+            GM_TP(1)
         }
         // fill_product (abstraction.cpp:150-159): warps claim rows of this batch
         for (;;) {
@@ -1109,8 +1122,15 @@ __global__ void __launch_bounds__(kThreads, 4) k_build_ws(GmDev D, long long row
                 wk.template next<TAB == TAB_P>();
             }
         }
+        GM_TP(2)
         __syncthreads();
+        GM_TP(3)
     }
+#undef GM_TP
+    if (prof)
+        printf("k_build_ws %s: rb %d npw %d cycles: %s %lld, %s %lld, fill %lld, batch barrier %lld\n",
+               threadIdx.x == 0 ? "producer" : "consumer", rb, npw, threadIdx.x == 0 ? "prologue" : "masses", tp[0],
+               threadIdx.x == 0 ? "wait tables" : "tables", tp[1], tp[2], tp[3]);
 }
 
 // Stage (ii), on the fly (synthesis.cpp:100-104 + dot_slab :18-47): row groups

@@ -15,6 +15,27 @@ def run(args):
     return subprocess.run(["ncu", "-i", *args], capture_output=True, text=True).stdout
 
 
+def dram_bytes(rep):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the first captured launch, in bytes."""
+    raw = list(csv.reader(io.StringIO(run([rep, "--page", "raw", "--csv"]))))
+    hh, units, vals = raw[0], raw[1], raw[2]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    tot = 0.0
+    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        i = hh.index(k)
+        tot += float(vals[i].replace(",", "")) * scale[units[i]]
+    return tot
+
+
+def record_traffic(rep, out, kernel, workload):
+    """Merges {kernel: {workload, dram_bytes_per_launch, report}} into `out` (read by bench.py)."""
+    import json
+    import os
+    d = json.load(open(out)) if os.path.exists(out) else {}
+    d[kernel] = {"workload": workload, "dram_bytes_per_launch": dram_bytes(rep), "report": os.path.basename(rep)}
+    json.dump(d, open(out, "w"), indent=1)
+
+
 def main(rep, top=25):
     rows = list(csv.reader(io.StringIO(run([rep, "--page", "details", "--csv"]))))
     h = rows[0]
@@ -41,4 +62,8 @@ def main(rep, top=25):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 25)
+    # ncu_summary.py REPORT [TOP]  |  ncu_summary.py --traffic OUT.json KERNEL WORKLOAD REPORT
+    if sys.argv[1] == "--traffic":
+        record_traffic(sys.argv[5], sys.argv[2], sys.argv[3], sys.argv[4])
+    else:
+        main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 25)
