@@ -984,44 +984,52 @@ __device__ __forceinline__ void build_prologue(const GmDev& D, const GmIns* spro
     }
 }
 
-template <int TAB>
+// Three-role pipeline over batches j = blockIdx.x + i*gridDim.x of rb rows.
+// Iteration i: producer warps run the row prologue of batch i+2 (-> pro[(i+2)&1]),
+// consumer warps turn batch i+1's prologue into cell masses and the prefix table
+// P (-> tab[(i+1)&1]), filler warps expand batch i from tab[i&1] (per row: line
+// prefixes Q[L] = P[a]*mm[j] into a per-warp scratch, then lane-strided
+// evict-first stores of Q[L]*ml[k] through the element table ET); producers and
+// consumers join the fill when their own work is done. One CTA barrier per
+// iteration. The fill streams continuously: ~8 storing warps per SM saturate
+// HBM writes for this row pattern (scripts/store_probe.cu).
+// QS = per-warp Q scratch + element table (n_lines and W_last small enough);
+// otherwise rows are expanded by the incremental slab walk, q = P[a]*mm[j] per term.
+template <bool QS>
 __global__ void __launch_bounds__(kThreads, 4) k_build_ws(GmDev D, long long row0, long long nrows, int rb,
-                                                      int npw, int opts, long long* __restrict__ origin_out,
+                                                      int npw, int ncw, int opts,
+                                                      long long* __restrict__ origin_out,
                                                       double* __restrict__ t0x_out, double* __restrict__ probs,
                                                       unsigned long long* err) {
-    const Layout Y(D, rb, TAB);
-    const int offPro = Y.offR + kThreads / 32;
-    const int psz = pro_doubles(rb);
-    const int offProg = offPro + 2 * psz;
+    const int mw = D.sumW + 1;
+    const int R = static_cast<int>(D.R);
+    const int nl = D.n_lines;
+    const int tsz = rb * (mw + D.P_size), psz = pro_doubles(rb);
+    const int offT = 0, offPro = offT + 2 * tsz, offQs = offPro + 2 * psz;
+    const int offProg = offQs + (QS ? (kThreads / 32) * nl : 0);
     GmIns* sprog = reinterpret_cast<GmIns*>(g_sm + offProg);
     double* slits = g_sm + offProg + D.n_ins;
-    int* claim = reinterpret_cast<int*>(slits + D.n_lits); // two fill-row counters (batch parity)
+    int* claim = reinterpret_cast<int*>(slits + D.n_lits); // fill-row counters by batch parity
+    int* ET = claim + 2;
     for (int c = threadIdx.x; c < D.n_ins; c += blockDim.x) sprog[c] = D.prog[c];
     for (int c = threadIdx.x; c < D.n_lits; c += blockDim.x) slits[c] = D.lits[c];
     if (threadIdx.x < 2) claim[threadIdx.x] = 0;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int mw = Y.mw;
-    const int R = static_cast<int>(D.R);
-    const int np = npw * 32;               // producer threads
-    const int nc = kThreads - np;          // consumer threads
-    const bool producer = warp < npw;
-    const int ct = threadIdx.x - np;       // consumer thread index
-    Walk wk0;
-    wk0.init(D, lane, 32);
-    // fill: opts bit 3 = element table ET[t] = byte offsets of (Q[L], ml[k]) in the row's
-    // tables (TAB_Q; 5% faster than the incremental slab walk on C2b)
-    int* ET = claim + 2;
-    const bool use_et = TAB == TAB_Q && (opts & 8);
-    if (use_et)
+    if (QS)
         for (int t = threadIdx.x; t < R; t += blockDim.x) {
             const int L = D.div_Wl.div(t);
             ET[t] = (L * 8) | ((t - L * D.Wl) * 8) << 16;
         }
-    const long long stride = static_cast<long long>(gridDim.x) * rb;
-    long long b0 = static_cast<long long>(blockIdx.x) * rb;
-    // opts bit 4: cycle totals of thread 0 (producer) and thread np (consumer), CTA 0
-    const bool prof = (opts & 16) && blockIdx.x == 0 && (threadIdx.x == 0 || threadIdx.x == np);
-    long long tp[4] = {0, 0, 0, 0}, tl = clock64();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int np = npw * 32, nc = ncw * 32;
+    const int role = warp < npw ? 0 : (warp < npw + ncw ? 1 : 2); // producer, consumer, filler
+    const int ct = threadIdx.x - np;
+    Walk wk0;
+    wk0.init(D, lane, 32);
+    auto first_row = [&](long long j) { return (static_cast<long long>(blockIdx.x) + j * gridDim.x) * rb; };
+    // opts bit 4: cycle totals of one thread per role (CTA 0; diagnostics only)
+    const bool prof = (opts & 16) && blockIdx.x == 0 && (threadIdx.x == 0 || threadIdx.x == np ||
+                                                         threadIdx.x == np + nc);
+    long long tp[3] = {0, 0, 0}, tl = clock64();
 #define GM_TP(k)                          \
     if (prof) {                           \
         const long long n_ = clock64();   \
@@ -1029,108 +1037,112 @@ __global__ void __launch_bounds__(kThreads, 4) k_build_ws(GmDev D, long long row
         tl = n_;                          \
     }
     __syncthreads();
-    if (producer && b0 < nrows)
-        build_prologue(D, sprog, slits, row0, nrows, b0, rb, threadIdx.x, np, pro_buf(offPro, rb), origin_out,
-                       t0x_out, err);
+    if (role == 0 && first_row(0) < nrows)
+        build_prologue(D, sprog, slits, row0, nrows, first_row(0), rb, threadIdx.x, np, pro_buf(offPro, rb),
+                       origin_out, t0x_out, err);
     __syncthreads();
-    for (int par = 0; b0 < nrows; b0 += stride, par ^= 1) {
-        const ProBuf cur = pro_buf(offPro + par * psz, rb);
-        if (producer) {
-            if (threadIdx.x == 0) claim[par ^ 1] = 0; // next batch's counter (unused in this one)
-            if (b0 + stride < nrows)
-                build_prologue(D, sprog, slits, row0, nrows, b0 + stride, rb, threadIdx.x, np,
-                               pro_buf(offPro + (par ^ 1) * psz, rb), origin_out, t0x_out, err);
-            GM_TP(0)
-            named_sync(2, kThreads); // the consumers have built this batch's tables
-            GM_TP(1)
-        } else {
-            // fill_axis_masses (abstraction.cpp:130-146): thread per (row, axis)
-            for (int c = ct; c < rb * D.n; c += nc) {
-                const int d = c / rb, i = c - d * rb;
-                if (cur.ok[i] != 0.0) {
-                    bool ok = true;
-                    axis_masses(D, d, cur.org[i * GMD_MAXD + d], cur.mu[i * GMD_MAXD + d],
-                                D.mult ? cur.x[i * GMD_MAXD + d] : 1.0, g_sm + i * mw + D.mass_off[d], 1, ok);
-                    if (!ok) record_error(err, row0 + b0 + i);
-                } else {
-                    for (int t = 0; t < D.W[d]; ++t) g_sm[i * mw + D.mass_off[d] + t] = 1.0;
-                }
-            }
-            for (int i = ct; i < rb; i += nc) g_sm[i * mw + D.sumW] = 1.0; // virtual-axis slot
-            named_sync(1, nc);
-            GM_TP(0)
-            // prefix tables P (and Q)
-            for (int c = ct; c < rb * D.P_size; c += nc) {
-                const int i = D.div_P.div(c), a = c - i * D.P_size;
-                const int mrow = i * mw;
-                int jv[GMD_MAXD];
-                int rem = a;
-#pragma unroll
-                for (int d = GMD_MAXD - 1; d >= 0; --d) {
-                    if (d < D.s_axes) {
-                        const int q = D.div_W[d].div(rem);
-                        jv[d] = rem - q * D.W[d];
-                        rem = q;
+    for (long long i = -1; first_row(i < 0 ? 0 : i) < nrows; ++i) {
+        if (threadIdx.x == 0 && i >= 0) claim[(i + 1) & 1] = 0; // used by the next iteration only
+        if (role == 0) {
+            const long long bn = first_row(i + 2);
+            if (bn < nrows)
+                build_prologue(D, sprog, slits, row0, nrows, bn, rb, threadIdx.x, np,
+                               pro_buf(offPro + static_cast<int>((i + 2) & 1) * psz, rb), origin_out, t0x_out, err);
+        } else if (role == 1) {
+            const long long bn = first_row(i + 1);
+            if (bn < nrows) {
+                const ProBuf cur = pro_buf(offPro + static_cast<int>((i + 1) & 1) * psz, rb);
+                double* tb = g_sm + offT + static_cast<int>((i + 1) & 1) * tsz;
+                // fill_axis_masses (abstraction.cpp:130-146): thread per (row, axis)
+                for (int c = ct; c < rb * D.n; c += nc) {
+                    const int d = c / rb, r = c - d * rb;
+                    if (cur.ok[r] != 0.0) {
+                        bool ok = true;
+                        axis_masses(D, d, cur.org[r * GMD_MAXD + d], cur.mu[r * GMD_MAXD + d],
+                                    D.mult ? cur.x[r * GMD_MAXD + d] : 1.0, tb + r * mw + D.mass_off[d], 1, ok);
+                        if (!ok) record_error(err, row0 + bn + r);
+                    } else {
+                        for (int t = 0; t < D.W[d]; ++t) tb[r * mw + D.mass_off[d] + t] = 1.0;
                     }
                 }
-                double acc = 1.0;
-#pragma unroll
-                for (int d = 0; d < GMD_MAXD; ++d)
-                    if (d < D.s_axes) acc *= g_sm[mrow + D.mass_off[d] + jv[d]];
-                g_sm[Y.offP + c] = acc;
-            }
-            if (TAB == TAB_Q) {
+                for (int r = ct; r < rb; r += nc) tb[r * mw + D.sumW] = 1.0; // virtual-axis slot
                 named_sync(1, nc);
-                const int nl = D.n_lines;
-                for (int c = ct; c < rb * nl; c += nc) {
-                    const int i = D.div_lines.div(c), L = c - i * nl;
-                    const int a = D.div_Wm.div(L), j = L - a * D.Wm;
-                    g_sm[Y.offQ + c] = g_sm[Y.offP + i * D.P_size + a] * g_sm[i * mw + D.mm_off + j];
+                // prefix products over the leading axes (abstraction.cpp:150-159 association)
+                double* P = tb + rb * mw;
+                for (int c = ct; c < rb * D.P_size; c += nc) {
+                    const int r = D.div_P.div(c), a = c - r * D.P_size;
+                    int jv[GMD_MAXD];
+                    int rem = a;
+#pragma unroll
+                    for (int d = GMD_MAXD - 1; d >= 0; --d) {
+                        if (d < D.s_axes) {
+                            const int q = D.div_W[d].div(rem);
+                            jv[d] = rem - q * D.W[d];
+                            rem = q;
+                        }
+                    }
+                    double acc = 1.0;
+#pragma unroll
+                    for (int d = 0; d < GMD_MAXD; ++d)
+                        if (d < D.s_axes) acc *= tb[r * mw + D.mass_off[d] + jv[d]];
+                    P[c] = acc;
                 }
             }
-            named_sync(1, nc);
-            named_arrive(2, kThreads);
-            GM_TP(1)
         }
-        // fill_product (abstraction.cpp:150-159): warps claim rows of this batch
-        for (;;) {
-            int i = 0;
-            if (lane == 0) i = atomicAdd(&claim[par], 1);
-            i = __shfl_sync(0xffffffffu, i, 0);
-            const long long row = b0 + i;
-            if (i >= rb || row >= nrows) break;
-            const int qo = Y.offQ + i * D.n_lines, po = Y.offP + i * D.P_size;
-            const int mmo = i * mw + D.mm_off, mlo = i * mw + D.ml_off;
-            double* out = probs + row * D.R;
-            if (use_et) {
-                const char* qb = reinterpret_cast<const char*>(g_sm + qo);
-                const char* mb = reinterpret_cast<const char*>(g_sm + mlo);
-#pragma unroll 4
-                for (int t = lane; t < R; t += 32) {
-                    const int e = ET[t];
-                    __stcs(out + t, *reinterpret_cast<const double*>(qb + (e & 0xffff)) *
-                                        *reinterpret_cast<const double*>(mb + (e >> 16)));
+        GM_TP(0)
+        if (i >= 0) {
+            // fill_product (abstraction.cpp:150-159) of batch i: warps claim rows
+            const long long b0 = first_row(i);
+            const double* tb = g_sm + offT + static_cast<int>(i & 1) * tsz;
+            const double* P = tb + rb * mw;
+            double* Qs = g_sm + offQs + warp * nl;
+            for (;;) {
+                int r = 0;
+                if (lane == 0) r = atomicAdd(&claim[i & 1], 1);
+                r = __shfl_sync(0xffffffffu, r, 0);
+                const long long row = b0 + r;
+                if (r >= rb || row >= nrows) break;
+                const double* m = tb + r * mw;
+                const double* Pr = P + r * D.P_size;
+                double* out = probs + row * D.R;
+                if (opts & 96) { // diagnostics: 32 = constant stores only, 64 = no stores
+                    if (opts & 32)
+                        for (int t = lane; t < R; t += 32) __stcs(out + t, 0.0);
+                    continue;
                 }
-                continue;
-            }
-            Walk wk = wk0;
+                if (QS) {
+                    for (int L = lane; L < nl; L += 32) {
+                        const int a = D.div_Wm.div(L), j = L - a * D.Wm;
+                        Qs[L] = Pr[a] * m[D.mm_off + j];
+                    }
+                    __syncwarp();
+                    const char* qb = reinterpret_cast<const char*>(Qs);
+                    const char* mb = reinterpret_cast<const char*>(m + D.ml_off);
 #pragma unroll 4
-            for (int t = lane; t < R; t += 32) {
-                const double p = TAB == TAB_Q ? g_sm[qo + wk.L] * g_sm[mlo + wk.k]
-                                              : (g_sm[po + wk.a] * g_sm[mmo + wk.j]) * g_sm[mlo + wk.k];
-                __stcs(out + t, p);
-                wk.template next<TAB == TAB_P>();
+                    for (int t = lane; t < R; t += 32) {
+                        const int e = ET[t];
+                        __stcs(out + t, *reinterpret_cast<const double*>(qb + (e & 0xffff)) *
+                                            *reinterpret_cast<const double*>(mb + (e >> 16)));
+                    }
+                    __syncwarp();
+                } else {
+                    Walk wk = wk0;
+#pragma unroll 4
+                    for (int t = lane; t < R; t += 32) {
+                        __stcs(out + t, (Pr[wk.a] * m[D.mm_off + wk.j]) * m[D.ml_off + wk.k]);
+                        wk.template next<true>();
+                    }
+                }
             }
         }
-        GM_TP(2)
+        GM_TP(1)
         __syncthreads();
-        GM_TP(3)
+        GM_TP(2)
     }
 #undef GM_TP
     if (prof)
-        printf("k_build_ws %s: rb %d npw %d cycles: %s %lld, %s %lld, fill %lld, batch barrier %lld\n",
-               threadIdx.x == 0 ? "producer" : "consumer", rb, npw, threadIdx.x == 0 ? "prologue" : "masses", tp[0],
-               threadIdx.x == 0 ? "wait tables" : "tables", tp[1], tp[2], tp[3]);
+        printf("k_build_ws %s: rb %d npw %d ncw %d cycles: own work %lld, fill %lld, barrier %lld\n",
+               role == 0 ? "producer" : (role == 1 ? "consumer" : "filler"), rb, npw, ncw, tp[0], tp[1], tp[2]);
 }
 
 // Stage (ii), on the fly (synthesis.cpp:100-104 + dot_slab :18-47): row groups
@@ -1845,34 +1857,42 @@ void build(const GmDev& D, long long row0, long long nrows, long long* origin_ou
     const size_t mw = static_cast<size_t>(D.sumW + 1);
     static const char* bw = std::getenv("GM_BUILD_WS"); // 0: single-role k_build
     if (!(bw && bw[0] == '0')) {
-        // warp-specialised build: layout of k_build_ws in doubles
+        // three-role pipelined build: layout of k_build_ws in doubles
         static const char* bo2 = std::getenv("GM_BUILD_OPTS");
-        const int wopts = bo2 ? std::atoi(bo2) : 8; // default: element-table fill
-        // + two claim counters, + the element table (R ints) when selected
-        const bool et = (wopts & 8) && D.n_lines * 8 < 65536 && D.Wl * 8 < 32768;
-        const size_t fixed_d = kThreads / 32 + D.n_ins + D.n_lits + 1 + (et ? (D.R + 1) / 2 : 0);
-        for (int t : {TAB_Q, TAB_P}) {
-            const size_t per_d = mw + D.P_size + (t == TAB_Q ? D.n_lines : 0) + 42; // + 2 prologue buffers
-            const size_t budget_d = 54 * 1024 / sizeof(double);                     // 4 CTAs/SM
-            if (fixed_d >= budget_d) break;
-            long long rb = std::min<long long>(96, static_cast<long long>((budget_d - fixed_d) / per_d));
-            if (rb < 16) continue;
-            const int npw = static_cast<int>((rb + 31) / 32);
-            const size_t smem = (fixed_d + per_d * static_cast<size_t>(rb)) * sizeof(double);
-            const long long batches = (nrows + rb - 1) / rb;
-            if (t == TAB_Q) {
-                allow_smem(k_build_ws<TAB_Q>, smem);
-                k_build_ws<TAB_Q><<<resident_grid(k_build_ws<TAB_Q>, smem, batches), kThreads, smem, s>>>(
-                    D, row0, nrows, static_cast<int>(rb), npw, et ? wopts : (wopts & ~8), origin_out, t0x_out,
-                    probs_out, d_err);
-            } else {
-                allow_smem(k_build_ws<TAB_P>, smem);
-                k_build_ws<TAB_P><<<resident_grid(k_build_ws<TAB_P>, smem, batches), kThreads, smem, s>>>(
-                    D, row0, nrows, static_cast<int>(rb), npw, et ? wopts : (wopts & ~8), origin_out, t0x_out,
-                    probs_out, d_err);
+        const int wopts = bo2 ? std::atoi(bo2) : 0;
+        const bool qs = D.n_lines <= 512 && D.n_lines * 8 < 65536 && D.Wl * 8 < 32768;
+        const size_t fixed_d = D.n_ins + D.n_lits + 1 + (qs ? (D.R + 1) / 2 + (kThreads / 32) * D.n_lines : 0);
+        const size_t per_d = 2 * (mw + D.P_size) + 42; // two table buffers + two prologue buffers
+        const size_t budget_d = 54 * 1024 / sizeof(double); // 4 CTAs/SM
+        if (fixed_d < budget_d) {
+            long long rb = std::min<long long>(64, static_cast<long long>((budget_d - fixed_d) / per_d));
+            // consumers: one (row, axis) item per thread; at least 2 filler warps
+            const int nw = kThreads / 32;
+            long long npw = (rb + 31) / 32;
+            long long ncw = (rb * D.n + 31) / 32;
+            while (rb > 8 && npw + ncw > nw - 2) {
+                --rb;
+                npw = (rb + 31) / 32;
+                ncw = (rb * D.n + 31) / 32;
             }
-            check_launch("build");
-            return;
+            if (npw + ncw > nw - 2) ncw = std::max<long long>(1, nw - 2 - npw);
+            if (rb >= 8 && npw + ncw <= nw - 1) {
+                const size_t smem = (fixed_d + per_d * static_cast<size_t>(rb)) * sizeof(double);
+                const long long batches = (nrows + rb - 1) / rb;
+                if (qs) {
+                    allow_smem(k_build_ws<true>, smem);
+                    k_build_ws<true><<<resident_grid(k_build_ws<true>, smem, batches), kThreads, smem, s>>>(
+                        D, row0, nrows, static_cast<int>(rb), static_cast<int>(npw), static_cast<int>(ncw), wopts,
+                        origin_out, t0x_out, probs_out, d_err);
+                } else {
+                    allow_smem(k_build_ws<false>, smem);
+                    k_build_ws<false><<<resident_grid(k_build_ws<false>, smem, batches), kThreads, smem, s>>>(
+                        D, row0, nrows, static_cast<int>(rb), static_cast<int>(npw), static_cast<int>(ncw), wopts,
+                        origin_out, t0x_out, probs_out, d_err);
+                }
+                check_launch("build");
+                return;
+            }
         }
     }
     const size_t fixed = (kThreads / 32 + D.n_ins + D.n_lits + 2) * sizeof(double) +

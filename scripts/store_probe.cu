@@ -15,6 +15,16 @@ __global__ void rows8(double* out, long long nrows, int R) {
     }
 }
 
+// (a2) warp per row, lane pairs: 16-byte stores (rows 16-byte aligned: R even)
+__global__ void rows16(double* out, long long nrows, int R) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (long long r = warp; r < nrows; r += nw) {
+        double2* o = reinterpret_cast<double2*>(out + r * R);
+        for (int t = lane; t < R / 2; t += 32) __stcs(o + t, make_double2(1.0 + t, 2.0 + t));
+    }
+}
+
 // (b) same, default (write-back) stores
 __global__ void rows8wb(double* out, long long nrows, int R) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
@@ -82,6 +92,13 @@ int main() {
         }
         printf("%-44s %8.2f ms  %7.1f GB/s  (%s)\n", name, best, bytes / best / 1e6, cudaGetErrorString(cudaGetLastError()));
     };
+    for (int per : {1, 2, 3}) {
+        char nm[64];
+        snprintf(nm, sizeof nm, "rows8 evict-first, %d CTAs/SM x256", per);
+        run(nm, [&] { rows8<<<sms * per, 256>>>(buf, nrows, R); });
+        snprintf(nm, sizeof nm, "rows16 (R=728) %d CTAs/SM x256", per);
+        run(nm, [&] { rows16<<<sms * per, 256>>>(buf, nrows, 728); });
+    }
     for (int per : {4, 8, 16}) {
         char nm[64];
         snprintf(nm, sizeof nm, "rows8 evict-first, %d CTAs/SM x256", per);
