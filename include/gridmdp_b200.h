@@ -114,6 +114,11 @@ gm_code gm_dynamics_image(const gm_model* m, int64_t row, double* mu_out, gm_sta
 const char* gm_model_output_path(const gm_model* m);
 /* Number of dynamics bytecode instructions (for tests / reporting). */
 int64_t gm_model_program_size(const gm_model* m);
+/* Dynamics compilation (eval_node, expr.cpp:404-501, compiled instead of
+ * interpreted): 1 if the last row-kernel launch of this model used the
+ * run-time compiled kernels, 0 if it used the bytecode interpreter (reason in
+ * why, e.g. NVRTC missing or GM_JIT=0). compile_s: NVRTC + load seconds. */
+int32_t gm_model_jit_status(const gm_model* m, double* compile_s, char* why, int64_t why_len);
 
 /* --------------------------------------------------------------- devices */
 

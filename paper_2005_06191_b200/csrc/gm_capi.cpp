@@ -4,6 +4,7 @@
 #include "gridmdp_b200.h"
 
 #include "gm_host.hpp"
+#include "gm_jit.hpp"
 #include "gm_kernels.cuh"
 
 #include <cuda_runtime.h>
@@ -269,7 +270,29 @@ struct gm_model {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_ready[2] = {}, ev_used[2] = {};
     bool dev_ready = false;
     bool absorb_ready = false;
+    // run-time compiled row kernels (gm_jit.cpp): state of the last row-kernel launch
+    bool jit_used = false;
+    double jit_compile_s = 0.0;
+    std::string jit_why;
 };
+
+// Row kernels with the dynamics compiled for this model, or nullptr (interpreter).
+// GM_JIT=1 forces run-time compiled kernels, 0 disables them; unset: used when
+// the launch covers >= 2^21 rows (a first compile costs 2-5 s, cached per process).
+static const gmj::Kernels* jit_kernels(gm_model* m, int want, int64_t rows) {
+    std::string why;
+    const char* env = std::getenv("GM_JIT");
+    if (!env && rows < (int64_t(1) << 21)) {
+        m->jit_used = false;
+        m->jit_why = "not used: fewer than 2^21 rows in the launch (GM_JIT=1 forces it)";
+        return nullptr;
+    }
+    const gmj::Kernels* k = gmj::kernels_for(m->M.prog, m->M.X.dim(), want, &why);
+    m->jit_used = k != nullptr;
+    m->jit_why = k ? std::string() : why;
+    m->jit_compile_s = k ? k->compile_s : 0.0;
+    return k;
+}
 
 struct gm_matrix {
     int device = -1;
@@ -447,6 +470,10 @@ void build_rows(gm_model* m, int64_t r0, int64_t r1, gm_matrix* tm, bool want_t0
         tm->has_t0x = true;
     }
     static const char* bp = std::getenv("GM_BUILD_PIPE");
+    const gmj::Kernels* J =
+        jit_kernels(m, (bp && bp[0] == '1') ? gmj::WANT_PROLOGUE
+                                            : (gmk::build_uses_qs(m->D) ? gmj::WANT_BUILD_QS : gmj::WANT_BUILD_NOQS),
+                    n);
     if (bp && bp[0] == '1' && n > 0) {
         // row prologue (image, origin, per-axis masses into an L2-resident scratch chunk)
         // on the aux stream, expansion of the previous chunk on the model stream
@@ -459,14 +486,15 @@ void build_rows(gm_model* m, int64_t r0, int64_t r1, gm_matrix* tm, bool want_t0
             [&](int64_t c0, int64_t cn, int b) {
                 gmk::prologue(m->D, r0 + c0, cn, gmk::PF_MASSES | (want_t0x ? gmk::PF_T0X : 0),
                               tm->origins.p + c0, want_t0x ? tm->t0x.p + c0 : nullptr, m->d_rowflag[b].p,
-                              m->d_mass[b].p, m->d_err.p, m->aux);
+                              m->d_mass[b].p, m->d_err.p, m->aux, J ? J->prologue : nullptr);
             },
             [&](int64_t c0, int64_t cn, int b) {
                 gmk::expand(m->D, cn, m->d_mass[b].p, tm->probs.p + c0 * R, m->stream);
             });
     } else {
         Launch L(gmk::KF_EXPAND, m->stream);
-        gmk::build(m->D, r0, n, tm->origins.p, want_t0x ? tm->t0x.p : nullptr, tm->probs.p, m->d_err.p, m->stream);
+        gmk::build(m->D, r0, n, tm->origins.p, want_t0x ? tm->t0x.p : nullptr, tm->probs.p, m->d_err.p, m->stream,
+                   J ? J->build_ws : nullptr);
     }
     ck(cudaStreamSynchronize(m->stream), "build");
     raise_device_error(m);
@@ -490,13 +518,14 @@ void step_states(gm_model* m, gm_matrix* tm, int64_t x0, int64_t x1, const doubl
         const int64_t chunk = std::min(chunk_rows(m), n);
         ensure_scratch(m, chunk);
         const bool reach = m->M.spec.reach();
+        const gmj::Kernels* J = jit_kernels(m, gmj::WANT_PROLOGUE, n);
         pipeline(
             m, n, chunk, s,
             [&](int64_t c0, int64_t cn, int b) {
                 Launch L(gmk::KF_PROLOGUE, m->aux);
                 gmk::prologue(m->D, r0 + c0, cn, gmk::PF_SKIP_ABSORBED | gmk::PF_MASSES | (reach ? gmk::PF_T0X : 0),
                               m->d_origin[b].p, m->d_t0x[b].p, m->d_rowflag[b].p, m->d_mass[b].p, m->d_err.p,
-                              m->aux);
+                              m->aux, J ? J->prologue : nullptr);
             },
             [&](int64_t c0, int64_t cn, int b) {
                 Launch L(gmk::KF_EXPECT_OFA, s);
@@ -514,11 +543,12 @@ void ensure_t0x(gm_model* m, gm_matrix* tm) {
     tm->t0x.ensure(static_cast<size_t>(std::max<int64_t>(n, 1)), "target-hit vector");
     const int64_t chunk = chunk_rows(m);
     ensure_scratch(m, std::min(chunk, std::max<int64_t>(n, 1)));
+    const gmj::Kernels* J = jit_kernels(m, gmj::WANT_PROLOGUE, n);
     for (int64_t c0 = 0; c0 < n; c0 += chunk) {
         const int64_t cn = std::min(chunk, n - c0);
         Launch L(gmk::KF_PROLOGUE, m->stream);
         gmk::prologue(m->D, tm->row_begin + c0, cn, gmk::PF_SKIP_ABSORBED | gmk::PF_T0X, m->d_origin[0].p,
-                      tm->t0x.p + c0, m->d_rowflag[0].p, nullptr, m->d_err.p, m->stream);
+                      tm->t0x.p + c0, m->d_rowflag[0].p, nullptr, m->d_err.p, m->stream, J ? J->prologue : nullptr);
     }
     ck(cudaStreamSynchronize(m->stream), "target hit");
     raise_device_error(m);
@@ -746,6 +776,15 @@ gm_code gm_dynamics_image(const gm_model* m, int64_t row, double* mu_out, gm_sta
 const char* gm_model_output_path(const gm_model* m) { return m->M.cfg.output.c_str(); }
 
 int64_t gm_model_program_size(const gm_model* m) { return static_cast<int64_t>(m->M.prog.code.size()); }
+
+int32_t gm_model_jit_status(const gm_model* m, double* compile_s, char* why, int64_t why_len) {
+    if (compile_s) *compile_s = m->jit_compile_s;
+    if (why && why_len > 0) {
+        std::strncpy(why, m->jit_why.c_str(), static_cast<size_t>(why_len - 1));
+        why[why_len - 1] = '\0';
+    }
+    return m->jit_used ? 1 : 0;
+}
 
 gm_code gm_set_device(int32_t device, gm_status* st) {
     return guarded(st, [&] { ck(cudaSetDevice(device), "cudaSetDevice"); });

@@ -2,7 +2,15 @@
 // sm_100a kernels (CUDA). Passed to kernels by value (kernel parameter space).
 #pragma once
 
+#ifdef __CUDACC_RTC__ // run-time compilation (gm_jit.cpp): no system headers
+typedef unsigned char uint8_t;
+typedef unsigned int uint32_t;
+typedef int int32_t;
+typedef unsigned long long uint64_t;
+typedef long long int64_t;
+#else
 #include <stdint.h>
+#endif
 
 #define GMD_MAXD 8      // max state / input / disturbance dimensions on device
 #define GMD_MAXREGS 32  // max dynamics-interpreter registers per row
@@ -46,6 +54,7 @@ struct GmFastDiv {
 #endif
 };
 
+#ifndef __CUDACC_RTC__
 static inline GmFastDiv gm_fastdiv(uint32_t d) {
     GmFastDiv f;
     f.d = d ? d : 1;
@@ -55,6 +64,7 @@ static inline GmFastDiv gm_fastdiv(uint32_t d) {
     f.m = static_cast<uint32_t>(((1ULL << 32) * ((1ULL << s) - f.d)) / f.d + 1);
     return f;
 }
+#endif
 
 struct GmDev {
     int n, m, p;             // state / input / disturbance dims

@@ -1,0 +1,37 @@
+// Run-time compilation of a model's dynamics (SURVEY.md §8 f row 2; expr.cpp:404-501).
+//
+// The bytecode program (gm_host.cpp Lowering) is turned into straight-line
+// device code (one double per register, goto for the lazy ite), compiled by
+// NVRTC together with the row-level kernels of gm_rowdev.cuh for sm_100a, and
+// loaded with the CUDA runtime's library API. Same IEEE operations, same
+// libdevice functions and --fmad=false as the ahead-of-time interpreter, so
+// rows are bit-identical (tests/test_gpu_jit.py). NVRTC is loaded with dlopen:
+// when it is absent or a compile fails the interpreter kernels are used.
+#pragma once
+
+#include "gm_host.hpp"
+
+#include <string>
+
+namespace gmj {
+
+// Kernel handles (cudaKernel_t, usable as `const void*` function arguments of
+// cudaLaunchKernel / cudaFuncSetAttribute / cudaOccupancy*).
+struct Kernels {
+    const void* build_ws[2] = {nullptr, nullptr}; // k_build_ws<false>, k_build_ws<true>
+    const void* prologue = nullptr;              // k_prologue
+    double compile_s = 0.0;
+};
+
+// CUDA source of `__device__ bool gm_dyn_jit(x, u, w, mu)` for program P.
+std::string dynamics_source(const gmh::Program& P, int n);
+
+enum Want { WANT_PROLOGUE = 1, WANT_BUILD_NOQS = 2, WANT_BUILD_QS = 4 };
+
+// Compiled kernels for program P (cached per generated source; each kernel kind
+// is its own NVRTC program, compiled on first use: ~2 s k_prologue, ~5 s
+// k_build_ws), or nullptr with the reason in *why (NVRTC missing, compile or
+// load failure, GM_JIT=0).
+const Kernels* kernels_for(const gmh::Program& P, int n, int want, std::string* why);
+
+} // namespace gmj

@@ -32,14 +32,18 @@ void zero_absorbing(const GmDev& D, double* d_v, cudaStream_t s);
 // Row prologue (RowKernel::compute + fill_axis_masses + box_mass,
 // abstraction.cpp:72-146,187-191) for rows [row0, row0+nrows): origins (flat),
 // per-axis cell masses (structure of arrays, pitch nrows), target-hit masses.
+// jit: run-time compiled k_prologue (gm_jit.cpp) or nullptr for the interpreter kernel.
 void prologue(const GmDev& D, long long row0, long long nrows, int flags, long long* origin_out,
               double* t0x_out, uint8_t* rowflag_out, double* mass_out,
-              unsigned long long* d_err_row, cudaStream_t s);
+              unsigned long long* d_err_row, cudaStream_t s, const void* jit = nullptr);
 
 // Fused stage (i) (build_matrix body, abstraction.cpp:211-223): rows
 // [row0, row0+nrows) -> origins, stored rows (and target-hit masses if t0x_out).
+// Whether build() uses the per-warp line-prefix variant k_build_ws<true>.
+bool build_uses_qs(const GmDev& D);
+// jit_ws: run-time compiled k_build_ws<false>, k_build_ws<true> (gm_jit.cpp) or nullptr.
 void build(const GmDev& D, long long row0, long long nrows, long long* origin_out, double* t0x_out,
-           double* probs_out, unsigned long long* d_err, cudaStream_t s);
+           double* probs_out, unsigned long long* d_err, cudaStream_t s, const void* const* jit_ws = nullptr);
 
 // Outer-product expansion of the prologue's masses into stored rows
 // (fill_product, abstraction.cpp:150-159).
