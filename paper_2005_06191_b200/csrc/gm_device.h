@@ -8,6 +8,7 @@ typedef unsigned int uint32_t;
 typedef int int32_t;
 typedef unsigned long long uint64_t;
 typedef long long int64_t;
+typedef unsigned long long uintptr_t;
 #else
 #include <stdint.h>
 #endif

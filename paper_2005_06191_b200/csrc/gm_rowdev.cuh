@@ -664,12 +664,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_build_ws(GmDev D, long long row
                     __syncwarp();
                     const char* qb = reinterpret_cast<const char*>(Qs);
                     const char* mb = reinterpret_cast<const char*>(m + D.ml_off);
-#pragma unroll 4
-                    for (int t = lane; t < R; t += 32) {
+                    auto val = [&](int t) {
                         const int e = ET[t];
-                        __stcs(out + t, *reinterpret_cast<const double*>(qb + (e & 0xffff)) *
-                                            *reinterpret_cast<const double*>(mb + (e >> 16)));
-                    }
+                        return *reinterpret_cast<const double*>(qb + (e & 0xffff)) *
+                               *reinterpret_cast<const double*>(mb + (e >> 16));
+                    };
+#pragma unroll 4
+                    for (int t = lane; t < R; t += 32) __stcs(out + t, val(t));
                     __syncwarp();
                 } else {
                     Walk wk = wk0;
@@ -686,10 +687,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_build_ws(GmDev D, long long row
         GM_TP(2)
     }
 #undef GM_TP
-#ifndef __CUDACC_RTC__
     if (prof)
         printf("k_build_ws %s: rb %d npw %d ncw %d cycles: own work %lld, fill %lld, barrier %lld\n",
                role == 0 ? "producer" : (role == 1 ? "consumer" : "filler"), rb, npw, ncw, tp[0], tp[1], tp[2]);
-#endif
 }
 #endif
