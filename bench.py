@@ -15,6 +15,10 @@ runs the 32 backward Bellman steps (all-gather of V between ranks).
              origins + target-hit vector read back into pinned host memory
              (wall clock, max over ranks); e2e_synthesize = one full
              gridmdp.synthesize (value/policy tables on the host)
+  cpu_baseline        the reference's row kernel on a bounded sample (probs/s)
+  cpu_baseline_sweep  one reference bellman_step over the whole workload (OFA,
+                      host threads) x T: the CPU sweep time the GPU's sweep_s
+                      is compared with
 
 `--impl reference` times the reference's own CPU implementation
 (oracle/_ref/gridmdp_ref: RowKernel::compute + fill_row, the body of
@@ -130,6 +134,29 @@ def cpu_sample(cfg_text: str, rows_total: int, target_s: float, threads: int = 0
         return n * R / s, n, R, th, s
     finally:
         os.unlink(path)
+
+
+def cpu_sweep_step(cfg_text: str, n_x: int, threads: int = 0):
+    """One reference bellman_step (synthesis.cpp:147-161) over the whole workload in OFA
+    mode (matrix-free: C2b's 108 GB matrix does not fit host RAM) with V_{k+1} ~ U(0,1)
+    from mt19937_64(20240), all host threads. Returns (seconds, threads)."""
+    import numpy as np
+    if not REF_BIN.exists():
+        raise FileNotFoundError(f"{REF_BIN} missing (make -C oracle ref)")
+    d = tempfile.mkdtemp()
+    try:
+        cfg = os.path.join(d, "w.cfg")
+        open(cfg, "w").write(cfg_text)
+        vn = os.path.join(d, "vnext.f64")
+        np.random.Generator(np.random.MT19937(20240)).random(n_x).astype(np.float64).tofile(vn)
+        th = threads or (os.cpu_count() or 1)
+        out = subprocess.run([str(REF_BIN), "step", "-c", cfg, "--mode", "ofa", "--threads", str(threads),
+                              "--vnext", vn, "-o", os.path.join(d, "out")], capture_output=True, text=True,
+                             check=True).stdout
+        secs = float(out.split("time_step_s:")[1].split()[0])
+        return secs, th
+    finally:
+        subprocess.run(["rm", "-rf", d])
 
 
 def reference_arm(args, cfg_text, sizes):
@@ -389,6 +416,15 @@ def main():
                                     "sample": f"{n} rows x R={Rr} (RowKernel::compute+fill_row), {s:.1f} s"}
         except Exception as e:  # noqa: BLE001
             line["cpu_baseline"] = {"value": None, "error": str(e)}
+        try:  # the sweep half of the metric: one reference Bellman step on the same workload
+            secs, th = cpu_sweep_step(cfg_text, n_x)
+            line["cpu_baseline_sweep"] = {
+                "value": secs * T, "unit": "s", "cores": th, "kind": "reference", "step_s": secs,
+                "sample": f"one OFA bellman_step over all {rows_all} rows (x{T} steps = a sweep); the stored-matrix "
+                          f"mode needs the {rows_all * R * 8 / 1e9:.0f} GB matrix in host RAM",
+                "gpu_speedup_sweep": secs * T / sweep_s if sweep_s else None}
+        except Exception as e:  # noqa: BLE001
+            line["cpu_baseline_sweep"] = {"value": None, "error": str(e)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist.is_initialized():
