@@ -60,6 +60,7 @@ typedef enum gm_spec_kind { GM_SAFETY = 0, GM_REACH = 1, GM_REACH_AVOID = 2 } gm
 typedef struct gm_model gm_model;   /* SystemModel + Spec + SynthesisOptions (model.hpp:15, spec.hpp:14) */
 typedef struct gm_matrix gm_matrix; /* device-resident TransitionMatrix row range (abstraction.hpp:22) */
 typedef struct gm_result gm_result; /* SynthesisResult (synthesis.hpp:28-40), host tables */
+typedef struct gm_sim gm_sim;       /* TrajectoryBatch (sim.hpp:24-27), host copy */
 
 /* CLI/config overrides (tools/gridmdp_main.cpp:20-41); negative / NULL = keep config value. */
 typedef struct gm_overrides {
@@ -225,6 +226,33 @@ gm_code gm_result_from_tables(const gm_model* m, const double* values, const uin
 /* write_results (io.hpp:13, io.cpp:142-179): the `gridmdp-results 1` container. */
 gm_code gm_result_write(const gm_result* r, const char* path, gm_status* st);
 void gm_result_free(gm_result* r);
+
+/* read_results (io.hpp:14, io.cpp:181-230): a `gridmdp-results 1` container. */
+gm_code gm_result_read(const char* path, gm_result** out, gm_status* st);
+/* values(point_to_index(state_grid, x), k) (gridmdp_main.cpp:133-134 value_at_x0). */
+gm_code gm_result_value_at(const gm_result* r, const double* x, int32_t n, int32_t k, double* v, gm_status* st);
+
+/* ----------------------------------------------------------- simulation */
+
+/* exec.runs / exec.seed of the configuration after overrides (config.hpp:40-41). */
+gm_code gm_model_sim_defaults(const gm_model* m, int32_t* runs, uint64_t* seed, gm_status* st);
+/* simulate (sim.hpp:42-44, sim.cpp:16-101): closed-loop Monte Carlo of `runs`
+ * rollouts from x0 under the result's policy and spec, one GPU thread per run;
+ * worst_case selects DisturbanceMode::worst_case. Runs use independent streams
+ * split from `seed` (derive_stream_seed, common.hpp:74-79) on a Philox
+ * generator, so batches are reproducible but not the reference's mt19937_64
+ * draws (statistical parity). want_traj records states/inputs/disturbances. */
+gm_code gm_simulate(gm_model* m, const gm_result* res, const double* x0, int32_t n_x0, int32_t runs,
+                    uint64_t seed, int32_t worst_case, int32_t want_traj, gm_sim** out, gm_status* st);
+/* empirical_rate (sim.cpp:103-108) with the run count and satisfied count. */
+gm_code gm_sim_summary(const gm_sim* s, int32_t* runs, int64_t* satisfied, double* rate, gm_status* st);
+/* Per-run flags / step counts and trajectories ([run][k][d]: T+1 state rows,
+ * T input and disturbance rows per run; rows past a run's steps are unused). */
+gm_code gm_sim_copy(const gm_sim* s, uint8_t* satisfied, int32_t* steps, double* states, double* inputs,
+                    double* dists, gm_status* st);
+/* write_trajectory_csv (sim.hpp:48-50, sim.cpp:117-154). */
+gm_code gm_sim_write_csv(const gm_sim* s, const char* path, gm_status* st);
+void gm_sim_free(gm_sim* s);
 
 /* Large device blocks (>= 64 MB, e.g. stored matrices) are kept for reuse after
  * release; this returns them to the driver. */

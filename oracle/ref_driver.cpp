@@ -12,9 +12,11 @@
 //   synthesize / bellman_step                                  (synthesis.hpp:46-66)
 //   write_results / write_matrix                               (io.hpp:13-23)
 //   parallel_for / resolve_threads                             (parallel.hpp:13-51)
+//   read_results / simulate / empirical_rate / write_trajectory_csv (io.hpp:14, sim.hpp:42-50)
 #include "gridmdp/config.hpp"
 #include "gridmdp/io.hpp"
 #include "gridmdp/parallel.hpp"
+#include "gridmdp/sim.hpp"
 
 #include <chrono>
 #include <cstdio>
@@ -29,7 +31,8 @@ using namespace gridmdp;
 namespace {
 
 struct Args {
-    std::string cmd, config, out, vnext;
+    std::string cmd, config, out, vnext, results, x0, dist_mode = "random", traj;
+    long long runs = -1, seed = -1;
     int threads = -1, time_steps = -1;
     std::string mode;
     long long row_begin = -1, row_end = -1;
@@ -43,6 +46,8 @@ double now_s() {
 Config effective(const Args& a) {
     Config cfg = load_config(a.config);
     if (a.threads >= 0) cfg.threads = a.threads;
+    if (a.runs >= 0) cfg.runs = static_cast<int>(a.runs);
+    if (a.seed >= 0) cfg.seed = static_cast<std::uint64_t>(a.seed);
     if (!a.mode.empty()) cfg.mode = a.mode;
     if (a.time_steps >= 0) cfg.time_steps = a.time_steps;
     return cfg;
@@ -181,6 +186,34 @@ int run(const Args& a) {
                     checksum);
         return 0;
     }
+    if (a.cmd == "simulate") { // as `gridmdp simulate` (tools/gridmdp_main.cpp:119-140)
+        const SynthesisResult res = read_results(a.results);
+        std::vector<double> x;
+        {
+            std::string inner = a.x0.substr(1, a.x0.size() - 2);
+            std::size_t pos = 0;
+            while (pos <= inner.size()) {
+                const std::size_t comma = inner.find(',', pos);
+                x.push_back(std::stod(comma == std::string::npos ? inner.substr(pos) : inner.substr(pos, comma - pos)));
+                if (comma == std::string::npos) break;
+                pos = comma + 1;
+            }
+        }
+        Vector x0(static_cast<Eigen::Index>(x.size()));
+        for (std::size_t i = 0; i < x.size(); ++i) x0[static_cast<Eigen::Index>(i)] = x[i];
+        const DisturbanceMode dm = a.dist_mode == "worst-case" ? DisturbanceMode::worst_case : DisturbanceMode::random;
+        const double t0 = now_s();
+        const TrajectoryBatch batch = simulate(m, res.spec, res, x0, cfg.runs, cfg.seed, dm, cfg.threads);
+        const double dt = now_s() - t0;
+        std::size_t steps = 0;
+        for (const Trajectory& t : batch.runs) steps += static_cast<std::size_t>(t.steps());
+        std::cout << "runs: " << batch.runs.size() << "\n";
+        std::cout << "empirical_rate: " << empirical_rate(batch) << "\n";
+        std::printf("satisfied: %zu\nsteps_total: %zu\ntime_simulate_s: %.6f\n",
+                    static_cast<std::size_t>(empirical_rate(batch) * batch.runs.size() + 0.5), steps, dt);
+        if (!a.traj.empty()) write_trajectory_csv(batch, a.traj);
+        return 0;
+    }
     throw ConfigError("unknown command '" + a.cmd + "'");
 }
 
@@ -190,8 +223,8 @@ int main(int argc, char** argv) {
     if (argc < 3) {
         std::fprintf(stderr,
                      "usage: gridmdp_ref {estimate|matrix|masked-matrix|target-hit|synthesize|step|"
-                     "time-rows} -c CFG [-o OUT] [--mode M] [--threads N] [--time-steps T] "
-                     "[--vnext F] [--rows B E]\n");
+                     "time-rows|simulate} -c CFG [-o OUT] [--mode M] [--threads N] [--time-steps T] "
+                     "[--vnext F] [--rows B E] [--results R --x0 {..} --runs N --seed S --dist-mode D --traj F]\n");
         return 1;
     }
     Args a;
@@ -209,6 +242,12 @@ int main(int argc, char** argv) {
             else if (k == "--threads") a.threads = std::stoi(next());
             else if (k == "--time-steps") a.time_steps = std::stoi(next());
             else if (k == "--vnext") a.vnext = next();
+            else if (k == "--results") a.results = next();
+            else if (k == "--x0") a.x0 = next();
+            else if (k == "--dist-mode") a.dist_mode = next();
+            else if (k == "--traj") a.traj = next();
+            else if (k == "--runs") a.runs = std::stoll(next());
+            else if (k == "--seed") a.seed = std::stoll(next());
             else if (k == "--rows") {
                 a.row_begin = std::stoll(next());
                 a.row_end = std::stoll(next());

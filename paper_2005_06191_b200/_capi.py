@@ -122,6 +122,15 @@ SIGNATURES = {
     "gm_result_write": (C.c_int, [_VP, C.c_char_p, _PS]),
     "gm_result_free": (None, [_VP]),
     "gm_release_cached_memory": (None, []),
+    "gm_result_read": (C.c_int, [C.c_char_p, C.POINTER(_VP), _PS]),
+    "gm_result_value_at": (C.c_int, [_VP, _VP, C.c_int32, C.c_int32, _D, _PS]),
+    "gm_model_sim_defaults": (C.c_int, [_VP, C.POINTER(C.c_int32), C.POINTER(C.c_uint64), _PS]),
+    "gm_simulate": (C.c_int, [_VP, _VP, _VP, C.c_int32, C.c_int32, C.c_uint64, C.c_int32, C.c_int32,
+                              C.POINTER(_VP), _PS]),
+    "gm_sim_summary": (C.c_int, [_VP, C.POINTER(C.c_int32), C.POINTER(_I64), _D, _PS]),
+    "gm_sim_copy": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _PS]),
+    "gm_sim_write_csv": (C.c_int, [_VP, C.c_char_p, _PS]),
+    "gm_sim_free": (None, [_VP]),
 }
 
 

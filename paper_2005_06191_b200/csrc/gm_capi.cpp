@@ -1308,3 +1308,334 @@ void gm_result_free(gm_result* r) { delete r; }
 void gm_release_cached_memory(void) { flush_cache(); }
 
 } // extern "C"
+
+// ===========================================================================
+// results reader (read_results, io.cpp:181-230) and the closed-loop simulator
+// (simulate / roll_one / write_trajectory_csv, sim.cpp:16-154)
+// ===========================================================================
+
+struct gm_sim {
+    int n = 0, m = 0, p = 0, T = 0;
+    int32_t runs = 0;
+    bool traj = false;
+    std::vector<uint8_t> sat;
+    std::vector<int32_t> steps;
+    std::vector<double> states, inputs, dists; // [run][k][d], T+1 / T / T rows per run
+};
+
+namespace {
+
+struct ManifestR { // io.cpp:72-121
+    std::map<std::string, std::string> kv;
+    ManifestR(std::istream& is, const char* magic) {
+        std::string line;
+        if (!std::getline(is, line)) throw IoErr("empty container");
+        std::istringstream head(line);
+        std::string mg;
+        int version = 0;
+        head >> mg >> version;
+        if (mg != magic) throw IoErr("bad magic line '" + line + "'");
+        if (version != 1) throw IoErr("unsupported container version " + std::to_string(version));
+        while (std::getline(is, line)) {
+            if (line == "payload") return;
+            const auto eq = line.find('=');
+            if (eq == std::string::npos || line.empty() || line.back() != ';')
+                throw IoErr("malformed manifest line '" + line + "'");
+            auto trim = [](std::string s) {
+                const auto b = s.find_first_not_of(" \t");
+                const auto e = s.find_last_not_of(" \t");
+                return b == std::string::npos ? std::string{} : s.substr(b, e - b + 1);
+            };
+            kv[trim(line.substr(0, eq))] = trim(line.substr(eq + 1, line.size() - eq - 2));
+        }
+        throw IoErr("missing payload marker");
+    }
+    bool has(const std::string& k) const { return kv.count(k) != 0; }
+    const std::string& str(const std::string& k) const {
+        auto it = kv.find(k);
+        if (it == kv.end()) throw IoErr("manifest key '" + k + "' missing");
+        return it->second;
+    }
+    int64_t integer(const std::string& k) const { return std::stoll(str(k)); }
+    double number(const std::string& k) const { return std::stod(str(k)); }
+    std::vector<double> vec(const std::string& k) const {
+        const std::string& s = str(k);
+        if (s.size() < 2 || s.front() != '{' || s.back() != '}')
+            throw IoErr("manifest key '" + k + "' is not a vector");
+        std::vector<double> out;
+        std::istringstream iss(s.substr(1, s.size() - 2));
+        std::string item;
+        while (std::getline(iss, item, ',')) out.push_back(std::stod(item));
+        return out;
+    }
+    Grid grid(const std::string& prefix) const {
+        if (integer(prefix + ".dim") == 0) return grid_from({}, {}, {});
+        return grid_from(vec(prefix + ".lb"), vec(prefix + ".ub"), vec(prefix + ".eta"));
+    }
+};
+
+// contains(grid, x), grid.cpp:67-75
+bool grid_contains(const Grid& g, const std::vector<double>& x) {
+    if (static_cast<int>(x.size()) != g.dim()) return false;
+    for (int d = 0; d < g.dim(); ++d) {
+        const double t = (x[d] - g.lb[d]) / g.eta[d];
+        if (t < -0.5 - 1e-9 || t > static_cast<double>(g.count[d] - 1) + 0.5 + 1e-9) return false;
+    }
+    return true;
+}
+
+void put_shortest(std::ostream& os, double v) { // std::to_chars, sim.cpp:109-114
+    char buf[32];
+    auto r = std::to_chars(buf, buf + sizeof buf, v);
+    os.write(buf, r.ptr - buf);
+}
+
+} // namespace
+
+extern "C" {
+
+gm_code gm_result_read(const char* path, gm_result** out, gm_status* st) {
+    return guarded(st, [&] {
+        std::ifstream is(path, std::ios::binary);
+        if (!is) throw IoErr(std::string("cannot open '") + path + "'");
+        ManifestR mf(is, "gridmdp-results");
+        auto r = std::make_unique<gm_result>();
+        r->mode = mf.str("mode") == "matrix" ? GM_MODE_MATRIX : GM_MODE_OFA;
+        r->meta.noise.gamma = mf.number("gamma");
+        const std::string kind = mf.str("spec.type");
+        if (kind == "safety") r->meta.spec.kind = GM_SPEC_SAFETY;
+        else if (kind == "reachability" || kind == "reach") r->meta.spec.kind = GM_SPEC_REACH;
+        else if (kind == "reach-avoid" || kind == "reach_avoid") r->meta.spec.kind = GM_SPEC_REACH_AVOID;
+        else throw ConfigErr("unknown spec type '" + kind + "'");
+        r->meta.spec.horizon = static_cast<int>(mf.integer("spec.time_steps"));
+        if (mf.has("target.lb")) r->meta.spec.target = BoxV{mf.vec("target.lb"), mf.vec("target.ub")};
+        if (mf.has("avoid.lb")) r->meta.spec.avoid = BoxV{mf.vec("avoid.lb"), mf.vec("avoid.ub")};
+        r->meta.X = mf.grid("states");
+        r->meta.U = mf.grid("inputs");
+        r->meta.W = mf.grid("disturbances");
+        std::istringstream vshape(mf.str("array.values"));
+        std::string tag;
+        int64_t n_x = 0;
+        int cols = 0;
+        vshape >> tag >> n_x >> cols;
+        if (tag != "f64" || n_x != r->meta.X.total || cols != r->meta.spec.horizon + 1)
+            throw IoErr("values array shape disagrees with the manifest");
+        std::istringstream ashape(mf.str("array.absorbing"));
+        int64_t n_abs = 0;
+        int one = 0;
+        ashape >> tag >> n_abs >> one;
+        if (tag != "u8" || (n_abs != 0 && n_abs != n_x)) throw IoErr("absorbing array shape disagrees with the manifest");
+        const int T = r->meta.spec.horizon;
+        r->n_x = n_x;
+        r->T = T;
+        const size_t nx = static_cast<size_t>(n_x);
+        std::vector<char> buf(nx * (T + 1) * 8);
+        auto get = [&](size_t bytes) {
+            buf.resize(bytes);
+            is.read(buf.data(), static_cast<std::streamsize>(bytes));
+            if (!is) throw IoErr("truncated payload");
+        };
+        // state-major on disk (io.cpp:171-177), column-major in memory
+        get(nx * (T + 1) * 8);
+        r->values.resize(nx * (T + 1));
+        for (size_t i = 0; i < nx; ++i)
+            for (int k = 0; k <= T; ++k)
+                std::memcpy(&r->values[static_cast<size_t>(k) * nx + i], &buf[(i * (T + 1) + k) * 8], 8);
+        for (std::vector<uint32_t>* dst : {&r->policy, &r->worst}) {
+            get(nx * T * 4);
+            dst->resize(nx * T);
+            for (size_t i = 0; i < nx; ++i)
+                for (int k = 0; k < T; ++k)
+                    std::memcpy(&(*dst)[static_cast<size_t>(k) * nx + i], &buf[(i * T + k) * 4], 4);
+        }
+        r->absorbing.resize(static_cast<size_t>(n_abs));
+        if (n_abs > 0) {
+            is.read(reinterpret_cast<char*>(r->absorbing.data()), n_abs);
+            if (!is) throw IoErr("truncated payload");
+        }
+        char extra;
+        if (is.get(extra)) throw IoErr("trailing bytes after the declared payload");
+        *out = r.release();
+    });
+}
+
+gm_code gm_result_value_at(const gm_result* r, const double* x, int32_t n, int32_t k, double* v, gm_status* st) {
+    return guarded(st, [&] {
+        if (k < 0 || k > r->T) throw std::out_of_range("value_at: step outside [0, T]");
+        const std::vector<double> p(x, x + n);
+        const int64_t ix = grid_index(r->meta.X, p); // point_to_index (out_of_range outside)
+        *v = r->values[static_cast<size_t>(k) * static_cast<size_t>(r->n_x) + static_cast<size_t>(ix)];
+    });
+}
+
+gm_code gm_model_sim_defaults(const gm_model* m, int32_t* runs, uint64_t* seed, gm_status* st) {
+    return guarded(st, [&] {
+        *runs = m->M.cfg.runs;
+        *seed = m->M.cfg.seed;
+    });
+}
+
+gm_code gm_simulate(gm_model* m, const gm_result* res, const double* x0, int32_t n_x0, int32_t runs, uint64_t seed,
+                    int32_t worst_case, int32_t want_traj, gm_sim** out, gm_status* st) {
+    return guarded(st, [&] {
+        const Model& M = m->M;
+        const SpecV& spec = res->meta.spec; // cmd_simulate passes res.spec (gridmdp_main.cpp:130)
+        check_spec(spec, M.X);               // validate_spec, sim.cpp:88
+        if (runs < 1) throw ConfigErr("simulate: need at least one run");
+        const std::vector<double> x(x0, x0 + std::max(n_x0, 0));
+        if (!grid_contains(M.X, x)) throw std::out_of_range("simulate: x0 lies outside the quantized region");
+        if (spec.horizon > res->T || res->meta.X.total != M.X.total)
+            throw ConfigErr("simulate: synthesis result does not match the model/spec");
+        prepare(m);
+        const int n = M.X.dim(), mu = M.U.dim(), p = M.W.dim(), T = spec.horizon;
+        gmk::SimArgs A{};
+        A.runs = runs;
+        A.T = T;
+        A.reach = spec.reach() ? 1 : 0;
+        A.has_avoid = spec.avoid.dim() > 0 ? 1 : 0;
+        A.worst_case = worst_case ? 1 : 0;
+        A.seed = seed;
+        for (int d = 0; d < n; ++d) {
+            A.x0[d] = x[d];
+            if (spec.target.dim() == n) { A.tlo[d] = spec.target.lo[d]; A.thi[d] = spec.target.hi[d]; }
+            if (spec.avoid.dim() == n) { A.alo[d] = spec.avoid.lo[d]; A.ahi[d] = spec.avoid.hi[d]; }
+        }
+        const Grid& RX = res->meta.X;
+        const Grid& RU = res->meta.U;
+        for (int d = 0; d < RX.dim() && d < GMD_MAXD; ++d) {
+            A.rs_lb[d] = RX.lb[d];
+            A.rs_eta[d] = RX.eta[d];
+            A.rs_count[d] = RX.count[d];
+            A.rs_stride[d] = RX.stride[d];
+        }
+        A.ru_dim = RU.dim();
+        for (int d = 0; d < RU.dim() && d < GMD_MAXD; ++d) {
+            A.ru_lb[d] = RU.lb[d];
+            A.ru_eta[d] = RU.eta[d];
+            A.ru_stride[d] = RU.stride[d];
+        }
+        A.rs_n = res->n_x;
+        const size_t nT = static_cast<size_t>(res->n_x) * static_cast<size_t>(res->T);
+        DevBuf<uint32_t> d_pol, d_wst;
+        d_pol.ensure(std::max<size_t>(nT, 1), "policy table");
+        d_wst.ensure(std::max<size_t>(nT, 1), "worst-disturbance table");
+        if (nT) {
+            ck(cudaMemcpy(d_pol.p, res->policy.data(), nT * 4, cudaMemcpyHostToDevice), "policy table");
+            ck(cudaMemcpy(d_wst.p, res->worst.data(), nT * 4, cudaMemcpyHostToDevice), "worst-disturbance table");
+        }
+        A.policy = d_pol.p;
+        A.worst = d_wst.p;
+        const size_t R = static_cast<size_t>(runs);
+        DevBuf<uint8_t> d_sat;
+        DevBuf<int> d_steps;
+        DevBuf<double> d_st, d_in, d_ds;
+        d_sat.ensure(R, "run flags");
+        d_steps.ensure(R, "run steps");
+        A.satisfied = d_sat.p;
+        A.steps = d_steps.p;
+        if (want_traj) {
+            d_st.ensure(R * (T + 1) * std::max(n, 1), "trajectories");
+            d_in.ensure(R * T * std::max(mu, 1), "trajectories");
+            d_ds.ensure(R * T * std::max(p, 1), "trajectories");
+            A.states = d_st.p;
+            A.inputs = mu ? d_in.p : nullptr;
+            A.dists = p ? d_ds.p : nullptr;
+        }
+        A.err = m->d_err.p;
+        {
+            Launch L(gmk::KF_MISC, m->stream);
+            gmk::simulate(m->D, A, m->stream);
+        }
+        ck(cudaStreamSynchronize(m->stream), "simulate");
+        unsigned long long bad = ULLONG_MAX;
+        ck(cudaMemcpy(&bad, m->d_err.p, sizeof bad, cudaMemcpyDeviceToHost), "error slot");
+        if (bad != ULLONG_MAX) {
+            const unsigned long long none = ULLONG_MAX;
+            ck(cudaMemcpy(m->d_err.p, &none, sizeof none, cudaMemcpyHostToDevice), "error slot");
+            throw DomainErr("simulate: the dynamics hit a domain error in run " + std::to_string(bad));
+        }
+        auto s = std::make_unique<gm_sim>();
+        s->n = n;
+        s->m = mu;
+        s->p = p;
+        s->T = T;
+        s->runs = runs;
+        s->traj = want_traj != 0;
+        s->sat.resize(R);
+        s->steps.resize(R);
+        ck(cudaMemcpy(s->sat.data(), d_sat.p, R, cudaMemcpyDeviceToHost), "run flags");
+        ck(cudaMemcpy(s->steps.data(), d_steps.p, R * 4, cudaMemcpyDeviceToHost), "run steps");
+        if (want_traj) {
+            s->states.resize(R * (T + 1) * n);
+            s->inputs.resize(R * T * mu);
+            s->dists.resize(R * T * p);
+            if (n) ck(cudaMemcpy(s->states.data(), d_st.p, s->states.size() * 8, cudaMemcpyDeviceToHost), "trajectories");
+            if (mu) ck(cudaMemcpy(s->inputs.data(), d_in.p, s->inputs.size() * 8, cudaMemcpyDeviceToHost), "trajectories");
+            if (p) ck(cudaMemcpy(s->dists.data(), d_ds.p, s->dists.size() * 8, cudaMemcpyDeviceToHost), "trajectories");
+        }
+        *out = s.release();
+    });
+}
+
+gm_code gm_sim_summary(const gm_sim* s, int32_t* runs, int64_t* satisfied, double* rate, gm_status* st) {
+    return guarded(st, [&] {
+        int64_t ok = 0;
+        for (uint8_t b : s->sat) ok += b;
+        *runs = s->runs;
+        *satisfied = ok;
+        if (s->runs < 1) throw ConfigErr("empirical_rate: empty batch");
+        *rate = static_cast<double>(ok) / static_cast<double>(s->runs); // empirical_rate, sim.cpp:103-108
+    });
+}
+
+gm_code gm_sim_copy(const gm_sim* s, uint8_t* satisfied, int32_t* steps, double* states, double* inputs,
+                    double* dists, gm_status* st) {
+    return guarded(st, [&] {
+        if (satisfied) std::memcpy(satisfied, s->sat.data(), s->sat.size());
+        if (steps) std::memcpy(steps, s->steps.data(), s->steps.size() * 4);
+        if ((states || inputs || dists) && !s->traj) throw ConfigErr("simulate: trajectories were not recorded");
+        if (states) std::memcpy(states, s->states.data(), s->states.size() * 8);
+        if (inputs) std::memcpy(inputs, s->inputs.data(), s->inputs.size() * 8);
+        if (dists) std::memcpy(dists, s->dists.data(), s->dists.size() * 8);
+    });
+}
+
+gm_code gm_sim_write_csv(const gm_sim* s, const char* path, gm_status* st) {
+    return guarded(st, [&] {
+        // write_trajectory_csv, sim.cpp:117-154
+        if (s->runs < 1) throw ConfigErr("write_trajectory_csv: empty batch");
+        if (!s->traj) throw ConfigErr("simulate: trajectories were not recorded");
+        std::ofstream os(path);
+        if (!os) throw IoErr(std::string("cannot open '") + path + "' for writing");
+        os << "run,k";
+        for (int d = 0; d < s->n; ++d) os << ",x" << d;
+        for (int d = 0; d < s->m; ++d) os << ",u" << d;
+        for (int d = 0; d < s->p; ++d) os << ",w" << d;
+        os << ",flag\n";
+        const size_t T = static_cast<size_t>(s->T);
+        for (size_t r = 0; r < static_cast<size_t>(s->runs); ++r) {
+            const int steps = s->steps[r];
+            for (int k = 0; k <= steps; ++k) {
+                os << r << ',' << k;
+                for (int d = 0; d < s->n; ++d) {
+                    os << ',';
+                    put_shortest(os, s->states[(r * (T + 1) + k) * s->n + d]);
+                }
+                for (int d = 0; d < s->m; ++d) {
+                    os << ',';
+                    if (k < steps) put_shortest(os, s->inputs[(r * T + k) * s->m + d]);
+                }
+                for (int d = 0; d < s->p; ++d) {
+                    os << ',';
+                    if (k < steps) put_shortest(os, s->dists[(r * T + k) * s->p + d]);
+                }
+                os << ',' << (s->sat[r] ? 1 : 0) << '\n';
+            }
+        }
+        if (!os) throw IoErr(std::string("failed while writing '") + path + "'");
+    });
+}
+
+void gm_sim_free(gm_sim* s) { delete s; }
+
+} // extern "C"

@@ -1075,6 +1075,185 @@ __global__ void k_mask(GmDev D, long long r_lo, long long nrows, double* probs,
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Closed-loop Monte Carlo (sim.cpp:16-101). Each run draws from its own
+// Philox4x32-10 stream keyed by derive_stream_seed(seed, run) (common.hpp:74-79),
+// so batches are reproducible for any launch shape. The reference draws from
+// libstdc++'s mt19937_64 + distributions; only the distributions agree, so
+// parity is statistical (tests/test_gpu_sim.py).
+// ---------------------------------------------------------------------------
+
+struct Philox {
+    uint32_t k0, k1, c0 = 0, c1 = 0;
+    uint64_t buf[2];
+    int left = 0;
+    __device__ Philox(uint64_t key) : k0(static_cast<uint32_t>(key)), k1(static_cast<uint32_t>(key >> 32)) {}
+    __device__ void refill() {
+        uint32_t x0 = c0, x1 = c1, x2 = 0, x3 = 0, a = k0, b = k1;
+#pragma unroll
+        for (int r = 0; r < 10; ++r) {
+            const uint32_t h0 = __umulhi(0xD2511F53u, x0), l0 = 0xD2511F53u * x0;
+            const uint32_t h1 = __umulhi(0xCD9E8D57u, x2), l1 = 0xCD9E8D57u * x2;
+            const uint32_t y0 = h1 ^ x1 ^ a, y1 = l1, y2 = h0 ^ x3 ^ b, y3 = l0;
+            x0 = y0; x1 = y1; x2 = y2; x3 = y3;
+            a += 0x9E3779B9u;
+            b += 0xBB67AE85u;
+        }
+        buf[0] = (static_cast<uint64_t>(x0) << 32) | x1;
+        buf[1] = (static_cast<uint64_t>(x2) << 32) | x3;
+        left = 2;
+        if (++c0 == 0) ++c1;
+    }
+    __device__ uint64_t next() {
+        if (!left) refill();
+        return buf[--left];
+    }
+    __device__ double uniform() { return static_cast<double>(next() >> 11) * 0x1.0p-53; } // [0, 1)
+    __device__ double normal() {                                                          // Box-Muller
+        const double u1 = 1.0 - uniform(), u2 = uniform();
+        return sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+    }
+    __device__ double gamma(double a) { // Marsaglia-Tsang, shape a, scale 1
+        double boost = 1.0;
+        if (a < 1.0) {
+            boost = pow(1.0 - uniform(), 1.0 / a);
+            a += 1.0;
+        }
+        const double d = a - 1.0 / 3.0, c = 1.0 / sqrt(9.0 * d);
+        for (;;) {
+            const double z = normal();
+            double v = 1.0 + c * z;
+            if (v <= 0.0) continue;
+            v = v * v * v;
+            const double u = 1.0 - uniform();
+            if (log(u) < 0.5 * z * z + d - d * v + d * log(v)) return d * v * boost;
+        }
+    }
+};
+
+__device__ __forceinline__ uint64_t derive_stream_seed(uint64_t master, uint64_t stream) {
+    uint64_t z = master + 0x9e3779b97f4a7c15ULL * (stream + 1);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+// contains(grid, x) (grid.cpp:67-75) for the model's state grid
+__device__ __forceinline__ bool in_region(const GmDev& D, const double* x) {
+    for (int d = 0; d < D.n; ++d) {
+        const double t = (x[d] - D.xlb[d]) / D.xeta[d];
+        if (t < -0.5 - kIdxTol || t > static_cast<double>(D.xcount[d] - 1) + 0.5 + kIdxTol) return false;
+    }
+    return true;
+}
+
+__device__ __forceinline__ bool in_spec_box(int n, const double* x, const double* lo, const double* hi) {
+    for (int d = 0; d < n; ++d)
+        if (!(x[d] >= lo[d] && x[d] <= hi[d])) return false;
+    return true;
+}
+
+// point_to_index (grid.cpp:77-96) on a region point: nearest representative, ties to +inf
+__device__ __forceinline__ long long nearest_index(int n, const double* x, const double* lb, const double* eta,
+                                                   const long long* count, const long long* stride) {
+    long long flat = 0;
+    for (int d = 0; d < n; ++d) {
+        long long j = static_cast<long long>(floor((x[d] - lb[d]) / eta[d] + 0.5));
+        if (j < 0) j = 0;
+        if (j >= count[d]) j = count[d] - 1;
+        flat += j * stride[d];
+    }
+    return flat;
+}
+
+__global__ void __launch_bounds__(128) k_simulate(GmDev D, SimArgs A) {
+    extern __shared__ __align__(16) unsigned char sim_sm[];
+    GmIns* sprog = reinterpret_cast<GmIns*>(sim_sm);
+    double* slits = reinterpret_cast<double*>(sim_sm + ((D.n_ins * sizeof(GmIns) + 15) / 16) * 16);
+    for (int i = threadIdx.x; i < D.n_ins; i += blockDim.x) sprog[i] = D.prog[i];
+    for (int i = threadIdx.x; i < D.n_lits; i += blockDim.x) slits[i] = D.lits[i];
+    __syncthreads();
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= A.runs) return;
+    Philox rng(derive_stream_seed(A.seed, static_cast<uint64_t>(r)));
+    const int n = D.n, m = D.m, p = D.p, T = A.T;
+    double x[GMD_MAXD], u[GMD_MAXD], w[GMD_MAXD], mu[GMD_MAXD];
+    for (int d = 0; d < n; ++d) x[d] = A.x0[d];
+    double* st = A.states ? A.states + static_cast<long long>(r) * (T + 1) * n : nullptr;
+    double* in = A.inputs ? A.inputs + static_cast<long long>(r) * T * m : nullptr;
+    double* ds = A.dists ? A.dists + static_cast<long long>(r) * T * p : nullptr;
+    if (st)
+        for (int d = 0; d < n; ++d) st[d] = x[d];
+    int state = 0; // 0 open, 1 satisfied, 2 failed
+    if (A.reach) { // immediate resolution at the start state; A wins over T
+        if (A.has_avoid && in_spec_box(n, x, A.alo, A.ahi)) state = 2;
+        else if (in_spec_box(n, x, A.tlo, A.thi)) state = 1;
+    }
+    int k = 0;
+    while (state == 0 && k < T) {
+        // query_policy(res, x, k+1)
+        const long long ix = nearest_index(n, x, A.rs_lb, A.rs_eta, A.rs_count, A.rs_stride);
+        long long iu = A.policy[static_cast<long long>(k) * A.rs_n + ix];
+        for (int d = 0; d < A.ru_dim; ++d) {
+            const long long j = iu / A.ru_stride[d];
+            iu -= j * A.ru_stride[d];
+            u[d] = A.ru_lb[d] + static_cast<double>(j) * A.ru_eta[d];
+        }
+        long long iw = 0;
+        if (D.n_w > 1) {
+            if (!A.worst_case) {
+                iw = static_cast<long long>(rng.uniform() * static_cast<double>(D.n_w));
+                if (iw >= D.n_w) iw = D.n_w - 1;
+            } else {
+                const long long jx = nearest_index(n, x, D.xlb, D.xeta, D.xcount, D.xstride);
+                iw = A.worst[static_cast<long long>(k) * D.n_x + jx];
+            }
+        }
+        long long rem = iw;
+        for (int d = 0; d < p; ++d) {
+            const long long j = rem / D.wstride[d];
+            rem -= j * D.wstride[d];
+            w[d] = D.wlb[d] + static_cast<double>(j) * D.weta[d];
+        }
+        double xi[GMD_MAXD];
+        for (int d = 0; d < n; ++d) { // sample_axis (noise.cpp:277-302)
+            double v;
+            switch (D.family) {
+                case GM_NORMAL: v = D.s[d] * 0.70710678118654752440 * rng.normal(); break; // s = sigma*sqrt2
+                case GM_UNIFORM: v = D.s[d] + (D.p2[d] - D.s[d]) * rng.uniform(); break;
+                case GM_EXPONENTIAL: v = -log1p(-rng.uniform()) / D.s[d]; break;
+                default: {
+                    const double ga = rng.gamma(D.s[d]), gb = rng.gamma(D.p2[d]);
+                    v = ga / (ga + gb);
+                }
+            }
+            xi[d] = D.mult ? v * x[d] : v;
+        }
+        if (!run_dynamics(D, sprog, slits, x, u, w, mu)) {
+            atomicMin(A.err, static_cast<unsigned long long>(r));
+            state = 2;
+            break;
+        }
+        if (in)
+            for (int d = 0; d < m; ++d) in[k * m + d] = u[d];
+        if (ds)
+            for (int d = 0; d < p; ++d) ds[k * p + d] = w[d];
+        for (int d = 0; d < n; ++d) x[d] = mu[d] + xi[d];
+        ++k;
+        if (st)
+            for (int d = 0; d < n; ++d) st[k * n + d] = x[d];
+        if (!in_region(D, x)) {
+            state = 2; // left the quantized region
+        } else if (A.reach) {
+            if (A.has_avoid && in_spec_box(n, x, A.alo, A.ahi)) state = 2;
+            else if (in_spec_box(n, x, A.tlo, A.thi)) state = 1;
+        }
+    }
+    if (state == 0) state = A.reach ? 2 : 1; // horizon exhausted
+    A.satisfied[r] = state == 1 ? 1 : 0;
+    A.steps[r] = k;
+}
 } // namespace
 
 // ---------------------------------------------------------------------------
@@ -1469,6 +1648,14 @@ void mask(const GmDev& D, long long r_lo, long long nrows, double* probs, const 
     blocks = std::min(blocks, num_sms() * 8);
     k_mask<<<blocks, kThreads, 0, s>>>(D, r_lo, nrows, probs, origins, inT, inA, axis_off);
     check_launch("mask");
+}
+
+void simulate(const GmDev& D, const SimArgs& A, cudaStream_t s) {
+    if (A.runs <= 0) return;
+    const size_t smem = ((D.n_ins * sizeof(GmIns) + 15) / 16) * 16 + D.n_lits * sizeof(double);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_simulate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_simulate<<<(A.runs + 127) / 128, 128, smem, s>>>(D, A);
+    check_launch("simulate");
 }
 
 } // namespace gmk

@@ -72,4 +72,31 @@ unsigned long long count_positive(const double* p, long long n, unsigned long lo
 void mask(const GmDev& D, long long r_lo, long long nrows, double* probs, const long long* origins,
           const uint8_t* inT, const uint8_t* inA, const long long* axis_off, cudaStream_t s);
 
+// Closed-loop Monte Carlo (simulate / roll_one, sim.cpp:16-101): one thread per
+// run. Grids of the synthesis result (query_policy, synthesis.cpp:230-239) next to
+// the model's (GmDev: dynamics, noise, disturbance grid, region check).
+struct SimArgs {
+    int runs, T, reach, has_avoid, worst_case;
+    unsigned long long seed;
+    double x0[GMD_MAXD];
+    double tlo[GMD_MAXD], thi[GMD_MAXD], alo[GMD_MAXD], ahi[GMD_MAXD]; // result spec boxes
+    // result grids: states (point_to_index) and inputs (index_to_point)
+    double rs_lb[GMD_MAXD], rs_eta[GMD_MAXD];
+    long long rs_count[GMD_MAXD], rs_stride[GMD_MAXD];
+    double ru_lb[GMD_MAXD], ru_eta[GMD_MAXD];
+    long long ru_stride[GMD_MAXD];
+    int ru_dim;
+    long long rs_n; // result states (column pitch of policy / worst_dist)
+    const uint32_t* policy; // [k][rs_n] (column-major n_x x T)
+    const uint32_t* worst;  // [k][n_x] of the model's state grid
+    // outputs (trajectories optional, [run][k][d])
+    unsigned char* satisfied;
+    int* steps;
+    double* states;
+    double* inputs;
+    double* dists;
+    unsigned long long* err; // lowest run hitting a dynamics domain error
+};
+void simulate(const GmDev& D, const SimArgs& A, cudaStream_t s);
+
 } // namespace gmk

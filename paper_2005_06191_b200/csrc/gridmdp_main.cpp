@@ -167,6 +167,73 @@ int cmd_export_prism(const Args& a) {
     return 0;
 }
 
+// parse_point (tools/gridmdp_main.cpp:56-71)
+bool parse_point(const std::string& s, std::vector<double>& out, int& rc) {
+    if (s.size() < 2 || s.front() != '{' || s.back() != '}') {
+        std::cerr << "error: --x0 expects a braced vector like {0, 0}\n";
+        rc = 2;
+        return false;
+    }
+    const std::string inner = s.substr(1, s.size() - 2);
+    size_t pos = 0;
+    try {
+        while (pos <= inner.size()) {
+            const size_t comma = inner.find(',', pos);
+            const std::string item = comma == std::string::npos ? inner.substr(pos) : inner.substr(pos, comma - pos);
+            out.push_back(std::stod(item));
+            if (comma == std::string::npos) break;
+            pos = comma + 1;
+        }
+    } catch (const std::exception& e) { // std::invalid_argument / out_of_range from stod
+        std::cerr << "error: " << e.what() << "\n";
+        rc = dynamic_cast<const std::out_of_range*>(&e) ? 4 : 1;
+        return false;
+    }
+    return true;
+}
+
+int cmd_simulate(const Args& a) {
+    // tools/gridmdp_main.cpp:119-140: closed-loop Monte Carlo under a stored result
+    gm_model* m = nullptr;
+    gm_sizes sz;
+    if (int rc = load(a, &m, &sz)) return rc;
+    const std::string rp = a.results.empty() ? std::string(gm_model_output_path(m)) : a.results;
+    if (rp.empty()) {
+        std::cerr << "error: simulate needs --results or exec.output in the config\n";
+        return 2;
+    }
+    gm_status st;
+    gm_result* res = nullptr;
+    if (gm_result_read(rp.c_str(), &res, &st) != GM_OK) return fail(st);
+    std::vector<double> x0;
+    int rc = 0;
+    if (!parse_point(a.x0, x0, rc)) return rc;
+    int32_t runs = 0;
+    uint64_t seed = 0;
+    if (gm_model_sim_defaults(m, &runs, &seed, &st) != GM_OK) return fail(st);
+    if (a.device != 0 && gm_set_device(a.device, &st) != GM_OK) return fail(st);
+    gm_sim* sim = nullptr;
+    if (gm_simulate(m, res, x0.data(), static_cast<int32_t>(x0.size()), runs, seed, a.dist_mode == "worst-case",
+                    a.traj.empty() ? 0 : 1, &sim, &st) != GM_OK)
+        return fail(st);
+    int32_t n = 0;
+    int64_t ok = 0;
+    double rate = 0.0, v = 0.0;
+    if (gm_sim_summary(sim, &n, &ok, &rate, &st) != GM_OK) return fail(st);
+    std::cout << "runs: " << n << "\n";
+    std::cout << "empirical_rate: " << rate << "\n";
+    if (gm_result_value_at(res, x0.data(), static_cast<int32_t>(x0.size()), 0, &v, &st) != GM_OK) return fail(st);
+    std::cout << "value_at_x0: " << v << "\n";
+    if (!a.traj.empty()) {
+        if (gm_sim_write_csv(sim, a.traj.c_str(), &st) != GM_OK) return fail(st);
+        std::cout << "trajectories: " << a.traj << "\n";
+    }
+    gm_sim_free(sim);
+    gm_result_free(res);
+    gm_model_free(m);
+    return 0;
+}
+
 int not_in_engine(const std::string& verb) {
     std::cerr << "error: '" << verb
               << "' is outside the B200 engine's hot path (MDP construction + synthesis); use the reference CLI\n";
@@ -247,8 +314,15 @@ int main(int argc, char** argv) {
                 std::cerr << "--mode: " << a.mode << " not in {matrix,ofa}\n";
                 return 105;
             }
-        } else if (a.verb == "simulate" && (k == "--results" || k == "--x0" || k == "--dist-mode" || k == "--traj")) {
-            (void)val();
+        } else if (a.verb == "simulate" && k == "--results") a.results = val();
+        else if (a.verb == "simulate" && k == "--x0") a.x0 = val();
+        else if (a.verb == "simulate" && k == "--traj") a.traj = val();
+        else if (a.verb == "simulate" && k == "--dist-mode") {
+            a.dist_mode = val();
+            if (a.dist_mode != "random" && a.dist_mode != "worst-case") {
+                std::cerr << "--dist-mode: " << a.dist_mode << " not in {random,worst-case}\n";
+                return 105;
+            }
         } else {
             std::cerr << "The following argument was not expected: " << k << "\n";
             return 109;
@@ -262,6 +336,12 @@ int main(int argc, char** argv) {
         case 0: return cmd_estimate(a);
         case 1: return cmd_abstract(a);
         case 2: return cmd_synthesize(a);
+        case 3:
+            if (a.x0.empty()) {
+                std::cerr << "--x0 is required\n";
+                return 106;
+            }
+            return cmd_simulate(a);
         case 4: return cmd_export_prism(a);
         default: return not_in_engine(a.verb);
     }

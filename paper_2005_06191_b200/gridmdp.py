@@ -575,5 +575,101 @@ def write_results(res: SynthesisResult, path: str) -> None:
     res.write(path)
 
 
+def read_results(path: str, model: Optional[SystemModel] = None) -> SynthesisResult:
+    """read_results (io.hpp:14, io.cpp:181-230): a `gridmdp-results 1` container."""
+    h = C.c_void_p()
+    call("gm_result_read", str(path).encode(), C.byref(h))
+    return _result_from_handle(model, None, h)
+
+
+def value_at(res: SynthesisResult, x, k: int = 0) -> float:
+    """values(point_to_index(state_grid, x), k) (gridmdp_main.cpp:133-134)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    v = C.c_double()
+    call("gm_result_value_at", res._h, ptr(x), C.c_int32(x.size), C.c_int32(k), C.byref(v))
+    return v.value
+
+
+@dataclass
+class TrajectoryBatch:
+    """sim.hpp:24-27: per-run outcome and (optionally) the rollouts, [run][k][d]
+    arrays with T+1 state rows and T input / disturbance rows per run; a run that
+    resolves early uses the first steps[r] (+1) rows."""
+
+    runs: int
+    satisfied: np.ndarray
+    steps: np.ndarray
+    states: Optional[np.ndarray] = None
+    inputs: Optional[np.ndarray] = None
+    dists: Optional[np.ndarray] = None
+    _h: Optional[C.c_void_p] = field(default=None, repr=False)
+
+    def __del__(self):
+        if self._h:
+            lib.gm_sim_free(self._h)
+            self._h = None
+
+    def empirical_rate(self) -> float:
+        return empirical_rate(self)
+
+    def write_csv(self, path: str) -> None:
+        write_trajectory_csv(self, path)
+
+
+def simulate(m: SystemModel, spec: Optional[Spec], res: SynthesisResult, x0, runs: Optional[int] = None,
+             seed: Optional[int] = None, dmode: str = "random", threads: int = 0,
+             trajectories: bool = False) -> TrajectoryBatch:
+    """simulate (sim.hpp:42-44, sim.cpp:85-101) on the GPU, one thread per run, under
+    the result's policy and spec (as `gridmdp simulate` passes res.spec). runs / seed
+    default to the configuration's exec.runs / exec.seed. `spec` and `threads` are
+    accepted for signature parity; statistical (not stream) parity with the reference."""
+    del spec, threads
+    if dmode not in ("random", "worst_case", "worst-case"):
+        raise ConfigError(f"simulate: unknown disturbance mode '{dmode}'")
+    r0, s0 = C.c_int32(), C.c_uint64()
+    call("gm_model_sim_defaults", m.handle, C.byref(r0), C.byref(s0))
+    runs = r0.value if runs is None else int(runs)
+    seed = s0.value if seed is None else int(seed)
+    if res._h is None:  # tables built in Python: hand them to the engine
+        h0 = C.c_void_p()
+        v = np.asfortranarray(res.values, dtype=np.float64)
+        p = np.asfortranarray(res.policy, dtype=np.uint32)
+        w = np.asfortranarray(res.worst_dist, dtype=np.uint32)
+        m.use_spec(res.spec)
+        call("gm_result_from_tables", m.handle, ptr(v), ptr(p), ptr(w), C.byref(h0))
+        res._h = h0
+    x = np.ascontiguousarray(x0, dtype=np.float64)
+    h = C.c_void_p()
+    call("gm_simulate", m.handle, res._h, ptr(x), C.c_int32(x.size), C.c_int32(runs), C.c_uint64(seed),
+         C.c_int32(1 if dmode != "random" else 0), C.c_int32(1 if trajectories else 0), C.byref(h))
+    n_runs, sat_n, rate = C.c_int32(), C.c_int64(), C.c_double()
+    call("gm_sim_summary", h, C.byref(n_runs), C.byref(sat_n), C.byref(rate))
+    sat = np.empty(runs, dtype=np.uint8)
+    steps = np.empty(runs, dtype=np.int32)
+    st = inp = ds = None
+    if trajectories:
+        T = res.values.shape[1] - 1
+        sz = m.sizes()
+        n, mu, pd = int(sz.n_dim), int(sz.m_dim), int(sz.p_dim)
+        st = np.empty((runs, T + 1, n))
+        inp = np.empty((runs, T, mu))
+        ds = np.empty((runs, T, pd))
+    call("gm_sim_copy", h, ptr(sat), ptr(steps), ptr(st), ptr(inp) if inp is not None and inp.size else None,
+         ptr(ds) if ds is not None and ds.size else None)
+    return TrajectoryBatch(runs, sat.astype(bool), steps, st, inp, ds, h)
+
+
+def empirical_rate(batch: TrajectoryBatch) -> float:
+    """Fraction of satisfied runs (sim.cpp:103-108)."""
+    if batch.runs < 1:
+        raise ConfigError("empirical_rate: empty batch")
+    return float(np.count_nonzero(batch.satisfied)) / batch.runs
+
+
+def write_trajectory_csv(batch: TrajectoryBatch, path: str) -> None:
+    """write_trajectory_csv (sim.cpp:117-154)."""
+    call("gm_sim_write_csv", batch._h, str(path).encode())
+
+
 def launch_count() -> int:
     return int(lib.gm_launch_count())
