@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define GM_MAX_DIMS 8
+#define GM_MAX_DIMS 12
 
 typedef enum gm_code {
     GM_OK = 0,

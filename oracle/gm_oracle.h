@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define OC_MAXD 8
+#define OC_MAXD 12
 
 typedef struct oc_desc {
     int n, m, p; /* state / input / disturbance dims (p may be 0) */

@@ -139,7 +139,7 @@ class OracleModel:
         if rc:
             raise ValueError(f"oracle: {err.value.decode()} (rc={rc})")
         self.h = h
-        out = (C.c_int64 * 13)()
+        out = (C.c_int64 * (5 + 12))()  # sizes + extents (OC_MAXD = 12)
         mem = C.c_uint64()
         lib().oc_sizes(h, out, C.byref(mem))
         self.n_x, self.n_u, self.n_w, self.rows, self.R = (int(out[i]) for i in range(5))

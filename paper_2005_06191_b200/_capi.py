@@ -14,7 +14,7 @@ PKG_DIR = Path(__file__).resolve().parent
 LIB_PATH = PKG_DIR / "libgridmdp_b200.so"
 CLI_PATH = PKG_DIR / "gridmdp"
 
-GM_MAX_DIMS = 8
+GM_MAX_DIMS = 12
 GM_OK, GM_ERR_OTHER, GM_ERR_CONFIG, GM_ERR_MEMORY, GM_ERR_DOMAIN, GM_ERR_IO, GM_ERR_RANGE, GM_ERR_CUDA = range(8)
 GM_MODE_MATRIX, GM_MODE_OFA = 0, 1
 GM_SAFETY, GM_REACH, GM_REACH_AVOID = 0, 1, 2

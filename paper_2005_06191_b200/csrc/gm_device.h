@@ -13,7 +13,7 @@ typedef unsigned long long uintptr_t;
 #include <stdint.h>
 #endif
 
-#define GMD_MAXD 8      // max state / input / disturbance dimensions on device
+#define GMD_MAXD 12     // max state / input / disturbance dimensions on device
 #define GMD_MAXREGS 32  // max dynamics-interpreter registers per row
 
 enum GmFamily { GM_NORMAL = 0, GM_UNIFORM = 1, GM_EXPONENTIAL = 2, GM_BETA = 3 };
@@ -100,6 +100,9 @@ struct GmDev {
     int mm_off, ml_off;      // offsets of the last two axes' masses (n == 1: mm_off = sumW, a 1.0 slot)
     GmFastDiv div_Wm, div_Wl, div_lines, div_P, div_mw; // n / d for n < 2^31 by multiply-shift
     GmFastDiv div_W[GMD_MAXD];
+    // prefix-table index a = sum_d j_d * Ps[d] over the s_axes leading axes (last fastest)
+    int Ps[GMD_MAXD];
+    GmFastDiv div_Ps[GMD_MAXD];
     // row decode by multiply-shift when every row index is < 2^31 (idx32)
     int idx32;
     GmFastDiv div_nw, div_nu, div_xs[GMD_MAXD], div_us[GMD_MAXD], div_ws[GMD_MAXD];

@@ -1191,6 +1191,14 @@ GmDev Model::device_descriptor() const {
     D.div_P = gm_fastdiv(static_cast<uint32_t>(D.P_size));
     D.div_mw = gm_fastdiv(static_cast<uint32_t>(D.sumW + 1));
     for (int d = 0; d < n; ++d) D.div_W[d] = gm_fastdiv(static_cast<uint32_t>(D.W[d]));
+    {
+        int64_t st = 1;
+        for (int d = D.s_axes - 1; d >= 0; --d) {
+            D.Ps[d] = static_cast<int>(st);
+            D.div_Ps[d] = gm_fastdiv(static_cast<uint32_t>(st));
+            st *= D.W[d];
+        }
+    }
     D.idx32 = rows() < (int64_t(1) << 31) ? 1 : 0;
     if (D.idx32) {
         D.div_nw = gm_fastdiv(static_cast<uint32_t>(D.n_w));

@@ -111,22 +111,7 @@ __device__ __forceinline__ void stage_tables(const GmDev& D, const Layout& Y, in
     const int mw = Y.mw;
     for (int c = threadIdx.x; c < rb * D.P_size; c += blockDim.x) {
         const int i = D.div_P.div(c), a = c - i * D.P_size;
-        const int mrow = i * mw;
-        int jv[GMD_MAXD];
-        int rem = a;
-#pragma unroll
-        for (int d = GMD_MAXD - 1; d >= 0; --d) { // row-major decode, last axis fastest
-            if (d < D.s_axes) {
-                const int q = D.div_W[d].div(rem);
-                jv[d] = rem - q * D.W[d];
-                rem = q;
-            }
-        }
-        double acc = 1.0;
-#pragma unroll
-        for (int d = 0; d < GMD_MAXD; ++d) // axis order, as the recursion multiplies
-            if (d < D.s_axes) acc *= g_sm[mrow + D.mass_off[d] + jv[d]];
-        g_sm[Y.offP + c] = acc;
+        g_sm[Y.offP + c] = prefix_product(D, g_sm + i * mw, a);
     }
     if (tab == TAB_Q) {
         __syncthreads();
@@ -1380,8 +1365,9 @@ void build(const GmDev& D, long long row0, long long nrows, long long* origin_ou
         static const char* bo2 = std::getenv("GM_BUILD_OPTS");
         const int wopts = bo2 ? std::atoi(bo2) : 0;
         const bool qs = build_uses_qs(D);
-        const size_t fixed_d = D.n_ins + D.n_lits + 1 + (qs ? (D.R + 1) / 2 + (kThreads / 32) * D.n_lines : 0);
-        const size_t per_d = 2 * (mw + D.P_size) + 42; // two table buffers + two prologue buffers
+        const size_t fixed_d = D.n_ins + D.n_lits + 3 + (qs ? (D.R + 1) / 2 + (kThreads / 32) * D.n_lines : 0);
+        // two table buffers + two prologue buffers (pro_doubles: <= (5n + 2) rb + 2 for both)
+        const size_t per_d = 2 * (mw + D.P_size) + 5 * static_cast<size_t>(D.n) + 2;
         const size_t budget_d = 54 * 1024 / sizeof(double); // 4 CTAs/SM
         if (fixed_d < budget_d) {
             long long rb = std::min<long long>(64, static_cast<long long>((budget_d - fixed_d) / per_d));

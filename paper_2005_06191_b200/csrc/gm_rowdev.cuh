@@ -340,6 +340,20 @@ __device__ __forceinline__ void record_error(unsigned long long* err, long long 
 
 extern __shared__ __align__(16) double g_sm[];
 
+// Prefix product of entry a of the P table (fill_product's recursion carried as
+// acc, abstraction.cpp:150-159): acc = ((1 * m0[j0]) * m1[j1]) * ... in axis
+// order, with (j0, j1, ...) decoded from a first axis first.
+__device__ __forceinline__ double prefix_product(const GmDev& D, const double* m, int a) {
+    double acc = 1.0;
+    int rem = a;
+    for (int d = 0; d < D.s_axes; ++d) {
+        const int j = D.div_Ps[d].div(rem);
+        rem -= j * D.Ps[d];
+        acc *= m[D.mass_off[d] + j];
+    }
+    return acc;
+}
+
 #if !defined(__CUDACC_RTC__) || defined(GM_JIT_PROLOGUE)
 // One thread per row: image, origin, per-axis masses (SoA, pitch nrows), T0x.
 __global__ void __launch_bounds__(kThreads) k_prologue(GmDev D, long long row0, long long nrows, int flags,
@@ -463,21 +477,23 @@ __device__ __forceinline__ void named_arrive(int id, int n) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-struct ProBuf { // one batch's prologue results in shared memory
-    double* mu;  // [rb][GMD_MAXD]
-    double* x;   // [rb][GMD_MAXD]
+struct ProBuf { // one batch's prologue results in shared memory (row stride n = state dim)
+    double* mu;  // [rb][n]
+    double* x;   // [rb][n]
     double* ok;  // [rb]
-    int* org;    // [rb][GMD_MAXD]
+    int* org;    // [rb][n]
+    int n;
 };
 
-__device__ __forceinline__ int pro_doubles(int rb) { return 2 * rb * GMD_MAXD + rb + (rb * GMD_MAXD + 1) / 2; }
+__device__ __forceinline__ int pro_doubles(int rb, int n) { return 2 * rb * n + rb + (rb * n + 1) / 2; }
 
-__device__ __forceinline__ ProBuf pro_buf(int base, int rb) {
+__device__ __forceinline__ ProBuf pro_buf(int base, int rb, int n) {
     ProBuf p;
     p.mu = g_sm + base;
-    p.x = p.mu + rb * GMD_MAXD;
-    p.ok = p.x + rb * GMD_MAXD;
+    p.x = p.mu + rb * n;
+    p.ok = p.x + rb * n;
     p.org = reinterpret_cast<int*>(p.ok + rb);
+    p.n = n;
     return p;
 }
 
@@ -500,10 +516,10 @@ __device__ __forceinline__ void build_prologue(const GmDev& D, const GmIns* spro
                 long long flat = 0;
                 for (int d = 0; d < D.n; ++d) {
                     const long long o = slab_origin(D, d, mu[d]);
-                    pb.org[i * GMD_MAXD + d] = static_cast<int>(o);
+                    pb.org[i * pb.n + d] = static_cast<int>(o);
                     flat += o * D.xstride[d];
-                    pb.mu[i * GMD_MAXD + d] = mu[d];
-                    pb.x[i * GMD_MAXD + d] = x[d];
+                    pb.mu[i * pb.n + d] = mu[d];
+                    pb.x[i * pb.n + d] = x[d];
                 }
                 origin_out[r] = flat;
                 if (t0x_out) {
@@ -550,7 +566,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_build_ws(GmDev D, long long row
     const int mw = D.sumW + 1;
     const int R = static_cast<int>(D.R);
     const int nl = D.n_lines;
-    const int tsz = rb * (mw + D.P_size), psz = pro_doubles(rb);
+    const int tsz = rb * (mw + D.P_size), psz = pro_doubles(rb, D.n);
     const int offT = 0, offPro = offT + 2 * tsz, offQs = offPro + 2 * psz;
     const int offProg = offQs + (QS ? (kThreads / 32) * nl : 0);
     GmIns* sprog = reinterpret_cast<GmIns*>(g_sm + offProg);
@@ -584,7 +600,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_build_ws(GmDev D, long long row
     }
     __syncthreads();
     if (role == 0 && first_row(0) < nrows)
-        build_prologue(D, sprog, slits, row0, nrows, first_row(0), rb, threadIdx.x, np, pro_buf(offPro, rb),
+        build_prologue(D, sprog, slits, row0, nrows, first_row(0), rb, threadIdx.x, np, pro_buf(offPro, rb, D.n),
                        origin_out, t0x_out, err);
     __syncthreads();
     for (long long i = -1; first_row(i < 0 ? 0 : i) < nrows; ++i) {
@@ -593,19 +609,19 @@ __global__ void __launch_bounds__(kThreads, 4) k_build_ws(GmDev D, long long row
             const long long bn = first_row(i + 2);
             if (bn < nrows)
                 build_prologue(D, sprog, slits, row0, nrows, bn, rb, threadIdx.x, np,
-                               pro_buf(offPro + static_cast<int>((i + 2) & 1) * psz, rb), origin_out, t0x_out, err);
+                               pro_buf(offPro + static_cast<int>((i + 2) & 1) * psz, rb, D.n), origin_out, t0x_out, err);
         } else if (role == 1) {
             const long long bn = first_row(i + 1);
             if (bn < nrows) {
-                const ProBuf cur = pro_buf(offPro + static_cast<int>((i + 1) & 1) * psz, rb);
+                const ProBuf cur = pro_buf(offPro + static_cast<int>((i + 1) & 1) * psz, rb, D.n);
                 double* tb = g_sm + offT + static_cast<int>((i + 1) & 1) * tsz;
                 // fill_axis_masses (abstraction.cpp:130-146): thread per (row, axis)
                 for (int c = ct; c < rb * D.n; c += nc) {
                     const int d = c / rb, r = c - d * rb;
                     if (cur.ok[r] != 0.0) {
                         bool ok = true;
-                        axis_masses(D, d, cur.org[r * GMD_MAXD + d], cur.mu[r * GMD_MAXD + d],
-                                    D.mult ? cur.x[r * GMD_MAXD + d] : 1.0, tb + r * mw + D.mass_off[d], 1, ok);
+                        axis_masses(D, d, cur.org[r * cur.n + d], cur.mu[r * cur.n + d],
+                                    D.mult ? cur.x[r * cur.n + d] : 1.0, tb + r * mw + D.mass_off[d], 1, ok);
                         if (!ok) record_error(err, row0 + bn + r);
                     } else {
                         for (int t = 0; t < D.W[d]; ++t) tb[r * mw + D.mass_off[d] + t] = 1.0;
@@ -617,21 +633,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_build_ws(GmDev D, long long row
                 double* P = tb + rb * mw;
                 for (int c = ct; c < rb * D.P_size; c += nc) {
                     const int r = D.div_P.div(c), a = c - r * D.P_size;
-                    int jv[GMD_MAXD];
-                    int rem = a;
-#pragma unroll
-                    for (int d = GMD_MAXD - 1; d >= 0; --d) {
-                        if (d < D.s_axes) {
-                            const int q = D.div_W[d].div(rem);
-                            jv[d] = rem - q * D.W[d];
-                            rem = q;
-                        }
-                    }
-                    double acc = 1.0;
-#pragma unroll
-                    for (int d = 0; d < GMD_MAXD; ++d)
-                        if (d < D.s_axes) acc *= tb[r * mw + D.mass_off[d] + jv[d]];
-                    P[c] = acc;
+                    P[c] = prefix_product(D, tb + r * mw, a);
                 }
             }
         }

@@ -316,6 +316,23 @@ def parse_config(text: str, name: str = "<config>", **overrides) -> SystemModel:
     return _model_from_text(text, name, overrides)
 
 
+def benchmark_chain_config(n: int) -> str:
+    """benchmark_chain_config (config.hpp:70, config.cpp:374-394): the Table-3 scaling
+    family as configuration text: n states in {0, 1}^n, x_i' = 0.9 x_i + 0 u0, normal
+    noise sigma 0.5, cutting probability 0.05, safety, T = 6, matrix mode."""
+    if n < 1:
+        raise ConfigError("benchmark_chain_config: dimension must be positive")
+    z, one = ", ".join(["0.0"] * n), ", ".join(["1.0"] * n)
+    lines = [f"states.dim = {n};", f"states.lb = {{{z}}};", f"states.ub = {{{one}}};",
+             f"states.eta = {{{one}}};", "inputs.dim = 1;", "inputs.lb = {0.0};", "inputs.ub = {0.0};",
+             "inputs.eta = {1.0};"]
+    lines += [f"dynamics.x{i} = 0.9*x{i} + 0*u0;" for i in range(n)]
+    lines += ["noise.type = normal;", f"noise.sigma = {{{', '.join(['0.5'] * n)}}};",
+              "noise.cutting_probability = 0.05;", "spec.type = safety;", "spec.time_steps = 6;",
+              "exec.mode = matrix;"]
+    return "\n".join(lines) + "\n"
+
+
 def make_model(state: Grid, input: Grid, disturbance: Optional[Grid], dynamics: Sequence[str],
                noise: NoiseSpec, constants: Optional[dict] = None) -> SystemModel:
     """make_model (model.hpp:40-42) from grids, expression texts and noise."""

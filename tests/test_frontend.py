@@ -140,3 +140,14 @@ def test_cli_exit_codes(tmp_path):
     r = _cli("abstract", "-c", d)
     import torch
     assert r.returncode == (4 if torch.cuda.is_available() else 1)
+
+
+def test_benchmark_chain_generator_sizes():
+    """benchmark_chain_config (config.cpp:374-394), test_config_io.cpp:137-143: n_x = 2^n, one input,
+    for n = 1..12 (the engine's dimension limit is 12 per grid)."""
+    from paper_2005_06191_b200 import gridmdp as g
+    for n in range(1, 13):
+        s = g.parse_config(g.benchmark_chain_config(n)).sizes()
+        assert s.n_states == 1 << n and s.n_inputs == 1
+    with pytest.raises(g.ConfigError):
+        g.benchmark_chain_config(0)
