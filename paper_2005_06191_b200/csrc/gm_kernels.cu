@@ -1505,7 +1505,9 @@ void expect_matrix(const GmDev& D, long long row0, long long r_lo, long long r_h
     // (per-term slab walk, 23 ms), ws (warp-specialised bulk ring, 28 ms), bulk
     // (CTA-synchronised ring, 25.6 ms), cp (per-warp cp.async double buffer, 32.8 ms).
     // Offsets held in registers instead of the table: 21.3 ms (92 registers) / equal
-    // (64 registers, spills); GM_CONTIG=1 (contiguous rows per CTA): equal.
+    // (64 registers, spills); GM_CONTIG=1 (contiguous rows per CTA): equal; V staged
+    // per chunk of states in shared memory (bounding box of the chunk's slabs): 23.2 ms
+    // (96-row chunks, 48 KB box; larger chunks lose occupancy: 31.7 ms at 200 rows).
     const bool allow_ws = force && std::string(force) == "ws";
     if (force && std::string(force) == "cp" && D.tpr == 32 && in_smem) {
         const size_t buf = ((static_cast<size_t>(D.R) * 8 + 16) + 15) / 16 * 16;
