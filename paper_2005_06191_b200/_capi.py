@@ -89,6 +89,7 @@ SIGNATURES = {
     "gm_model_output_path": (C.c_char_p, [_VP]),
     "gm_model_program_size": (C.c_int64, [_VP]),
     "gm_model_jit_status": (C.c_int32, [_VP, C.POINTER(C.c_double), C.c_char_p, C.c_int64]),
+    "gm_model_jit_compile": (C.c_int, [_VP, C.c_int32, C.POINTER(C.c_double), _PS]),
     "gm_set_device": (C.c_int, [C.c_int32, _PS]),
     "gm_model_set_stream": (C.c_int, [_VP, _VP, C.c_int32, _PS]),
     "gm_launch_count": (C.c_int64, []),

@@ -777,6 +777,13 @@ const char* gm_model_output_path(const gm_model* m) { return m->M.cfg.output.c_s
 
 int64_t gm_model_program_size(const gm_model* m) { return static_cast<int64_t>(m->M.prog.code.size()); }
 
+gm_code gm_model_jit_compile(const gm_model* m, int32_t kind, double* seconds, gm_status* st) {
+    return guarded(st, [&] {
+        const std::string err = gmj::compile_only(m->M.prog, m->M.X.dim(), kind, seconds);
+        if (!err.empty()) throw std::runtime_error(err);
+    });
+}
+
 int32_t gm_model_jit_status(const gm_model* m, double* compile_s, char* why, int64_t why_len) {
     if (compile_s) *compile_s = m->jit_compile_s;
     if (why && why_len > 0) {

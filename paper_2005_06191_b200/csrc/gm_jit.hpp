@@ -34,4 +34,9 @@ enum Want { WANT_PROLOGUE = 1, WANT_BUILD_NOQS = 2, WANT_BUILD_QS = 4 };
 // load failure, GM_JIT=0).
 const Kernels* kernels_for(const gmh::Program& P, int n, int want, std::string* why);
 
+// NVRTC compile of one kernel kind (0 k_prologue, 1 k_build_ws<false>, 2
+// k_build_ws<true>) without loading it: "" on success, else the compiler log.
+// Needs no GPU (tests run it on the build host).
+std::string compile_only(const gmh::Program& P, int n, int kind, double* seconds);
+
 } // namespace gmj

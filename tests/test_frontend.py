@@ -151,3 +151,18 @@ def test_benchmark_chain_generator_sizes():
         assert s.n_states == 1 << n and s.n_inputs == 1
     with pytest.raises(g.ConfigError):
         g.benchmark_chain_config(0)
+
+
+@pytest.mark.parametrize("case", ["chain09", "ref_bmw7_desk", "ref_vehicle3_desk", "domain", "mult1d", "beta1d",
+                                  "chain_bench12"])
+def test_dynamics_compile_for_sm100a(case):
+    """The generated straight-line dynamics (gm_jit.cpp) + gm_rowdev.cuh compile with NVRTC
+    for sm_100a (no GPU needed): ite / goto, domain checks, 7- and 12-dim models."""
+    import golden_io as G
+    from paper_2005_06191_b200 import _capi
+    from paper_2005_06191_b200 import gridmdp as g
+    e = G.manifest()["cases"][case]
+    m = g.load_config(str(G.case_cfg(case)), **G.case_overrides(e))
+    secs = ctypes.c_double()
+    _capi.call("gm_model_jit_compile", m.handle, ctypes.c_int32(0), ctypes.byref(secs))
+    assert secs.value > 0
