@@ -165,10 +165,14 @@ gm_code gm_matrix_copy_rows(const gm_matrix* tm, int64_t row_begin, int64_t row_
  * GM_ERR_CONFIG when the matrix carries none. */
 gm_code gm_matrix_copy_t0x(const gm_matrix* tm, int64_t row_begin, int64_t row_end, double* t0x_out,
                            gm_status* st);
-/* Device pointers and row range of a matrix (for stream-level callers). */
+/* Device pointers and row range of a matrix (for stream-level callers). Row r of
+ * d_probs starts at d_probs + (r - row_begin) * gm_matrix_pitch(tm): rows are padded
+ * with zeros to an aligned stride (>= row_width). */
 gm_code gm_matrix_info(const gm_matrix* tm, int64_t* row_begin, int64_t* row_end,
                        int64_t* row_width, const double** d_probs, const int64_t** d_origins,
                        gm_status* st);
+/* Row stride of the device payload in doubles. */
+int64_t gm_matrix_pitch(const gm_matrix* tm);
 /* write_matrix (io.hpp:19, io.cpp:236-256): the raw `gridmdp-matrix 1` container. */
 gm_code gm_matrix_write(const gm_matrix* tm, const gm_model* m, const char* path, gm_status* st);
 /* export_prism (io.hpp:21, io.cpp:289-317): PRISM explicit transitions

@@ -105,6 +105,7 @@ SIGNATURES = {
     "gm_matrix_copy_t0x": (C.c_int, [_VP, _I64, _I64, _VP, _PS]),
     "gm_matrix_info": (C.c_int, [_VP, C.POINTER(_I64), C.POINTER(_I64), C.POINTER(_I64), C.POINTER(_VP),
                                  C.POINTER(_VP), _PS]),
+    "gm_matrix_pitch": (C.c_int64, [_VP]),
     "gm_matrix_write": (C.c_int, [_VP, _VP, C.c_char_p, _PS]),
     "gm_matrix_write_prism": (C.c_int, [_VP, _VP, C.c_char_p, _PS]),
     "gm_matrix_free": (None, [_VP]),

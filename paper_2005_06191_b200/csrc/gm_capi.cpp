@@ -297,6 +297,7 @@ static const gmj::Kernels* jit_kernels(gm_model* m, int want, int64_t rows) {
 struct gm_matrix {
     int device = -1;
     int64_t row_begin = 0, row_end = 0, R = 0;
+    int64_t pitch = 0; // row stride of `probs` in doubles (>= R, zero padding)
     DevBuf<double> probs;
     DevBuf<long long> origins;
     DevBuf<double> t0x; // optional (shard builds for reach specs)
@@ -462,7 +463,8 @@ void build_rows(gm_model* m, int64_t r0, int64_t r1, gm_matrix* tm, bool want_t0
     tm->row_begin = r0;
     tm->row_end = r1;
     tm->R = m->M.R;
-    const uint64_t cells = mul_checked(static_cast<uint64_t>(n), static_cast<uint64_t>(m->M.R), "matrix size");
+    tm->pitch = m->D.pitch;
+    const uint64_t cells = mul_checked(static_cast<uint64_t>(n), static_cast<uint64_t>(tm->pitch), "matrix size");
     tm->probs.ensure(cells, "matrix payload");
     tm->origins.ensure(static_cast<size_t>(n), "matrix origins");
     if (want_t0x) {
@@ -479,7 +481,7 @@ void build_rows(gm_model* m, int64_t r0, int64_t r1, gm_matrix* tm, bool want_t0
         // on the aux stream, expansion of the previous chunk on the model stream
         const int64_t chunk = std::min(chunk_rows(m), n);
         ensure_scratch(m, chunk);
-        const int64_t R = m->M.R;
+        const int64_t R = tm->pitch;
         Launch L(gmk::KF_EXPAND, m->stream);
         pipeline(
             m, n, chunk, m->stream,
@@ -938,7 +940,9 @@ gm_code gm_matrix_copy_rows(const gm_matrix* tm, int64_t r0, int64_t r1, int64_t
         if (origins)
             ck(cudaMemcpy(origins, tm->origins.p + a, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost), "origins");
         if (probs)
-            ck(cudaMemcpy(probs, tm->probs.p + a * tm->R, static_cast<size_t>(n * tm->R) * 8, cudaMemcpyDeviceToHost),
+            ck(cudaMemcpy2D(probs, static_cast<size_t>(tm->R) * 8, tm->probs.p + a * tm->pitch,
+                            static_cast<size_t>(tm->pitch) * 8, static_cast<size_t>(tm->R) * 8, static_cast<size_t>(n),
+                            cudaMemcpyDeviceToHost),
                "probs");
     });
 }
@@ -954,6 +958,8 @@ gm_code gm_matrix_copy_t0x(const gm_matrix* tm, int64_t r0, int64_t r1, double* 
                "t0x");
     });
 }
+
+int64_t gm_matrix_pitch(const gm_matrix* tm) { return tm->pitch; }
 
 gm_code gm_matrix_info(const gm_matrix* tm, int64_t* rb, int64_t* re, int64_t* R, const double** probs,
                        const int64_t** origins, gm_status* st) {
@@ -997,7 +1003,10 @@ gm_code gm_matrix_write(const gm_matrix* tm, const gm_model* m, const char* path
         for (int64_t r = 0; r < rows; r += blk) {
             const int64_t n = std::min(blk, rows - r);
             buf.resize(static_cast<size_t>(n * tm->R));
-            ck(cudaMemcpy(buf.data(), tm->probs.p + r * tm->R, buf.size() * 8, cudaMemcpyDeviceToHost), "probs");
+            ck(cudaMemcpy2D(buf.data(), static_cast<size_t>(tm->R) * 8, tm->probs.p + r * tm->pitch,
+                            static_cast<size_t>(tm->pitch) * 8, static_cast<size_t>(tm->R) * 8, static_cast<size_t>(n),
+                            cudaMemcpyDeviceToHost),
+               "probs");
             for (double v : buf) put_f64(os, v);
         }
         if (!os) throw IoErr(std::string("failed while writing '") + path + "'");
@@ -1016,7 +1025,8 @@ gm_code gm_matrix_write_prism(const gm_matrix* tm, const gm_model* m, const char
         const int64_t rows = tm->row_end - tm->row_begin, R = tm->R;
         DevBuf<unsigned long long> cnt;
         cnt.ensure(1, "count");
-        const unsigned long long transitions = gmk::count_positive(tm->probs.p, rows * R, cnt.p, nullptr);
+        // padding is zero, so the count over rows x pitch is the count over the rows
+        const unsigned long long transitions = gmk::count_positive(tm->probs.p, rows * tm->pitch, cnt.p, nullptr);
         const int64_t choices = M.n_u() * M.n_w();
         os << M.n_x() << ' ' << rows << ' ' << transitions << '\n';
         const Grid& g = M.X;
@@ -1031,7 +1041,10 @@ gm_code gm_matrix_write_prism(const gm_matrix* tm, const gm_model* m, const char
             org.resize(static_cast<size_t>(nb));
             buf.resize(static_cast<size_t>(nb * R));
             ck(cudaMemcpy(org.data(), tm->origins.p + r0, org.size() * 8, cudaMemcpyDeviceToHost), "origins");
-            ck(cudaMemcpy(buf.data(), tm->probs.p + r0 * R, buf.size() * 8, cudaMemcpyDeviceToHost), "probs");
+            ck(cudaMemcpy2D(buf.data(), static_cast<size_t>(R) * 8, tm->probs.p + r0 * tm->pitch,
+                            static_cast<size_t>(tm->pitch) * 8, static_cast<size_t>(R) * 8, static_cast<size_t>(nb),
+                            cudaMemcpyDeviceToHost),
+               "probs");
             for (int64_t i = 0; i < nb; ++i) {
                 const int64_t r = r0 + i, src = r / choices, choice = r % choices;
                 // visit_slab (abstraction.hpp:130-149): row-major over the extents
@@ -1163,7 +1176,8 @@ gm_code gm_synthesize(gm_model* m, gm_result** out, gm_status* st) {
             size_t free_b = 0, total_b = 0;
             ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
             free_b += cached_bytes(); // released matrices kept for reuse count as free
-            const uint64_t dev_need = need + static_cast<uint64_t>(m->M.rows()) * 16;
+            const uint64_t dev_need = need + static_cast<uint64_t>(m->M.rows()) * 16 +
+                                      static_cast<uint64_t>(m->M.rows()) * static_cast<uint64_t>(m->D.pitch - m->M.R) * 8;
             if (dev_need > static_cast<uint64_t>(free_b)) {
                 std::ostringstream os;
                 os << "matrix mode needs " << dev_need << " bytes of device memory but only " << free_b

@@ -74,6 +74,7 @@ struct GmDev {
     int tpr;                 // threads per row in the expected-value kernels
     int n_ins, n_lits, nregs;
     long long n_x, n_u, n_w, rows, R;
+    long long pitch;         // row stride of stored matrices in doubles (R padded to an aligned granule)
 
     long long xcount[GMD_MAXD], xstride[GMD_MAXD];
     long long ustride[GMD_MAXD], wstride[GMD_MAXD];

@@ -1003,6 +1003,18 @@ uint64_t Model::memory_estimate() const {
     return payload + origins + 4096ULL;
 }
 
+int64_t row_pitch(int64_t R) {
+    // stored rows start on the largest power-of-two granule (<= GM_PITCH_GRANULE doubles,
+    // default 32 = 256 bytes) that costs at most 1/32 of padding: whole-line loads and stores
+    static const char* gr = std::getenv("GM_PITCH_GRANULE");
+    const int64_t top = gr ? std::max(1, std::atoi(gr)) : 32;
+    for (int64_t g = top; g >= 2; g /= 2) {
+        const int64_t p = (R + g - 1) / g * g;
+        if ((p - R) * 32 <= R) return p;
+    }
+    return R;
+}
+
 int tpr_for_width(int64_t R) {
     // Threads cooperating on one row's dot product (identical in matrix and
     // OFA mode, so both accumulate in the same order): ~16 terms per thread,
@@ -1148,6 +1160,7 @@ GmDev Model::device_descriptor() const {
     D.n_w = n_w();
     D.rows = rows();
     D.R = R;
+    D.pitch = row_pitch(R);
     for (int d = 0; d < n; ++d) {
         D.xcount[d] = X.count[d];
         D.xstride[d] = X.stride[d];

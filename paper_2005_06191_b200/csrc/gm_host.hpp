@@ -149,6 +149,7 @@ struct Model {
 Model build_model_from_cfg(const Cfg& cfg);
 SpecV spec_from_cfg(const Cfg& cfg);
 int tpr_for_width(int64_t R);
+int64_t row_pitch(int64_t R); // row stride of stored matrices (doubles)
 
 std::string fmt_shortest(double v);
 std::string fmt_vec(const std::vector<double>& v);

@@ -261,7 +261,8 @@ __global__ void __launch_bounds__(kThreads) k_expand(GmDev D, long long nrows, i
             if (row >= nrows) break;
             const int qo = Y.offQ + i * D.n_lines, po = Y.offP + i * D.P_size;
             const int mmo = i * Y.mw + D.mm_off, mlo = i * Y.mw + D.ml_off;
-            double* out = probs + row * D.R;
+            double* out = probs + row * D.pitch;
+            for (long long t = R + lane; t < D.pitch; t += 32) __stcs(out + t, 0.0); // row padding
             Walk w;
             w.init(D, lane, 32);
 #pragma unroll 4
@@ -386,7 +387,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_build(GmDev D, long long row0, 
                 if (row >= nrows) break;
                 const int qo = Y.offQ + i * D.n_lines, po = Y.offP + i * D.P_size;
                 const int mmo = i * mw + D.mm_off, mlo = i * mw + D.ml_off;
-                double* out = probs + row * D.R;
+                double* out = probs + row * D.pitch;
+                for (long long t = R + lane; t < D.pitch; t += 32) __stcs(out + t, 0.0); // row padding
                 const int head = (reinterpret_cast<uintptr_t>(out) & 15) ? 1 : 0; // element t at buf[t + head]
                 if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                 __syncwarp();
@@ -435,7 +437,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_build(GmDev D, long long row0, 
             if (row >= nrows) break;
             const int qo = Y.offQ + i * D.n_lines, po = Y.offP + i * D.P_size;
             const int mmo = i * mw + D.mm_off, mlo = i * mw + D.ml_off;
-            double* out = probs + row * D.R;
+            double* out = probs + row * D.pitch;
+            for (long long t = R + lane; t < D.pitch; t += 32) __stcs(out + t, 0.0); // row padding
             if (TAB == TAB_Q && use_tab) {
                 // warp-uniform walk (L0, k0) over 32-element windows; the lane offsets come
                 // from the per-CTA table tab[k0][lane] = (dL, k) of element k0 + lane
@@ -540,8 +543,8 @@ __global__ void __launch_bounds__(kThreads) k_expect_matrix(GmDev D, long long r
         const long long ra = (it2 * gridDim.x + blockIdx.x) * groups;
         if (ra >= nrows) return;
         const long long rz = ra + groups < nrows ? ra + groups : nrows;
-        const uintptr_t a = reinterpret_cast<uintptr_t>(probs + (r_lo + ra) * D.R) & ~uintptr_t(15);
-        const uintptr_t z = reinterpret_cast<uintptr_t>(probs + (r_lo + rz) * D.R) & ~uintptr_t(15);
+        const uintptr_t a = reinterpret_cast<uintptr_t>(probs + (r_lo + ra) * D.pitch) & ~uintptr_t(15);
+        const uintptr_t z = reinterpret_cast<uintptr_t>(probs + (r_lo + rz) * D.pitch) & ~uintptr_t(15);
         if (z > a)
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(static_cast<uint32_t>(z - a))
                          : "memory");
@@ -557,7 +560,7 @@ __global__ void __launch_bounds__(kThreads) k_expect_matrix(GmDev D, long long r
         if (valid && reach && D.absorb != nullptr) skip = D.absorb[(row0 + r) / nuw];
         double s = 0.0;
         if (!skip)
-            s = row_dot<0, 8, LS>(D, lane, tpr, probs + r * D.R, 0, 0, 0, 0, V + origins[r], D.line_off, Y.offL);
+            s = row_dot<0, 8, LS>(D, lane, tpr, probs + r * D.pitch, 0, 0, 0, 0, V + origins[r], D.line_off, Y.offL);
         s = group_reduce(s, tpr, Y.offR, g * tpr);
         if (valid && lane == 0) v_in[rl] = skip ? 0.0 : (reach ? s + t0x[r] : s);
     }
@@ -629,7 +632,7 @@ __global__ void __launch_bounds__(kThreads) k_expect_matrix_et(GmDev D, long lon
         }
         double s = 0.0;
         if (!skip) {
-            const double* pr = probs + r * R + lane;
+            const double* pr = probs + r * D.pitch + lane;
             const double* vb = V + origins[r];
             const int* e = E + lane;
             for (int b = 0; b < n_full; b += U) {
@@ -1056,7 +1059,7 @@ __global__ void k_mask(GmDev D, long long r_lo, long long nrows, double* probs,
             zt = zt && inT[c];
             if (inA) za = za && inA[c];
         }
-        if (zt || za) probs[(r_lo + rl) * D.R + (e - rl * D.R)] = 0.0;
+        if (zt || za) probs[(r_lo + rl) * D.pitch + (e - rl * D.R)] = 0.0;
     }
 }
 
@@ -1365,7 +1368,7 @@ void build(const GmDev& D, long long row0, long long nrows, long long* origin_ou
         static const char* bo2 = std::getenv("GM_BUILD_OPTS");
         const int wopts = bo2 ? std::atoi(bo2) : 0;
         const bool qs = build_uses_qs(D);
-        const size_t fixed_d = D.n_ins + D.n_lits + 3 + (qs ? (D.R + 1) / 2 + (kThreads / 32) * D.n_lines : 0);
+        const size_t fixed_d = D.n_ins + D.n_lits + 3 + (qs ? (D.pitch + 1) / 2 + (kThreads / 32) * D.n_lines : 0);
         // two table buffers + two prologue buffers (pro_doubles: <= (5n + 2) rb + 2 for both)
         const size_t per_d = 2 * (mw + D.P_size) + 5 * static_cast<size_t>(D.n) + 2;
         const size_t budget_d = 54 * 1024 / sizeof(double); // 4 CTAs/SM
@@ -1509,7 +1512,9 @@ void expect_matrix(const GmDev& D, long long row0, long long r_lo, long long r_h
     // per chunk of states in shared memory (bounding box of the chunk's slabs): 23.2 ms
     // (96-row chunks, 48 KB box; larger chunks lose occupancy: 31.7 ms at 200 rows).
     const bool allow_ws = force && std::string(force) == "ws";
-    if (force && std::string(force) == "cp" && D.tpr == 32 && in_smem) {
+    // the opt-in staged variants address rows at stride R (unpadded layouts only)
+    const bool unpadded = D.pitch == D.R;
+    if (force && std::string(force) == "cp" && D.tpr == 32 && in_smem && unpadded) {
         const size_t buf = ((static_cast<size_t>(D.R) * 8 + 16) + 15) / 16 * 16;
         const size_t smem = (kThreads / 32) * 2 * buf + (kThreads / 32) * sizeof(double) + table;
         if (smem <= 110 * 1024) {
@@ -1532,7 +1537,7 @@ void expect_matrix(const GmDev& D, long long row0, long long r_lo, long long r_h
         // a multiple of the group count: slot s is always consumed by group s % groups, so
         // a consumer is never more than one phase ahead of a slot's mbarrier (parity waits)
         ns -= ns % groups;
-        if (allow_ws && in_smem && ns >= groups && ns >= 4) {
+        if (allow_ws && in_smem && ns >= groups && ns >= 4 && unpadded) {
             const size_t smem = static_cast<size_t>(ns) * slot_b + tail_b + 2 * ns * sizeof(uint64_t) + 16;
             allow_smem(k_expect_matrix_ws<true>, smem);
             const long long nrows = r_hi - r_lo;
@@ -1548,7 +1553,7 @@ void expect_matrix(const GmDev& D, long long row0, long long r_lo, long long r_h
     }
     const size_t slot = ((static_cast<size_t>(groups) * D.R * 8 + 16) + 15) / 16 * 16;
     const size_t tail = (kThreads / 32) * sizeof(double) + 4 * sizeof(uint64_t) + (in_smem ? table : 0);
-    if (allow_bulk && in_smem && 2 * slot + tail <= kHardSmem) {
+    if (allow_bulk && in_smem && 2 * slot + tail <= kHardSmem && unpadded) {
         BulkPlan bp;
         bp.ns = (3 * slot + tail <= kHardSmem && 2 * slot + tail > 112 * 1024) ? 3 : 2;
         bp.slot_dbl = static_cast<int>(slot / 8);

@@ -577,9 +577,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_build_ws(GmDev D, long long row
     for (int c = threadIdx.x; c < D.n_lits; c += blockDim.x) slits[c] = D.lits[c];
     if (threadIdx.x < 2) claim[threadIdx.x] = 0;
     if (QS)
-        for (int t = threadIdx.x; t < R; t += blockDim.x) {
-            const int L = D.div_Wl.div(t);
-            ET[t] = (L * 8) | ((t - L * D.Wl) * 8) << 16;
+        for (int t = threadIdx.x; t < D.pitch; t += blockDim.x) { // entries past R: padding (unused)
+            const int L = D.div_Wl.div(t < R ? t : 0);
+            ET[t] = t < R ? (L * 8) | ((t - L * D.Wl) * 8) << 16 : 0;
         }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int np = npw * 32, nc = ncw * 32;
@@ -652,10 +652,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_build_ws(GmDev D, long long row
                 if (r >= rb || row >= nrows) break;
                 const double* m = tb + r * mw;
                 const double* Pr = P + r * D.P_size;
-                double* out = probs + row * D.R;
+                double* out = probs + row * D.pitch;
+                const int pitch = static_cast<int>(D.pitch); // rows end in zero padding up to the pitch
                 if (opts & 96) { // diagnostics: 32 = constant stores only, 64 = no stores
                     if (opts & 32)
-                        for (int t = lane; t < R; t += 32) __stcs(out + t, 0.0);
+                        for (int t = lane; t < pitch; t += 32) __stcs(out + t, 0.0);
                     continue;
                 }
                 if (QS) {
@@ -672,7 +673,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_build_ws(GmDev D, long long row
                                *reinterpret_cast<const double*>(mb + (e >> 16));
                     };
 #pragma unroll 4
-                    for (int t = lane; t < R; t += 32) __stcs(out + t, val(t));
+                    for (int t = lane; t < pitch; t += 32) __stcs(out + t, t < R ? val(t) : 0.0);
                     __syncwarp();
                 } else {
                     Walk wk = wk0;
@@ -681,6 +682,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_build_ws(GmDev D, long long row
                         __stcs(out + t, (Pr[wk.a] * m[D.mm_off + wk.j]) * m[D.ml_off + wk.k]);
                         wk.template next<true>();
                     }
+                    for (int t = R + lane; t < pitch; t += 32) __stcs(out + t, 0.0);
                 }
             }
         }
