@@ -33,6 +33,7 @@ namespace {
 struct Args {
     std::string cmd, config, out, vnext, results, x0, dist_mode = "random", traj;
     long long runs = -1, seed = -1;
+    std::string custom_pdf, custom_lb, custom_ub; // NoiseSpec::custom over the config's model
     int threads = -1, time_steps = -1;
     std::string mode;
     long long row_begin = -1, row_end = -1;
@@ -87,9 +88,43 @@ void print_sizes(const SystemModel& m) {
     std::cout << "memory_estimate_bytes: " << memory_estimate(m) << "\n";
 }
 
+std::vector<double> braced(const std::string& s) {
+    std::vector<double> v;
+    std::string inner = s.substr(1, s.size() - 2);
+    std::size_t pos = 0;
+    while (pos <= inner.size()) {
+        const std::size_t comma = inner.find(',', pos);
+        v.push_back(std::stod(comma == std::string::npos ? inner.substr(pos) : inner.substr(pos, comma - pos)));
+        if (comma == std::string::npos) break;
+        pos = comma + 1;
+    }
+    return v;
+}
+
+// The config's model, or -- with --custom-pdf -- the same grids and dynamics with
+// NoiseSpec::custom (noise.cpp:75-85) whose pdf callback evaluates the reference's
+// own expression language (parse_expression / eval, expr.hpp:66-74) over xi.
+SystemModel model_of(const Config& cfg, const Args& a) {
+    SystemModel m = build_model(cfg);
+    if (a.custom_pdf.empty()) return m;
+    const int n = m.state_dim();
+    const Expr e = parse_expression(a.custom_pdf, Dims{n, 0, 0}, cfg.constants);
+    CustomDensity cd;
+    cd.pdf = [e](const Vector& xi) { return eval(e, xi.data(), nullptr, nullptr); };
+    const std::vector<double> lo = braced(a.custom_lb), hi = braced(a.custom_ub);
+    Vector l(n), h(n);
+    for (int d = 0; d < n; ++d) {
+        l[d] = lo[static_cast<std::size_t>(d)];
+        h[d] = hi[static_cast<std::size_t>(d)];
+    }
+    cd.support = Box(l, h);
+    return make_model(m.state, m.input, m.disturbance, m.dynamics,
+                      NoiseSpec::custom(cd, m.noise.gamma(), m.noise.mode()));
+}
+
 int run(const Args& a) {
     const Config cfg = effective(a);
-    const SystemModel m = build_model(cfg);
+    const SystemModel m = model_of(cfg, a);
     if (a.cmd == "estimate") {
         print_sizes(m);
         return 0;
@@ -247,6 +282,9 @@ int main(int argc, char** argv) {
             else if (k == "--dist-mode") a.dist_mode = next();
             else if (k == "--traj") a.traj = next();
             else if (k == "--runs") a.runs = std::stoll(next());
+            else if (k == "--custom-pdf") a.custom_pdf = next();
+            else if (k == "--custom-lb") a.custom_lb = next();
+            else if (k == "--custom-ub") a.custom_ub = next();
             else if (k == "--seed") a.seed = std::stoll(next());
             else if (k == "--rows") {
                 a.row_begin = std::stoll(next());

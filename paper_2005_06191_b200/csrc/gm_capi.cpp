@@ -263,7 +263,7 @@ struct gm_model {
     DevBuf<uint8_t> d_absorb;
     DevBuf<unsigned long long> d_err;
     // step scratch
-    DevBuf<double> d_mass[2], d_t0x[2], d_vin;
+    DevBuf<double> d_mass[2], d_t0x[2], d_vin, d_chunk;
     DevBuf<long long> d_origin[2];
     DevBuf<uint8_t> d_rowflag[2];
     cudaStream_t aux = nullptr; // producer stream of the row-prologue pipeline
@@ -281,6 +281,11 @@ struct gm_model {
 // the launch covers >= 2^21 rows (a first compile costs 2-5 s, cached per process).
 static const gmj::Kernels* jit_kernels(gm_model* m, int want, int64_t rows) {
     std::string why;
+    if (m->M.noise.family == GM_CUSTOM) { // the quadrature kernels interpret the pdf
+        m->jit_used = false;
+        m->jit_why = "not used: custom densities run the bytecode interpreter";
+        return nullptr;
+    }
     const char* env = std::getenv("GM_JIT");
     if (!env && rows < (int64_t(1) << 21)) {
         m->jit_used = false;
@@ -405,6 +410,8 @@ void raise_device_error(gm_model* m) {
     } catch (const DomainErr& e) {
         throw DomainAt(e.what(), static_cast<int64_t>(row));
     }
+    if (m->M.noise.family == GM_CUSTOM)
+        throw DomainAt("adaptive_simpson: quadrature did not converge", static_cast<int64_t>(row));
     throw DomainAt("inc_beta: continued fraction did not converge", static_cast<int64_t>(row));
 }
 
@@ -476,7 +483,7 @@ void build_rows(gm_model* m, int64_t r0, int64_t r1, gm_matrix* tm, bool want_t0
         jit_kernels(m, (bp && bp[0] == '1') ? gmj::WANT_PROLOGUE
                                             : (gmk::build_uses_qs(m->D) ? gmj::WANT_BUILD_QS : gmj::WANT_BUILD_NOQS),
                     n);
-    if (bp && bp[0] == '1' && n > 0) {
+    if (bp && bp[0] == '1' && n > 0 && m->M.noise.family != GM_CUSTOM) {
         // row prologue (image, origin, per-axis masses into an L2-resident scratch chunk)
         // on the aux stream, expansion of the previous chunk on the model stream
         const int64_t chunk = std::min(chunk_rows(m), n);
@@ -516,6 +523,25 @@ void step_states(gm_model* m, gm_matrix* tm, int64_t x0, int64_t x1, const doubl
         Launch L(gmk::KF_EXPECT_MATRIX, s);
         gmk::expect_matrix(m->D, tm->row_begin, r0 - tm->row_begin, r1 - tm->row_begin, tm->probs.p,
                            tm->origins.p, tm->has_t0x ? tm->t0x.p : nullptr, v_next, m->d_vin.p, s);
+    } else if (n > 0 && m->M.noise.family == GM_CUSTOM) {
+        // custom densities: rows of a chunk are integrated into a transient matrix
+        // (k_build_custom) and dotted with V by the stored-matrix kernel
+        const int64_t pitch = m->D.pitch;
+        const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n, (64LL << 20) / 8 / std::max<int64_t>(pitch, 1)));
+        ensure_scratch(m, chunk);
+        m->d_chunk.ensure(static_cast<size_t>(chunk * pitch), "custom row chunk");
+        const bool reach = m->M.spec.reach();
+        for (int64_t c0 = 0; c0 < n; c0 += chunk) {
+            const int64_t cn = std::min(chunk, n - c0);
+            {
+                Launch L(gmk::KF_PROLOGUE, s);
+                gmk::build_custom(m->D, r0 + c0, cn, m->d_origin[0].p, reach ? m->d_t0x[0].p : nullptr, m->d_chunk.p,
+                                  m->d_err.p, s);
+            }
+            Launch L(gmk::KF_EXPECT_MATRIX, s);
+            gmk::expect_matrix(m->D, r0 + c0, 0, cn, m->d_chunk.p, m->d_origin[0].p, reach ? m->d_t0x[0].p : nullptr,
+                               v_next, m->d_vin.p + c0, s);
+        }
     } else if (n > 0) {
         const int64_t chunk = std::min(chunk_rows(m), n);
         ensure_scratch(m, chunk);
@@ -549,6 +575,11 @@ void ensure_t0x(gm_model* m, gm_matrix* tm) {
     for (int64_t c0 = 0; c0 < n; c0 += chunk) {
         const int64_t cn = std::min(chunk, n - c0);
         Launch L(gmk::KF_PROLOGUE, m->stream);
+        if (m->M.noise.family == GM_CUSTOM) {
+            gmk::build_custom(m->D, tm->row_begin + c0, cn, m->d_origin[0].p, tm->t0x.p + c0, nullptr, m->d_err.p,
+                              m->stream);
+            continue;
+        }
         gmk::prologue(m->D, tm->row_begin + c0, cn, gmk::PF_SKIP_ABSORBED | gmk::PF_T0X, m->d_origin[0].p,
                       tm->t0x.p + c0, m->d_rowflag[0].p, nullptr, m->d_err.p, m->stream, J ? J->prologue : nullptr);
     }
@@ -1500,6 +1531,8 @@ gm_code gm_simulate(gm_model* m, const gm_result* res, const double* x0, int32_t
                     int32_t worst_case, int32_t want_traj, gm_sim** out, gm_status* st) {
     return guarded(st, [&] {
         const Model& M = m->M;
+        if (M.noise.family == GM_CUSTOM)
+            throw ConfigErr("simulate: custom densities are not supported by the GPU simulator");
         const SpecV& spec = res->meta.spec; // cmd_simulate passes res.spec (gridmdp_main.cpp:130)
         check_spec(spec, M.X);               // validate_spec, sim.cpp:88
         if (runs < 1) throw ConfigErr("simulate: need at least one run");

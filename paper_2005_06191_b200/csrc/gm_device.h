@@ -16,7 +16,7 @@ typedef unsigned long long uintptr_t;
 #define GMD_MAXD 12     // max state / input / disturbance dimensions on device
 #define GMD_MAXREGS 32  // max dynamics-interpreter registers per row
 
-enum GmFamily { GM_NORMAL = 0, GM_UNIFORM = 1, GM_EXPONENTIAL = 2, GM_BETA = 3 };
+enum GmFamily { GM_NORMAL = 0, GM_UNIFORM = 1, GM_EXPONENTIAL = 2, GM_BETA = 3, GM_CUSTOM = 4 };
 enum GmCut { GM_CUT_NONE = 0, GM_CUT_DEGENERATE = 1, GM_CUT_RADIUS = 2 };
 enum GmSpecKind { GM_SPEC_SAFETY = 0, GM_SPEC_REACH = 1, GM_SPEC_REACH_AVOID = 2 };
 enum GmModeInt { GM_MODE_MATRIX_ = 0, GM_MODE_OFA_ = 1 };
@@ -87,6 +87,7 @@ struct GmDev {
     double inv_s[GMD_MAXD];  // normal: 1 / s (the device scales erf arguments by a multiply)
     double p2[GMD_MAXD];     // uniform b / beta beta
     double tlo[GMD_MAXD], thi[GMD_MAXD], alo[GMD_MAXD], ahi[GMD_MAXD];
+    double sup_lo[GMD_MAXD], sup_hi[GMD_MAXD]; // custom density support (noise coordinates)
     int W[GMD_MAXD];
     int mass_off[GMD_MAXD + 1];
 
@@ -108,7 +109,7 @@ struct GmDev {
     int idx32;
     GmFastDiv div_nw, div_nu, div_xs[GMD_MAXD], div_us[GMD_MAXD], div_ws[GMD_MAXD];
 
-    int entry[GMD_MAXD + 1]; // bytecode offsets of the n dynamics expressions
+    int entry[GMD_MAXD + 2]; // bytecode offsets of the n dynamics expressions (+ the custom pdf at n)
     const GmIns* prog;
     const double* lits;
     const int* line_off;     // n_lines relative flat offsets of slab lines

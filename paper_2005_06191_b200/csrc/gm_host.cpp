@@ -666,6 +666,9 @@ std::optional<std::vector<double>> cut_radius(const Noise& ns) {
         case GM_BETA:
             for (int i = 0; i < n; ++i) r[i] = 1.0;
             return r;
+        case GM_CUSTOM: // noise.cpp:172-177
+            for (int i = 0; i < n; ++i) r[i] = std::max(std::fabs(ns.p1[i]), std::fabs(ns.p2[i]));
+            return r;
     }
     return std::nullopt;
 }
@@ -698,6 +701,12 @@ Noise make_noise(int family, const std::vector<double>& a, const std::vector<dou
         case GM_EXPONENTIAL:
             need(all(a, [](double s) { return s > 0.0; }), "noise: exponential rates must be positive");
             break;
+        case GM_CUSTOM: { // noise.cpp:75-85
+            bool nonempty = !a.empty() && a.size() == b.size();
+            for (size_t i = 0; nonempty && i < a.size(); ++i) nonempty = a[i] <= b[i];
+            need(nonempty, "noise: custom density requires a non-empty support box");
+            break;
+        }
         case GM_BETA:
             need(a.size() == b.size(), "noise: beta shape dimension mismatch");
             need(all(a, [](double s) { return s > 0.0; }) && all(b, [](double s) { return s > 0.0; }),
@@ -827,6 +836,12 @@ public:
         } else if (c.noise_type == "beta") {
             c.alpha = vec("noise.alpha");
             c.beta = vec("noise.beta");
+        } else if (c.noise_type == "custom") {
+            // engine extension of NoiseSpec::custom (noise.hpp:16-19, noise.cpp:75-85):
+            // the joint pdf as an expression over the noise coordinates x0..x{n-1}
+            c.pdf = req("noise.pdf").value;
+            c.support_lb = vec("noise.support.lb");
+            c.support_ub = vec("noise.support.ub");
         } else {
             throw ConfigErr(name_ + ": unknown noise.type '" + c.noise_type + "'");
         }
@@ -946,6 +961,8 @@ private:
         per_state(c.rate, "noise.rate");
         per_state(c.alpha, "noise.alpha");
         per_state(c.beta, "noise.beta");
+        per_state(c.support_lb, "noise.support.lb");
+        per_state(c.support_ub, "noise.support.ub");
         auto box = [&](const std::optional<BoxCfg>& b, const char* key) {
             if (b && (static_cast<int>(b->lb.size()) != c.states.dim ||
                       static_cast<int>(b->ub.size()) != c.states.dim))
@@ -1056,6 +1073,16 @@ void Model::refresh() {
         nregs = std::max(nregs, L.maxreg);
         prog.entry.push_back(static_cast<int32_t>(prog.code.size()));
     }
+    if (noise.family == GM_CUSTOM) { // the pdf as expression n (noise coordinates in x)
+        Lowering L{noise.pdf, prog};
+        try {
+            L.gen(noise.pdf.root, 0);
+        } catch (const ConfigErr& e) {
+            throw ConfigErr(std::string("noise.pdf: ") + e.what());
+        }
+        nregs = std::max(nregs, L.maxreg);
+        prog.entry.push_back(static_cast<int32_t>(prog.code.size()));
+    }
     prog.nregs = nregs;
 }
 
@@ -1077,7 +1104,14 @@ Model build_model_from_cfg(const Cfg& c) {
     if (c.noise_type == "normal") M.noise = make_noise(GM_NORMAL, c.sigma, {}, g, c.noise_mult);
     else if (c.noise_type == "uniform") M.noise = make_noise(GM_UNIFORM, c.a, c.b, g, c.noise_mult);
     else if (c.noise_type == "exponential") M.noise = make_noise(GM_EXPONENTIAL, c.rate, {}, g, c.noise_mult);
-    else M.noise = make_noise(GM_BETA, c.alpha, c.beta, g, c.noise_mult);
+    else if (c.noise_type == "custom") {
+        M.noise = make_noise(GM_CUSTOM, c.support_lb, c.support_ub, g, c.noise_mult);
+        try {
+            M.noise.pdf = parse_expr_text(c.pdf, n, 0, 0, c.constants);
+        } catch (const ParseErr& e) {
+            throw ConfigErr(std::string("noise.pdf: ") + e.what());
+        }
+    } else M.noise = make_noise(GM_BETA, c.alpha, c.beta, g, c.noise_mult);
 
     // make_model checks (model.cpp:15-29)
     if (n == 0) throw ConfigErr("model: the state grid must have at least one dimension");
@@ -1220,7 +1254,12 @@ GmDev Model::device_descriptor() const {
         for (int d = 0; d < D.m; ++d) D.div_us[d] = gm_fastdiv(static_cast<uint32_t>(D.ustride[d]));
         for (int d = 0; d < D.p; ++d) D.div_ws[d] = gm_fastdiv(static_cast<uint32_t>(D.wstride[d]));
     }
-    for (size_t i = 0; i < prog.entry.size() && i <= GMD_MAXD; ++i) D.entry[i] = prog.entry[i];
+    for (size_t i = 0; i < prog.entry.size() && i <= GMD_MAXD + 1; ++i) D.entry[i] = prog.entry[i];
+    if (noise.family == GM_CUSTOM)
+        for (int d = 0; d < n; ++d) {
+            D.sup_lo[d] = noise.p1[d];
+            D.sup_hi[d] = noise.p2[d];
+        }
     return D;
 }
 

@@ -66,7 +66,8 @@ struct Noise {
     int family = GM_NORMAL;
     int mult = 0;
     double gamma = 0.0;
-    std::vector<double> p1, p2;
+    std::vector<double> p1, p2; // custom: support lower / upper corner
+    Expr pdf;                   // custom: joint density over xi (state variables x_i)
     int dim() const { return static_cast<int>(p1.size()); }
 };
 std::optional<std::vector<double>> cut_radius(const Noise& ns);
@@ -98,6 +99,8 @@ struct Cfg {
     int noise_mult = 0;
     double gamma = 0.0;
     std::vector<double> sigma, a, b, rate, alpha, beta;
+    std::string pdf;                       // noise.type = custom (engine extension)
+    std::vector<double> support_lb, support_ub;
     std::string spec_type;
     int time_steps = 0;
     std::optional<BoxCfg> target, avoid;

@@ -1242,6 +1242,159 @@ __global__ void __launch_bounds__(128) k_simulate(GmDev D, SimArgs A) {
     A.satisfied[r] = state == 1 ? 1 : 0;
     A.steps[r] = k;
 }
+
+// ---------------------------------------------------------------------------
+// Custom joint densities (NoiseSpec::custom, noise.cpp:75-85, 205-250): no
+// per-axis factorisation, every cell of a slab is the nested adaptive-Simpson
+// integral of the pdf over the cell's preimage in noise coordinates
+// (integrate_custom / adaptive_simpson, noise.cpp:208-221, 405-425), the pdf
+// being the program's expression n. Device recursion mirrors the reference's
+// (tolerance 1e-10 per level, depth limit 40); one warp per row.
+// ---------------------------------------------------------------------------
+
+struct CustomCtx {
+    const GmDev* D;
+    const GmIns* prog;
+    const double* lits;
+    double lo[GMD_MAXD], hi[GMD_MAXD], point[GMD_MAXD];
+    bool ok, conv;
+};
+
+__device__ double custom_integrate(CustomCtx& c, int level);
+
+__device__ __forceinline__ double custom_f(CustomCtx& c, int level, double t) {
+    c.point[level] = t;
+    if (level + 1 == c.D->n) {
+        double v = 0.0;
+        if (!run_expr(*c.D, c.prog, c.lits, c.D->n, c.point, nullptr, nullptr, v)) c.ok = false;
+        return v;
+    }
+    return custom_integrate(c, level + 1);
+}
+
+__device__ double simpson_rec(CustomCtx& c, int level, double a, double m, double b, double fa, double fm, double fb,
+                              double whole, double tol, int depth) {
+    const double lm = 0.5 * (a + m), rm = 0.5 * (m + b);
+    const double flm = custom_f(c, level, lm), frm = custom_f(c, level, rm);
+    const double left = (m - a) / 6.0 * (fa + 4.0 * flm + fm);
+    const double right = (b - m) / 6.0 * (fm + 4.0 * frm + fb);
+    if (depth > 40) {
+        c.conv = false;
+        return left + right;
+    }
+    if (fabs(left + right - whole) <= 15.0 * tol) return left + right + (left + right - whole) / 15.0;
+    const double lv = simpson_rec(c, level, a, lm, m, fa, flm, fm, left, tol / 2.0, depth + 1);
+    const double rv = simpson_rec(c, level, m, rm, b, fm, frm, fb, right, tol / 2.0, depth + 1);
+    return lv + rv;
+}
+
+__device__ double custom_integrate(CustomCtx& c, int level) {
+    const double lo = smax(c.lo[level], c.D->sup_lo[level]);
+    const double hi = smin(c.hi[level], c.D->sup_hi[level]);
+    if (hi <= lo) return 0.0;
+    const double m = 0.5 * (lo + hi);
+    const double fa = custom_f(c, level, lo), fm = custom_f(c, level, m), fb = custom_f(c, level, hi);
+    const double whole = (hi - lo) / 6.0 * (fa + 4.0 * fm + fb);
+    return simpson_rec(c, level, lo, m, hi, fa, fm, fb, whole, 1e-10, 0);
+}
+
+// cell_probability_impl, custom branch (noise.cpp:231-249): P(mean + s o xi in box)
+__device__ double custom_cell_prob(CustomCtx& c, const double* mean, const double* blo, const double* bhi,
+                                   const double* x) {
+    const GmDev& D = *c.D;
+    for (int d = 0; d < D.n; ++d) {
+        const double s = D.mult ? x[d] : 1.0;
+        if (s == 0.0) {
+            c.ok = false; // "multiplicative custom density degenerates at state 0"
+            return 0.0;
+        }
+        double a = s == 1.0 ? blo[d] - mean[d] : (blo[d] - mean[d]) / s;
+        double b = s == 1.0 ? bhi[d] - mean[d] : (bhi[d] - mean[d]) / s;
+        if (s < 0.0) {
+            const double t = a;
+            a = b;
+            b = t;
+        }
+        c.lo[d] = a;
+        c.hi[d] = b;
+    }
+    const double p = custom_integrate(c, 0);
+    return smin(1.0, smax(0.0, p));
+}
+
+// Stage (i) for custom densities: one warp per row (lane 0 runs the row
+// prologue, the lanes integrate the row's cells); probs may be null (T0x only).
+__global__ void __launch_bounds__(128) k_build_custom(GmDev D, long long row0, long long nrows,
+                                                     long long* __restrict__ origin_out,
+                                                     double* __restrict__ t0x_out, double* __restrict__ probs,
+                                                     unsigned long long* err) {
+    extern __shared__ __align__(16) unsigned char cu_sm[];
+    GmIns* sprog = reinterpret_cast<GmIns*>(cu_sm);
+    double* slits = reinterpret_cast<double*>(cu_sm + ((D.n_ins * sizeof(GmIns) + 15) / 16) * 16);
+    for (int i = threadIdx.x; i < D.n_ins; i += blockDim.x) sprog[i] = D.prog[i];
+    for (int i = threadIdx.x; i < D.n_lits; i += blockDim.x) slits[i] = D.lits[i];
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const long long wpb = blockDim.x >> 5;
+    const int n = D.n, R = static_cast<int>(D.R);
+    const bool reach = D.spec_kind != GM_SPEC_SAFETY;
+    CustomCtx c;
+    c.D = &D;
+    c.prog = sprog;
+    c.lits = slits;
+    for (long long row = blockIdx.x * wpb + (threadIdx.x >> 5); row < nrows; row += gridDim.x * wpb) {
+        double x[GMD_MAXD], u[GMD_MAXD], w[GMD_MAXD], mu[GMD_MAXD];
+        long long ix;
+        decode_row(D, row0 + row, ix, x, u, w);
+        int okd = 1;
+        if (lane == 0) okd = run_dynamics(D, sprog, slits, x, u, w, mu) ? 1 : 0;
+        okd = __shfl_sync(0xffffffffu, okd, 0);
+        if (!okd) {
+            if (lane == 0) record_error(err, row0 + row);
+            continue;
+        }
+        long long o[GMD_MAXD];
+        long long flat = 0;
+        for (int d = 0; d < n; ++d) {
+            mu[d] = __shfl_sync(0xffffffffu, mu[d], 0);
+            o[d] = slab_origin(D, d, mu[d]);
+            flat += o[d] * D.xstride[d];
+        }
+        if (lane == 0) {
+            if (origin_out) origin_out[row] = flat;
+            if (t0x_out) { // box_mass over the target (abstraction.cpp:187-191, 260-266)
+                double p = 0.0;
+                if (!(reach && D.absorb != nullptr && D.absorb[ix])) {
+                    c.ok = c.conv = true;
+                    p = custom_cell_prob(c, mu, D.tlo, D.thi, x);
+                    if (!c.ok || !c.conv) record_error(err, row0 + row);
+                }
+                t0x_out[row] = p;
+            }
+        }
+        if (!probs) continue;
+        double* out = probs + row * D.pitch;
+        for (int t = lane; t < D.pitch; t += 32) {
+            double v = 0.0;
+            if (t < R) { // fill_row, custom branch (abstraction.cpp:164-181): slab cell t
+                double blo[GMD_MAXD], bhi[GMD_MAXD];
+                int rem = t;
+                for (int d = n - 1; d >= 0; --d) {
+                    const int q = D.div_W[d].div(rem);
+                    const int j = rem - q * D.W[d];
+                    rem = q;
+                    const double rep = D.xlb[d] + static_cast<double>(o[d] + j) * D.xeta[d];
+                    blo[d] = rep - 0.5 * D.xeta[d];
+                    bhi[d] = rep + 0.5 * D.xeta[d];
+                }
+                c.ok = c.conv = true;
+                v = custom_cell_prob(c, mu, blo, bhi, x);
+                if (!c.ok || !c.conv) record_error(err, row0 + row);
+            }
+            out[t] = v;
+        }
+    }
+}
 } // namespace
 
 // ---------------------------------------------------------------------------
@@ -1356,11 +1509,32 @@ void expand(const GmDev& D, long long nrows, const double* mass, double* probs_o
 
 // Fused stage (i): rows per batch so that the per-row tables, prologue data and
 // the dynamics program fit the soft shared-memory budget.
+void build_custom(const GmDev& D, long long row0, long long nrows, long long* origin_out, double* t0x_out,
+                  double* probs_out, unsigned long long* d_err, cudaStream_t s) {
+    if (nrows <= 0) return;
+    // nested adaptive Simpson recurses up to 42 simpson_rec frames (~0.5 KB each,
+    // ptxas -v) per noise dimension: the per-thread stack must hold n of those chains
+    size_t stack = 0;
+    cudaDeviceGetLimit(&stack, cudaLimitStackSize);
+    const size_t want = 4096 + static_cast<size_t>(D.n) * 42 * 640;
+    if (stack < want && cudaDeviceSetLimit(cudaLimitStackSize, want) != cudaSuccess)
+        throw std::runtime_error("build_custom: cannot reserve the quadrature stack");
+    const size_t smem = ((D.n_ins * sizeof(GmIns) + 15) / 16) * 16 + D.n_lits * sizeof(double);
+    const long long blocks = std::min<long long>((nrows + 3) / 4, static_cast<long long>(num_sms()) * 16);
+    k_build_custom<<<static_cast<unsigned>(std::max<long long>(blocks, 1)), 128, smem, s>>>(D, row0, nrows, origin_out,
+                                                                                        t0x_out, probs_out, d_err);
+    check_launch("build_custom");
+}
+
 bool build_uses_qs(const GmDev& D) { return D.n_lines <= 512 && D.n_lines * 8 < 65536 && D.Wl * 8 < 32768; }
 
 void build(const GmDev& D, long long row0, long long nrows, long long* origin_out, double* t0x_out,
            double* probs_out, unsigned long long* d_err, cudaStream_t s, const void* const* jit_ws) {
     if (nrows <= 0) return;
+    if (D.family == GM_CUSTOM) {
+        build_custom(D, row0, nrows, origin_out, t0x_out, probs_out, d_err, s);
+        return;
+    }
     const size_t mw = static_cast<size_t>(D.sumW + 1);
     static const char* bw = std::getenv("GM_BUILD_WS"); // 0: single-role k_build
     if (!(bw && bw[0] == '0')) {

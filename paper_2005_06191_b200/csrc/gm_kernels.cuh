@@ -39,6 +39,10 @@ void prologue(const GmDev& D, long long row0, long long nrows, int flags, long l
 
 // Fused stage (i) (build_matrix body, abstraction.cpp:211-223): rows
 // [row0, row0+nrows) -> origins, stored rows (and target-hit masses if t0x_out).
+// Stage (i) for custom joint densities (nested quadrature per cell, k_build_custom);
+// probs_out may be null (origins and target-hit masses only).
+void build_custom(const GmDev& D, long long row0, long long nrows, long long* origin_out, double* t0x_out,
+                  double* probs_out, unsigned long long* d_err, cudaStream_t s);
 // Whether build() uses the per-warp line-prefix variant k_build_ws<true>.
 bool build_uses_qs(const GmDev& D);
 // jit_ws: run-time compiled k_build_ws<false>, k_build_ws<true> (gm_jit.cpp) or nullptr.

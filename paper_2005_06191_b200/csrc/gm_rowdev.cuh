@@ -86,78 +86,85 @@ __device__ __forceinline__ bool run_dynamics(const GmDev&, const GmIns*, const d
 #else
 // Dynamics bytecode interpreter (semantics of expr.cpp:404-480: IEEE double,
 // comparisons 1/0, lazy ite, domain errors). Returns false on a domain error.
+// One expression of the program (pc range entry[e]..entry[e+1]) into `out`;
+// false on a domain error.
+__device__ bool run_expr(const GmDev& D, const GmIns* __restrict__ prog, const double* __restrict__ lits, int e,
+                         const double* x, const double* u, const double* w, double& out) {
+    double r[GMD_MAXREGS];
+    int pc = D.entry[e];
+    const int end = D.entry[e + 1];
+    while (pc < end) {
+        const GmIns I = prog[pc++];
+        const double a = r[I.a];
+        const double b = r[I.b];
+        double v;
+        switch (I.op) {
+            case GI_LIT: v = lits[I.arg]; break;
+            case GI_LDX: v = x[I.arg]; break;
+            case GI_LDU: v = u[I.arg]; break;
+            case GI_LDW: v = w[I.arg]; break;
+            case GI_ADD: v = a + b; break;
+            case GI_SUB: v = a - b; break;
+            case GI_MUL: v = a * b; break;
+            case GI_DIV:
+                if (b == 0.0) return false;
+                v = a / b;
+                break;
+            case GI_POW:
+                if (a < 0.0 && b != floor(b)) return false;
+                if (a == 0.0 && b < 0.0) return false;
+                v = (b == 2.0) ? a * a : pow(a, b);
+                break;
+            case GI_LT: v = a < b ? 1.0 : 0.0; break;
+            case GI_LE: v = a <= b ? 1.0 : 0.0; break;
+            case GI_GT: v = a > b ? 1.0 : 0.0; break;
+            case GI_GE: v = a >= b ? 1.0 : 0.0; break;
+            case GI_EQ: v = a == b ? 1.0 : 0.0; break;
+            case GI_NE: v = a != b ? 1.0 : 0.0; break;
+            case GI_NEG: v = -a; break;
+            case GI_SIN: v = sin(a); break;
+            case GI_COS: v = cos(a); break;
+            case GI_TAN: v = tan(a); break;
+            case GI_ASIN:
+                if (a < -1.0 || a > 1.0) return false;
+                v = asin(a);
+                break;
+            case GI_ACOS:
+                if (a < -1.0 || a > 1.0) return false;
+                v = acos(a);
+                break;
+            case GI_ATAN: v = atan(a); break;
+            case GI_EXP: v = exp(a); break;
+            case GI_LN:
+                if (a <= 0.0) return false;
+                v = log(a);
+                break;
+            case GI_SQRT:
+                if (a < 0.0) return false;
+                v = sqrt(a);
+                break;
+            case GI_ABS: v = fabs(a); break;
+            case GI_MIN: v = fmin(a, b); break;
+            case GI_MAX: v = fmax(a, b); break;
+            case GI_JZ:
+                if (a == 0.0) pc = I.arg;
+                continue;
+            case GI_JMP:
+                pc = I.arg;
+                continue;
+            default: return false;
+        }
+        r[I.dst] = v;
+    }
+    out = r[0];
+    return true;
+}
+
 __device__ bool run_dynamics(const GmDev& D, const GmIns* __restrict__ prog,
                              const double* __restrict__ lits, const double* x, const double* u,
                              const double* w, double* mu) {
-    double r[GMD_MAXREGS];
-    for (int i = 0; i < D.n; ++i) {
-        int pc = D.entry[i];
-        const int end = D.entry[i + 1];
-        while (pc < end) {
-            const GmIns I = prog[pc++];
-            const double a = r[I.a];
-            const double b = r[I.b];
-            double v;
-            switch (I.op) {
-                case GI_LIT: v = lits[I.arg]; break;
-                case GI_LDX: v = x[I.arg]; break;
-                case GI_LDU: v = u[I.arg]; break;
-                case GI_LDW: v = w[I.arg]; break;
-                case GI_ADD: v = a + b; break;
-                case GI_SUB: v = a - b; break;
-                case GI_MUL: v = a * b; break;
-                case GI_DIV:
-                    if (b == 0.0) return false;
-                    v = a / b;
-                    break;
-                case GI_POW:
-                    if (a < 0.0 && b != floor(b)) return false;
-                    if (a == 0.0 && b < 0.0) return false;
-                    v = (b == 2.0) ? a * a : pow(a, b);
-                    break;
-                case GI_LT: v = a < b ? 1.0 : 0.0; break;
-                case GI_LE: v = a <= b ? 1.0 : 0.0; break;
-                case GI_GT: v = a > b ? 1.0 : 0.0; break;
-                case GI_GE: v = a >= b ? 1.0 : 0.0; break;
-                case GI_EQ: v = a == b ? 1.0 : 0.0; break;
-                case GI_NE: v = a != b ? 1.0 : 0.0; break;
-                case GI_NEG: v = -a; break;
-                case GI_SIN: v = sin(a); break;
-                case GI_COS: v = cos(a); break;
-                case GI_TAN: v = tan(a); break;
-                case GI_ASIN:
-                    if (a < -1.0 || a > 1.0) return false;
-                    v = asin(a);
-                    break;
-                case GI_ACOS:
-                    if (a < -1.0 || a > 1.0) return false;
-                    v = acos(a);
-                    break;
-                case GI_ATAN: v = atan(a); break;
-                case GI_EXP: v = exp(a); break;
-                case GI_LN:
-                    if (a <= 0.0) return false;
-                    v = log(a);
-                    break;
-                case GI_SQRT:
-                    if (a < 0.0) return false;
-                    v = sqrt(a);
-                    break;
-                case GI_ABS: v = fabs(a); break;
-                case GI_MIN: v = fmin(a, b); break;
-                case GI_MAX: v = fmax(a, b); break;
-                case GI_JZ:
-                    if (a == 0.0) pc = I.arg;
-                    continue;
-                case GI_JMP:
-                    pc = I.arg;
-                    continue;
-                default: return false;
-            }
-            r[I.dst] = v;
-        }
-        mu[i] = r[0];
-    }
+    for (int i = 0; i < D.n; ++i)
+        if (!run_expr(D, prog, lits, i, x, u, w, mu[i])) return false;
     return true;
 }
 #endif

@@ -133,7 +133,20 @@ class NoiseSpec:
     def beta(alpha, beta_, gamma, mode="additive"):
         return NoiseSpec("beta", tuple(map(float, alpha)), tuple(map(float, beta_)), float(gamma), mode)
 
+    @staticmethod
+    def custom(pdf: str, support_lo, support_hi, gamma, mode="additive"):
+        """NoiseSpec::custom (noise.hpp:16-19, noise.cpp:75-85) with the joint pdf given as an
+        expression over the noise coordinates x0..x{n-1} (the C++ API takes a callback)."""
+        return NoiseSpec("custom", tuple(map(float, support_lo)), tuple(map(float, support_hi)), float(gamma), mode,
+                         pdf)
+
+    pdf: str = ""
+
     def config_lines(self) -> list[str]:
+        if self.family == "custom":
+            return [f"noise.type = custom;", f"noise.mode = {self.mode};",
+                    f"noise.cutting_probability = {_fmt(self.gamma)};", f"noise.pdf = {self.pdf};",
+                    f"noise.support.lb = {_vec(self.p1)};", f"noise.support.ub = {_vec(self.p2)};"]
         keys = {"normal": ("sigma",), "uniform": ("a", "b"), "exponential": ("rate",), "beta": ("alpha", "beta")}[
             self.family]
         out = [f"noise.type = {self.family};", f"noise.mode = {self.mode};",

@@ -141,13 +141,41 @@ def main() -> None:
         (OUT / "_bad.bin").unlink(missing_ok=True)
 
     cases = sorted(p.stem for p in CASES.glob("*.cfg"))
+
+    def ref_case(cfgp: Path):
+        """(reference config, extra flags): custom-density cases (engine-format keys
+        noise.pdf / noise.support.*) run the reference through ref_driver --custom-*
+        on the same config with a placeholder noise (NoiseSpec::custom, noise.cpp:75-85)."""
+        text = cfgp.read_text()
+        if "noise.type = custom;" not in text:
+            return cfgp, []
+        kv = {}
+        keep = []
+        for raw in text.splitlines():
+            line = raw.split("#", 1)[0].strip()
+            k = line.split("=", 1)[0].strip() if "=" in line else ""
+            if k in ("noise.type", "noise.pdf", "noise.support.lb", "noise.support.ub"):
+                kv[k] = line.split("=", 1)[1].strip().rstrip(";").strip()
+            else:
+                keep.append(raw)
+        n = int(re.search(r"states.dim = (\d+);", text).group(1))
+        keep += ["noise.type = normal;", "noise.sigma = {" + ", ".join(["1.0"] * n) + "};"]
+        rp = OUT / f"_{cfgp.stem}.ref.cfg"
+        rp.write_text("\n".join(keep) + "\n")
+        return rp, ["--custom-pdf", kv["noise.pdf"], "--custom-lb", kv["noise.support.lb"], "--custom-ub",
+                    kv["noise.support.ub"]]
+
     rng = np.random.default_rng(20240)  # robot_safety.cfg:34 seed
     for c in cases:
-        cfgp = CASES / f"{c}.cfg"
+        cfgp0 = CASES / f"{c}.cfg"
+        cfgp, custom = ref_case(cfgp0)
         bundled = c[4:] if c.startswith("ref_") else None
-        extra = BUNDLED[bundled][1] if bundled else []
+        extra = (BUNDLED[bundled][1] if bundled else []) + custom
         modes = BUNDLED[bundled][2] if bundled else HAND_MODES.get(c, ["matrix", "ofa"])
-        entry = {"overrides": extra, "modes": {}, "files": {}}
+        entry = {"overrides": extra if not custom else (BUNDLED[bundled][1] if bundled else []), "modes": {},
+                 "files": {}}
+        if custom:
+            entry["custom_density"] = True
         est = ref("estimate", "-c", cfgp, *extra)
         entry["sizes"] = parse_sizes(est.stdout)
         rows, R = entry["sizes"]["rows"], entry["sizes"]["row_width"]
@@ -179,11 +207,11 @@ def main() -> None:
             f = OUT / f"{c}.prism.tra"
             ref("prism", "-c", cfgp, "-o", f, *extra)
             entry["files"]["prism"] = f.name
-            if "spec.type = safety" not in cfgp.read_text():
+            if "spec.type = safety" not in cfgp0.read_text():
                 f = OUT / f"{c}.masked.bin"
                 ref("masked-matrix", "-c", cfgp, "-o", f, *extra)
                 entry["files"]["masked"] = f.name
-        if "spec.type = safety" not in cfgp.read_text() and rows <= 100_000:
+        if "spec.type = safety" not in cfgp0.read_text() and rows <= 100_000:
             f = OUT / f"{c}.t0x.f64"
             ref("target-hit", "-c", cfgp, "-o", f, *extra)
             entry["files"]["t0x"] = f.name
@@ -197,6 +225,8 @@ def main() -> None:
             entry["files"]["vnext"] = vf.name
             entry["files"]["step_prefix"] = f"{c}.step"
         manifest["cases"][c] = entry
+        if custom:
+            cfgp.unlink()
         print(c, entry["sizes"], list(entry["modes"]), list(entry["files"]), flush=True)
     for f in OUT.iterdir():  # compress the raw binaries
         if f.suffix != ".gz":

@@ -11,7 +11,10 @@ import golden_io as G
 from oracle import oracle_py as O
 
 MAN = G.manifest()
-CASES = sorted(c for c, e in MAN["cases"].items() if "results" in e)
+# the C restatement covers the config-reachable families; custom densities (a C++
+# callback in the reference) are checked GPU-vs-reference only (tests/test_gpu_parity.py)
+_ORACLE = {c: e for c, e in MAN["cases"].items() if not e.get("custom_density")}
+CASES = sorted(c for c, e in _ORACLE.items() if "results" in e)
 
 
 def oracle(case):
@@ -36,7 +39,7 @@ def test_synthesis_bit_exact(case):
         assert np.array_equal(r["absorbing"], ref["absorbing"])
 
 
-@pytest.mark.parametrize("case", sorted(c for c, e in MAN["cases"].items() if "matrix" in e.get("files", {})))
+@pytest.mark.parametrize("case", sorted(c for c, e in _ORACLE.items() if "matrix" in e.get("files", {})))
 def test_matrix_bit_exact(case):
     e = MAN["cases"][case]
     want = G.read_matrix(G.load(e["files"]["matrix"]))
@@ -51,13 +54,13 @@ def test_matrix_bit_exact(case):
         assert np.array_equal(bits(p), bits(masked["probs"]))
 
 
-@pytest.mark.parametrize("case", sorted(c for c, e in MAN["cases"].items() if "t0x" in e.get("files", {})))
+@pytest.mark.parametrize("case", sorted(c for c, e in _ORACLE.items() if "t0x" in e.get("files", {})))
 def test_target_hit_bit_exact(case):
     want = np.frombuffer(G.load(MAN["cases"][case]["files"]["t0x"]), "<f8")
     assert np.array_equal(bits(oracle(case).target_hit()), bits(want))
 
 
-@pytest.mark.parametrize("case", sorted(c for c, e in MAN["cases"].items() if "step_prefix" in e.get("files", {})))
+@pytest.mark.parametrize("case", sorted(c for c, e in _ORACLE.items() if "step_prefix" in e.get("files", {})))
 def test_bellman_step_bit_exact(case):
     m = oracle(case)
     for mode in ("ofa", "matrix"):
