@@ -109,9 +109,27 @@ __device__ __forceinline__ const int* sm_ints() { return reinterpret_cast<const 
 // Builds the prefix tables P (and Q) from the staged masses of rb rows.
 __device__ __forceinline__ void stage_tables(const GmDev& D, const Layout& Y, int rb, int tab) {
     const int mw = Y.mw;
-    for (int c = threadIdx.x; c < rb * D.P_size; c += blockDim.x) {
-        const int i = D.div_P.div(c), a = c - i * D.P_size;
-        g_sm[Y.offP + c] = prefix_product(D, g_sm + i * mw, a);
+    if (D.s_axes == 0) {
+        for (int i = threadIdx.x; i < rb; i += blockDim.x) g_sm[Y.offP + i] = 1.0;
+    } else {
+        // one item per (row, run of the last prefix axis): the prefix over the other
+        // axes once, then W_last products -- the association of prefix_product
+        const int last = D.s_axes - 1, wl = D.W[last];
+        const int nb = D.P_size / wl;
+        for (int c = threadIdx.x; c < rb * nb; c += blockDim.x) {
+            const int i = c / nb, b = c - i * nb;
+            const double* m = g_sm + i * mw;
+            double acc = 1.0;
+            int rem = b * wl;
+            for (int d = 0; d < last; ++d) {
+                const int j = D.div_Ps[d].div(rem);
+                rem -= j * D.Ps[d];
+                acc *= m[D.mass_off[d] + j];
+            }
+            double* P = g_sm + Y.offP + i * D.P_size + b * wl;
+            const double* ml = m + D.mass_off[last];
+            for (int j = 0; j < wl; ++j) P[j] = acc * ml[j];
+        }
     }
     if (tab == TAB_Q) {
         __syncthreads();
@@ -128,20 +146,13 @@ __device__ __forceinline__ void stage_tables(const GmDev& D, const Layout& Y, in
             }
             return;
         }
-        // wide rows: per row, lanes stride L by blockDim with an incremental (a, j)
-        const int st = blockDim.x;
-        const int qa = D.div_Wm.div(st), qj = st - qa * D.Wm;
-        const int a0 = D.div_Wm.div(threadIdx.x), j0 = threadIdx.x - a0 * D.Wm;
-        for (int i = 0; i < rb; ++i) {
-            const int po = Y.offP + i * D.P_size, mo = i * mw + D.mm_off, qo = Y.offQ + i * D.n_lines;
-            int a = a0, j = j0;
-            for (int L = threadIdx.x; L < D.n_lines; L += st) {
-                g_sm[qo + L] = g_sm[po + a] * g_sm[mo + j];
-                j += qj;
-                const int c = j >= D.Wm;
-                j -= c ? D.Wm : 0;
-                a += qa + c;
-            }
+        // wide rows: one item per (row, prefix entry a): its Wm lines Q[a*Wm + j]
+        for (int c = threadIdx.x; c < rb * D.P_size; c += blockDim.x) {
+            const int i = D.div_P.div(c), a = c - i * D.P_size;
+            const double pa = g_sm[Y.offP + c];
+            const double* mm = g_sm + i * mw + D.mm_off;
+            double* q = g_sm + Y.offQ + i * D.n_lines + a * D.Wm;
+            for (int j = 0; j < D.Wm; ++j) q[j] = pa * mm[j];
         }
     }
 }
