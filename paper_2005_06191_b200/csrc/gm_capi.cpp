@@ -478,29 +478,9 @@ void build_rows(gm_model* m, int64_t r0, int64_t r1, gm_matrix* tm, bool want_t0
         tm->t0x.ensure(static_cast<size_t>(n), "target-hit vector");
         tm->has_t0x = true;
     }
-    static const char* bp = std::getenv("GM_BUILD_PIPE");
     const gmj::Kernels* J =
-        jit_kernels(m, (bp && bp[0] == '1') ? gmj::WANT_PROLOGUE
-                                            : (gmk::build_uses_qs(m->D) ? gmj::WANT_BUILD_QS : gmj::WANT_BUILD_NOQS),
-                    n);
-    if (bp && bp[0] == '1' && n > 0 && m->M.noise.family != GM_CUSTOM) {
-        // row prologue (image, origin, per-axis masses into an L2-resident scratch chunk)
-        // on the aux stream, expansion of the previous chunk on the model stream
-        const int64_t chunk = std::min(chunk_rows(m), n);
-        ensure_scratch(m, chunk);
-        const int64_t R = tm->pitch;
-        Launch L(gmk::KF_EXPAND, m->stream);
-        pipeline(
-            m, n, chunk, m->stream,
-            [&](int64_t c0, int64_t cn, int b) {
-                gmk::prologue(m->D, r0 + c0, cn, gmk::PF_MASSES | (want_t0x ? gmk::PF_T0X : 0),
-                              tm->origins.p + c0, want_t0x ? tm->t0x.p + c0 : nullptr, m->d_rowflag[b].p,
-                              m->d_mass[b].p, m->d_err.p, m->aux, J ? J->prologue : nullptr);
-            },
-            [&](int64_t c0, int64_t cn, int b) {
-                gmk::expand(m->D, cn, m->d_mass[b].p, tm->probs.p + c0 * R, m->stream);
-            });
-    } else {
+        jit_kernels(m, gmk::build_uses_qs(m->D) ? gmj::WANT_BUILD_QS : gmj::WANT_BUILD_NOQS, n);
+    {
         Launch L(gmk::KF_EXPAND, m->stream);
         gmk::build(m->D, r0, n, tm->origins.p, want_t0x ? tm->t0x.p : nullptr, tm->probs.p, m->d_err.p, m->stream,
                    J ? J->build_ws : nullptr);

@@ -252,41 +252,6 @@ __device__ __forceinline__ double row_dot(const GmDev& D, int lane, int tpr, con
     return s;
 }
 
-// Stage (i) expansion: a warp writes one row's R products lane-strided
-// (coalesced 256-byte stores, evict-first).
-template <int TAB>
-__global__ void __launch_bounds__(kThreads) k_expand(GmDev D, long long nrows, int rb, GmFastDiv div_rb,
-                                                    const double* __restrict__ mass,
-                                                    double* __restrict__ probs) {
-    const Layout Y(D, rb, TAB);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nwarps = blockDim.x >> 5;
-    const int R = static_cast<int>(D.R);
-    for (long long b0 = static_cast<long long>(blockIdx.x) * rb; b0 < nrows;
-         b0 += static_cast<long long>(gridDim.x) * rb) {
-        __syncthreads();
-        stage_rows(D, Y, mass, nrows, b0, rb, div_rb, TAB);
-        __syncthreads();
-        for (int i = warp; i < rb; i += nwarps) {
-            const long long row = b0 + i;
-            if (row >= nrows) break;
-            const int qo = Y.offQ + i * D.n_lines, po = Y.offP + i * D.P_size;
-            const int mmo = i * Y.mw + D.mm_off, mlo = i * Y.mw + D.ml_off;
-            double* out = probs + row * D.pitch;
-            for (long long t = R + lane; t < D.pitch; t += 32) __stcs(out + t, 0.0); // row padding
-            Walk w;
-            w.init(D, lane, 32);
-#pragma unroll 4
-            for (int t = lane; t < R; t += 32) {
-                const double p = TAB == TAB_Q ? g_sm[qo + w.L] * g_sm[mlo + w.k]
-                                              : (g_sm[po + w.a] * g_sm[mmo + w.j]) * g_sm[mlo + w.k];
-                __stcs(out + t, p);
-                w.template next<TAB == TAB_P>();
-            }
-        }
-    }
-}
-
 // Stage (i), fused: each CTA batch evaluates its rows' prologue (image, origin,
 // target-hit mass: one thread per row), their per-axis cell masses (one thread
 // per row x cell), the prefix tables, then streams the R products of every row
@@ -294,7 +259,7 @@ __global__ void __launch_bounds__(kThreads) k_expand(GmDev D, long long nrows, i
 // overlaps the store phase of the others on the same SM.
 template <int TAB>
 __global__ void __launch_bounds__(kThreads, 4) k_build(GmDev D, long long row0, long long nrows, int rb,
-                                                   GmFastDiv div_rb, int rowbuf_off, int vec_copy,
+                                                   GmFastDiv div_rb,
                                                    long long* __restrict__ origin_out,
                                                    double* __restrict__ t0x_out, double* __restrict__ probs,
                                                    unsigned long long* err) {
@@ -317,16 +282,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_build(GmDev D, long long row0, 
     const bool reach = D.spec_kind != GM_SPEC_SAFETY;
     Walk wk0;
     wk0.init(D, lane, 32);
-    // store-walk table (TAB_Q, W_last <= 64): tab[k0][l] = ((k0 + l) / Wl) | ((k0 + l) % Wl) << 16
-    const bool use_tab = false; // table-driven store walk: measured slower (30.0 vs 25.6 ms on C2b)
-    int* stab = reinterpret_cast<int*>(g_sm + offProg + D.n_ins + D.n_lits);
-    const int c32L = D.div_Wl.div(32), c32k = 32 - c32L * D.Wl;
-    if (TAB == TAB_Q && use_tab)
-        for (int c = threadIdx.x; c < D.Wl * 32; c += blockDim.x) {
-            const int k0 = c >> 5, l = c & 31, e = k0 + l;
-            const int dL = D.div_Wl.div(e);
-            stab[c] = dL | ((e - dL * D.Wl) << 16);
-        }
     for (long long b0 = static_cast<long long>(blockIdx.x) * rb; b0 < nrows;
          b0 += static_cast<long long>(gridDim.x) * rb) {
         __syncthreads();
@@ -388,61 +343,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_build(GmDev D, long long row0, 
         __syncthreads();
         stage_tables(D, Y, rb, TAB);
         __syncthreads();
-        if (rowbuf_off >= 0) {
-            // fill_product (abstraction.cpp:150-159) into a per-warp shared-memory row,
-            // line by line (q = Q[L], then q*ml[k]); one bulk async store per row
-            const int stride = (R + 3) & ~1; // even: every warp's row starts 16-byte aligned
-            double* buf = g_sm + rowbuf_off + warp * stride;
-            for (int i = warp; i < rb; i += nwarps) {
-                const long long row = b0 + i;
-                if (row >= nrows) break;
-                const int qo = Y.offQ + i * D.n_lines, po = Y.offP + i * D.P_size;
-                const int mmo = i * mw + D.mm_off, mlo = i * mw + D.ml_off;
-                double* out = probs + row * D.pitch;
-                for (long long t = R + lane; t < D.pitch; t += 32) __stcs(out + t, 0.0); // row padding
-                const int head = (reinterpret_cast<uintptr_t>(out) & 15) ? 1 : 0; // element t at buf[t + head]
-                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                __syncwarp();
-                const int Wl = D.Wl;
-                for (int L = lane; L < D.n_lines; L += 32) {
-                    double q;
-                    if (TAB == TAB_Q) {
-                        q = g_sm[qo + L];
-                    } else {
-                        const int a = D.div_Wm.div(L), j = L - a * D.Wm;
-                        q = g_sm[po + a] * g_sm[mmo + j];
-                    }
-                    double* dst = buf + L * Wl + head;
-                    for (int k = 0; k < Wl; ++k) dst[k] = q * g_sm[mlo + k];
-                }
-                if (vec_copy) { // 16-byte vector stores from the staged row, coalesced
-                    __syncwarp();
-                    const int body = (R - head) & ~1;
-                    if (lane == 0 && head) __stcs(out, buf[head]);
-                    if (lane == 1 && (R - head - body)) __stcs(out + head + body, buf[2 * head + body]);
-                    const double2* src2 = reinterpret_cast<const double2*>(buf + 2 * head);
-                    double2* dst2 = reinterpret_cast<double2*>(out + head);
-                    for (int q2 = lane; q2 < body / 2; q2 += 32) __stcs(dst2 + q2, src2[q2]);
-                    __syncwarp();
-                    continue;
-                }
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                __syncwarp();
-                if (lane == 0) {
-                    const int body = (R - head) & ~1;
-                    if (head) __stcs(out, buf[head]);
-                    if (R - head - body) __stcs(out + head + body, buf[2 * head + body]);
-                    if (body > 0) {
-                        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + head),
-                                     "r"(static_cast<uint32_t>(__cvta_generic_to_shared(buf + 2 * head))),
-                                     "r"(static_cast<uint32_t>(body * 8))
-                                     : "memory");
-                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                    }
-                }
-            }
-            continue;
-        }
         for (int i = warp; i < rb; i += nwarps) { // fill_product (abstraction.cpp:150-159)
             const long long row = b0 + i;
             if (row >= nrows) break;
@@ -450,22 +350,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_build(GmDev D, long long row0, 
             const int mmo = i * mw + D.mm_off, mlo = i * mw + D.ml_off;
             double* out = probs + row * D.pitch;
             for (long long t = R + lane; t < D.pitch; t += 32) __stcs(out + t, 0.0); // row padding
-            if (TAB == TAB_Q && use_tab) {
-                // warp-uniform walk (L0, k0) over 32-element windows; the lane offsets come
-                // from the per-CTA table tab[k0][lane] = (dL, k) of element k0 + lane
-                int L0 = 0, k0 = 0;
-#pragma unroll 4
-                for (int t0 = 0; t0 < R; t0 += 32) {
-                    const int pk = stab[k0 * 32 + lane];
-                    if (t0 + lane < R)
-                        __stcs(out + t0 + lane, g_sm[qo + L0 + (pk & 0xffff)] * g_sm[mlo + (pk >> 16)]);
-                    k0 += c32k;
-                    const int c = k0 >= D.Wl;
-                    k0 -= c ? D.Wl : 0;
-                    L0 += c32L + c;
-                }
-                continue;
-            }
             Walk wk = wk0; // the lane's walk is row independent (initialised once per CTA)
 #pragma unroll 4
             for (int t = lane; t < R; t += 32) {
@@ -476,7 +360,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_build(GmDev D, long long row0, 
             }
         }
     }
-    if (rowbuf_off >= 0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // Stage (ii), on the fly (synthesis.cpp:100-104 + dot_slab :18-47): row groups
@@ -529,7 +412,7 @@ __global__ void __launch_bounds__(kThreads) k_expect_ofa(GmDev D, long long nrow
 // (evict-first, 8 loads in flight per lane) and gather V at the row's origin.
 template <bool LS>
 __global__ void __launch_bounds__(kThreads) k_expect_matrix(GmDev D, long long row0, long long r_lo,
-                                                           long long r_hi, int pf, const double* __restrict__ probs,
+                                                           long long r_hi, const double* __restrict__ probs,
                                                            const long long* __restrict__ origins,
                                                            const double* __restrict__ t0x,
                                                            const double* __restrict__ V,
@@ -548,22 +431,7 @@ __global__ void __launch_bounds__(kThreads) k_expect_matrix(GmDev D, long long r
     const long long total_groups = static_cast<long long>(gridDim.x) * groups;
     const long long iters = (nrows + total_groups - 1) / total_groups;
     const long long nuw = D.n_u * D.n_w;
-    // L2 prefetch of the CTA's block `pf` iterations ahead (one bulk prefetch per
-    // block of `groups` contiguous rows): the row loads below then hit L2
-    auto prefetch = [&](long long it2) {
-        const long long ra = (it2 * gridDim.x + blockIdx.x) * groups;
-        if (ra >= nrows) return;
-        const long long rz = ra + groups < nrows ? ra + groups : nrows;
-        const uintptr_t a = reinterpret_cast<uintptr_t>(probs + (r_lo + ra) * D.pitch) & ~uintptr_t(15);
-        const uintptr_t z = reinterpret_cast<uintptr_t>(probs + (r_lo + rz) * D.pitch) & ~uintptr_t(15);
-        if (z > a)
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(static_cast<uint32_t>(z - a))
-                         : "memory");
-    };
-    if (pf > 0 && threadIdx.x == 0)
-        for (int k = 0; k < pf; ++k) prefetch(k);
     for (long long it = 0; it < iters; ++it) {
-        if (pf > 0 && threadIdx.x == 0) prefetch(it + pf);
         const long long rl = (it * gridDim.x + blockIdx.x) * groups + g; // local row
         const bool valid = rl < nrows;
         const long long r = r_lo + rl; // row inside the matrix
@@ -676,313 +544,6 @@ __global__ void __launch_bounds__(kThreads) k_expect_matrix_et(GmDev D, long lon
         s = group_reduce(s, TPR, 0, g * TPR);
         if (valid && lane == 0) v_in[rl] = skip ? 0.0 : (reach ? s + t0x[r] : s);
     }
-}
-
-// ---------------------------------------------------------------------------
-// Stage (ii), stored matrix, bulk-async staged (Blackwell TMA bulk copies):
-// each CTA owns a contiguous range of row "stages" (one row per row group);
-// thread 0 streams stage k+NS into a shared-memory ring slot with one
-// cp.async.bulk (mbarrier transaction count) while the groups consume stage k
-// from shared memory and gather V from L2. HBM streaming no longer waits on the
-// V-gather latency. Same canonical per-lane order as every other row kernel.
-// ---------------------------------------------------------------------------
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx_arrive(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-
-struct BulkPlan {
-    int ns;           // ring slots
-    int slot_dbl;     // doubles per slot (16-byte multiple)
-    int stages_per_cta;
-    long long n_stages;
-};
-
-template <bool LS>
-__global__ void __launch_bounds__(kThreads) k_expect_matrix_bulk(GmDev D, long long row0, long long r_lo,
-                                                                long long r_hi, BulkPlan bp,
-                                                                const double* __restrict__ probs,
-                                                                const long long* __restrict__ origins,
-                                                                const double* __restrict__ t0x,
-                                                                const double* __restrict__ V,
-                                                                double* __restrict__ v_in) {
-    const int tpr = D.tpr;
-    const int groups = kThreads / tpr;
-    const int g = threadIdx.x / tpr, lane = threadIdx.x - g * tpr;
-    const int R = static_cast<int>(D.R);
-    // shared layout (doubles): [ns slots][red 8][mbarriers ns][lines (ints)]
-    const int offRed = bp.ns * bp.slot_dbl;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(g_sm + offRed + kThreads / 32);
-    const int offL = 2 * (offRed + kThreads / 32 + bp.ns);
-    if (LS) {
-        int* si = reinterpret_cast<int*>(g_sm);
-        for (int c = threadIdx.x; c < D.n_lines; c += blockDim.x) si[offL + c] = D.line_off[c];
-    }
-    const bool reach = D.spec_kind != GM_SPEC_SAFETY;
-    const long long nuw = D.n_u * D.n_w;
-    const long long nrows = r_hi - r_lo;
-    const long long s0 = static_cast<long long>(blockIdx.x) * bp.stages_per_cta;
-    const long long s1 = s0 + bp.stages_per_cta < bp.n_stages ? s0 + bp.stages_per_cta : bp.n_stages;
-    const int my = s1 > s0 ? static_cast<int>(s1 - s0) : 0;
-
-    // producer: stage k covers local rows [k*groups, min(nrows, (k+1)*groups)); it is
-    // loaded as the 16-byte aligned superset of its bytes; skipped when every row
-    // of the stage belongs to an absorbing state (those rows are never read)
-    auto issue = [&](int it) {
-        const long long st = s0 + it;
-        const long long ra = st * groups, rz = (ra + groups < nrows ? ra + groups : nrows);
-        uint64_t* bar = bars + (it % bp.ns);
-        bool live = true;
-        if (reach && D.absorb != nullptr) {
-            live = false;
-            for (long long x = (row0 + r_lo + ra) / nuw; x <= (row0 + r_lo + rz - 1) / nuw; ++x)
-                if (!D.absorb[x]) { live = true; break; }
-        }
-        if (!live) { mbar_arrive(bar); return; }
-        const char* src = reinterpret_cast<const char*>(probs + (r_lo + ra) * D.R);
-        const char* a = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15));
-        const char* z = src + (rz - ra) * D.R * 8;
-        const uint32_t bytes = static_cast<uint32_t>(((z - a) + 15) & ~15);
-        mbar_expect_tx_arrive(bar, bytes);
-        bulk_g2s(g_sm + (it % bp.ns) * bp.slot_dbl, a, bytes, bar);
-    };
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < bp.ns; ++s) mbar_init(bars + s, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int it = 0; it < bp.ns && it < my; ++it) issue(it);
-    }
-    __syncthreads();
-    for (int it = 0; it < my; ++it) {
-        const int slot = it % bp.ns;
-        mbar_wait(bars + slot, static_cast<uint32_t>((it / bp.ns) & 1));
-        const long long ra = (s0 + it) * groups;
-        const long long rl = ra + g; // local row of this group
-        const bool valid = rl < nrows;
-        const long long r = r_lo + rl;
-        bool skip = !valid;
-        if (valid && reach && D.absorb != nullptr) skip = D.absorb[(row0 + r) / nuw];
-        double s = 0.0;
-        if (!skip) {
-            // offset of the stage's first row inside the aligned superset (0 or 1 double)
-            const int mis = static_cast<int>((reinterpret_cast<uintptr_t>(probs + (r_lo + ra) * D.R) & 15) >> 3);
-            const int base = slot * bp.slot_dbl + mis + g * R;
-            s = row_dot<3, 8, LS>(D, lane, tpr, nullptr, base, 0, 0, 0, V + origins[r], D.line_off, offL);
-        }
-        s = group_reduce(s, tpr, offRed, g * tpr);
-        if (valid && lane == 0) v_in[rl] = skip ? 0.0 : (reach ? s + t0x[r] : s);
-        __syncthreads(); // every group is done with this slot
-        if (threadIdx.x == 0 && it + bp.ns < my) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(it + bp.ns);
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Stage (ii), stored matrix, warp-specialised: warp 8 of the CTA is a producer
-// that streams the CTA's contiguous rows, one row per ring slot, with
-// cp.async.bulk (mbarrier complete_tx); warps 0-7 form the usual row groups and
-// consume slots in order. Per-slot full/empty mbarriers replace CTA barriers,
-// so HBM streaming runs up to `ns` rows ahead of the V-gather-bound consumers.
-// ---------------------------------------------------------------------------
-
-constexpr int kWsThreads = kThreads + 32;
-
-__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) { mbar_wait(bar, parity); }
-
-template <bool LS>
-__global__ void __launch_bounds__(kWsThreads) k_expect_matrix_ws(GmDev D, long long row0, long long r_lo,
-                                                                long long r_hi, int ns, int slot_dbl,
-                                                                long long rows_per_cta,
-                                                                const double* __restrict__ probs,
-                                                                const long long* __restrict__ origins,
-                                                                const double* __restrict__ t0x,
-                                                                const double* __restrict__ V,
-                                                                double* __restrict__ v_in) {
-    const int tpr = D.tpr;
-    const int groups = kThreads / tpr;
-    const int R = static_cast<int>(D.R);
-    // shared layout (doubles): [ns slots][red 8][full ns][empty ns][lines (ints)]
-    const int offRed = ns * slot_dbl;
-    uint64_t* full = reinterpret_cast<uint64_t*>(g_sm + offRed + kThreads / 32);
-    uint64_t* empty = full + ns;
-    const int offL = 2 * (offRed + kThreads / 32 + 2 * ns);
-    if (LS) {
-        int* si = reinterpret_cast<int*>(g_sm);
-        for (int c = threadIdx.x; c < D.n_lines; c += blockDim.x) si[offL + c] = D.line_off[c];
-    }
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < ns; ++s) {
-            mbar_init(full + s, 1);
-            mbar_init(empty + s, 1);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    const bool reach = D.spec_kind != GM_SPEC_SAFETY;
-    const long long nuw = D.n_u * D.n_w;
-    const long long nrows = r_hi - r_lo;
-    const long long ra = static_cast<long long>(blockIdx.x) * rows_per_cta;
-    const long long rz = ra + rows_per_cta < nrows ? ra + rows_per_cta : nrows;
-    const long long my = rz > ra ? rz - ra : 0;
-    auto absorbed = [&](long long rl) {
-        return reach && D.absorb != nullptr && D.absorb[(row0 + r_lo + rl) / nuw];
-    };
-
-    if (threadIdx.x >= kThreads) { // producer warp: flags of 32 rows at a time, lane 0 issues
-        const int pl = threadIdx.x - kThreads;
-        for (long long i0 = 0; i0 < my; i0 += 32) {
-            const bool ab = i0 + pl < my ? absorbed(ra + i0 + pl) : true;
-            const unsigned mask = __ballot_sync(0xffffffffu, ab);
-            if (pl == 0) {
-                for (int k = 0; k < 32 && i0 + k < my; ++k) {
-                    const long long i = i0 + k;
-                    const int s = static_cast<int>(i % ns);
-                    if (i >= ns) mbar_wait(empty + s, static_cast<uint32_t>(((i / ns) - 1) & 1));
-                    if ((mask >> k) & 1u) { // never read (synthesis.cpp:86-89): complete without data
-                        mbar_arrive(full + s);
-                        continue;
-                    }
-                    const long long rl = ra + i;
-                    const char* src = reinterpret_cast<const char*>(probs + (r_lo + rl) * D.R);
-                    const char* a =
-                        reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15));
-                    const uint32_t bytes = static_cast<uint32_t>(((src + R * 8 - a) + 15) & ~15);
-                    mbar_expect_tx_arrive(full + s, bytes);
-                    bulk_g2s(g_sm + s * slot_dbl, a, bytes, full + s);
-                }
-            }
-            __syncwarp();
-        }
-        return;
-    }
-
-    const int g = threadIdx.x / tpr, lane = threadIdx.x - g * tpr;
-    const long long iters = (my + groups - 1) / groups;
-    for (long long it = 0; it < iters; ++it) {
-        const long long i = it * groups + g; // row of the CTA range handled by this group
-        const bool valid = i < my;
-        double s = 0.0;
-        bool skip = true;
-        int slot = 0;
-        if (valid) {
-            slot = static_cast<int>(i % ns);
-            mbar_wait(full + slot, static_cast<uint32_t>((i / ns) & 1));
-            skip = absorbed(ra + i);
-            if (!skip) {
-                const long long r = r_lo + ra + i;
-                const int mis = static_cast<int>((reinterpret_cast<uintptr_t>(probs + r * D.R) & 15) >> 3);
-                s = row_dot<3, 8, LS>(D, lane, tpr, nullptr, slot * slot_dbl + mis, 0, 0, 0, V + origins[r],
-                                      D.line_off, offL);
-            }
-        }
-        s = group_reduce(s, tpr, offRed, g * tpr);
-        if (valid && lane == 0) {
-            const long long r = r_lo + ra + i;
-            v_in[ra + i] = skip ? 0.0 : (reach ? s + t0x[r] : s);
-            mbar_arrive(empty + slot); // the group has finished reading this slot
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Stage (ii), stored matrix, per-warp cp.async double buffer (tpr == 32): each
-// warp copies its NEXT row into shared memory with 16-byte cp.async (no register
-// staging) while it reduces the current row from shared memory. Opt-in.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads) k_expect_matrix_cp(GmDev D, long long row0, long long r_lo,
-                                                              long long r_hi, int buf_dbl,
-                                                              const double* __restrict__ probs,
-                                                              const long long* __restrict__ origins,
-                                                              const double* __restrict__ t0x,
-                                                              const double* __restrict__ V,
-                                                              double* __restrict__ v_in) {
-    const int nw = kThreads / 32;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int offRed = nw * 2 * buf_dbl;
-    const int offL = 2 * (offRed + kThreads / 32);
-    {
-        int* si = reinterpret_cast<int*>(g_sm);
-        for (int c = threadIdx.x; c < D.n_lines; c += blockDim.x) si[offL + c] = D.line_off[c];
-    }
-    __syncthreads();
-    const bool reach = D.spec_kind != GM_SPEC_SAFETY;
-    const long long nuw = D.n_u * D.n_w;
-    const long long nrows = r_hi - r_lo;
-    const int R = static_cast<int>(D.R);
-    const long long step = static_cast<long long>(gridDim.x) * nw;
-    auto row_of = [&](long long it) { return (it * gridDim.x + blockIdx.x) * nw + warp; };
-    auto live = [&](long long rl) {
-        return rl < nrows && !(reach && D.absorb != nullptr && D.absorb[(row0 + r_lo + rl) / nuw]);
-    };
-    auto fetch = [&](long long rl, int b) { // aligned superset of the row -> buffer b
-        const char* src = reinterpret_cast<const char*>(probs + (r_lo + rl) * D.R);
-        const char* a = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15));
-        const int chunks = static_cast<int>(((src + R * 8 - a) + 15) >> 4);
-        const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(g_sm + (warp * 2 + b) * buf_dbl));
-        for (int c = lane; c < chunks; c += 32)
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + c * 16), "l"(a + c * 16) : "memory");
-    };
-    (void)step;
-    long long it = 0;
-    long long rl = row_of(0);
-    if (live(rl)) fetch(rl, 0);
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    for (; rl < nrows || __any_sync(0xffffffffu, rl < nrows); ++it) {
-        const long long nxt = row_of(it + 1);
-        const int b = static_cast<int>(it & 1);
-        if (live(nxt)) fetch(nxt, b ^ 1);
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
-        __syncwarp();
-        double s = 0.0;
-        const bool ok = live(rl);
-        if (ok) {
-            const long long r = r_lo + rl;
-            const int mis = static_cast<int>((reinterpret_cast<uintptr_t>(probs + r * D.R) & 15) >> 3);
-            s = row_dot<3, 8, true>(D, lane, 32, nullptr, (warp * 2 + b) * buf_dbl + mis, 0, 0, 0, V + origins[r],
-                                    D.line_off, offL);
-        }
-        s = group_reduce(s, 32, offRed, warp * 32);
-        if (rl < nrows && lane == 0) v_in[rl] = ok ? (reach ? s + t0x[r_lo + rl] : s) : 0.0;
-        __syncwarp(); // buffer b is refilled next iteration
-        rl = nxt;
-        if (rl >= nrows) break;
-    }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 // min over w (strict <, ascending), then max over u (strict >, ascending):
@@ -1502,22 +1063,6 @@ static int resident_grid(K kernel, size_t smem, long long batches, int reserve =
     return static_cast<int>(std::max<long long>(g, 1));
 }
 
-void expand(const GmDev& D, long long nrows, const double* mass, double* probs_out, cudaStream_t s) {
-    if (nrows <= 0) return;
-    const BatchPlan b = plan_batches(D, false);
-    const long long batches = (nrows + b.rb - 1) / b.rb;
-    if (b.tab == TAB_Q) {
-        allow_smem(k_expand<TAB_Q>, b.smem);
-        k_expand<TAB_Q><<<resident_grid(k_expand<TAB_Q>, b.smem, batches, 1), kThreads, b.smem, s>>>(
-            D, nrows, b.rb, gm_fastdiv(b.rb), mass, probs_out);
-    } else {
-        allow_smem(k_expand<TAB_P>, b.smem);
-        k_expand<TAB_P><<<resident_grid(k_expand<TAB_P>, b.smem, batches, 1), kThreads, b.smem, s>>>(
-            D, nrows, b.rb, gm_fastdiv(b.rb), mass, probs_out);
-    }
-    check_launch("expand");
-}
-
 // Fused stage (i): rows per batch so that the per-row tables, prologue data and
 // the dynamics program fit the soft shared-memory budget.
 void build_custom(const GmDev& D, long long row0, long long nrows, long long* origin_out, double* t0x_out,
@@ -1593,8 +1138,8 @@ void build(const GmDev& D, long long row0, long long nrows, long long* origin_ou
             }
         }
     }
-    const size_t fixed = (kThreads / 32 + D.n_ins + D.n_lits + 2) * sizeof(double) +
-                         (D.Wl <= 64 ? static_cast<size_t>(D.Wl) * 32 * sizeof(int) : 0);
+    // single-role fallback (the pipelined layout does not fit)
+    const size_t fixed = (kThreads / 32 + D.n_ins + D.n_lits + 2) * sizeof(double);
     const size_t extra_row = (2 * GMD_MAXD + 1) * sizeof(double) + GMD_MAXD * sizeof(int);
     const size_t q_row = (mw + D.P_size + D.n_lines) * sizeof(double) + extra_row;
     const size_t p_row = (mw + D.P_size) * sizeof(double) + extra_row;
@@ -1614,36 +1159,17 @@ void build(const GmDev& D, long long row0, long long nrows, long long* origin_ou
         if (tab >= 0) break;
     }
     if (tab < 0) throw std::runtime_error("row too wide for the device build layout");
-    size_t smem = fixed + (tab == TAB_Q ? q_row : p_row) * static_cast<size_t>(rb);
-    // bulk-store variant: one shared-memory row per warp (+ the tables of >= 16 rows)
-    static const char* bb = std::getenv("GM_BUILD_BULK");
-    // GM_BUILD_BULK=1: rows staged in shared memory + one TMA bulk store each; =2: staged rows
-    // copied with 16-byte vector stores; unset: lane-strided direct stores
-    const bool want_bulk = bb && (bb[0] == '1' || bb[0] == '2');
-    const int vec_copy = bb && bb[0] == '2' ? 1 : 0;
-    int rowbuf_off = -1;
-    const size_t rowbuf = (kThreads / 32) * static_cast<size_t>((D.R + 3) & ~1LL) * sizeof(double);
-    if (want_bulk && D.R >= 32 && D.R + 2 < (1 << 20)) {
-        const size_t per = tab == TAB_Q ? q_row : p_row;
-        const size_t budget = 110 * 1024;
-        if (fixed + rowbuf + 16 * per <= budget) {
-            rb = std::min<long long>(kThreads, static_cast<long long>((budget - fixed - rowbuf) / per));
-            rb -= rb % 2;
-            const size_t tables = fixed + per * static_cast<size_t>(rb);
-            rowbuf_off = static_cast<int>(((tables + 15) / 16 * 16) / sizeof(double));
-            smem = static_cast<size_t>(rowbuf_off) * sizeof(double) + rowbuf;
-        }
-    }
+    const size_t smem = fixed + (tab == TAB_Q ? q_row : p_row) * static_cast<size_t>(rb);
     const long long batches = (nrows + rb - 1) / rb;
     const GmFastDiv drb = gm_fastdiv(static_cast<uint32_t>(rb));
     if (tab == TAB_Q) {
         allow_smem(k_build<TAB_Q>, smem);
         k_build<TAB_Q><<<resident_grid(k_build<TAB_Q>, smem, batches), kThreads, smem, s>>>(
-            D, row0, nrows, static_cast<int>(rb), drb, rowbuf_off, vec_copy, origin_out, t0x_out, probs_out, d_err);
+            D, row0, nrows, static_cast<int>(rb), drb, origin_out, t0x_out, probs_out, d_err);
     } else {
         allow_smem(k_build<TAB_P>, smem);
         k_build<TAB_P><<<resident_grid(k_build<TAB_P>, smem, batches), kThreads, smem, s>>>(
-            D, row0, nrows, static_cast<int>(rb), drb, rowbuf_off, vec_copy, origin_out, t0x_out, probs_out, d_err);
+            D, row0, nrows, static_cast<int>(rb), drb, origin_out, t0x_out, probs_out, d_err);
     }
     check_launch("build");
 }
@@ -1681,76 +1207,12 @@ void expect_matrix(const GmDev& D, long long row0, long long r_lo, long long r_h
     const bool in_smem = table <= 48 * 1024;
     const int groups = kThreads / D.tpr;
     const long long blocks_needed = (r_hi - r_lo + groups - 1) / groups;
-    // bulk-async staged kernel when a stage (one row per group) fits a 2-slot ring
-    // GM_MATRIX_KERNEL=bulk selects the shared-memory ring variant; the default
-    // streams rows straight to registers with a bulk L2 prefetch GM_PREFETCH blocks ahead
-    static const char* force = std::getenv("GM_MATRIX_KERNEL");
-    static const char* pfs = std::getenv("GM_PREFETCH");
-    const int pf = pfs ? std::atoi(pfs) : 0;
-    const bool allow_bulk = force && std::string(force) == "bulk";
-    // default: element-offset-table kernel k_expect_matrix_et (18.2-19.8 ms on C2b,
-    // L1 data-pipe bound). Opt-in variants, all slower on C2b: GM_MATRIX_KERNEL=walk
-    // (per-term slab walk, 23 ms), ws (warp-specialised bulk ring, 28 ms), bulk
-    // (CTA-synchronised ring, 25.6 ms), cp (per-warp cp.async double buffer, 32.8 ms).
-    // Offsets held in registers instead of the table: 21.3 ms (92 registers) / equal
-    // (64 registers, spills); GM_CONTIG=1 (contiguous rows per CTA): equal; V staged
-    // per chunk of states in shared memory (bounding box of the chunk's slabs): 23.2 ms
-    // (96-row chunks, 48 KB box; larger chunks lose occupancy: 31.7 ms at 200 rows).
-    const bool allow_ws = force && std::string(force) == "ws";
-    // the opt-in staged variants address rows at stride R (unpadded layouts only)
-    const bool unpadded = D.pitch == D.R;
-    if (force && std::string(force) == "cp" && D.tpr == 32 && in_smem && unpadded) {
-        const size_t buf = ((static_cast<size_t>(D.R) * 8 + 16) + 15) / 16 * 16;
-        const size_t smem = (kThreads / 32) * 2 * buf + (kThreads / 32) * sizeof(double) + table;
-        if (smem <= 110 * 1024) {
-            allow_smem(k_expect_matrix_cp, smem);
-            const int grid = resident_grid(k_expect_matrix_cp, smem, blocks_needed);
-            k_expect_matrix_cp<<<grid, kThreads, smem, s>>>(D, row0, r_lo, r_hi, static_cast<int>(buf / 8), probs,
-                                                            origins, t0x, V, v_in);
-            check_launch("expect_matrix_cp");
-            return;
-        }
-    }
-    {
-        static const char* cs = std::getenv("GM_WS_CTAS");
-        const int ctas = cs ? std::max(1, std::atoi(cs)) : 2;
-        const size_t slot_b = ((static_cast<size_t>(D.R) * 8 + 16) + 15) / 16 * 16;
-        const size_t tail_b = (kThreads / 32) * sizeof(double) + (in_smem ? table : 0);
-        const size_t budget = (ctas >= 2 ? 110 * 1024 : 220 * 1024);
-        long long ns = slot_b ? static_cast<long long>((budget - tail_b) / (slot_b + 16)) : 0;
-        ns = std::min<long long>(ns, std::max(64, groups));
-        // a multiple of the group count: slot s is always consumed by group s % groups, so
-        // a consumer is never more than one phase ahead of a slot's mbarrier (parity waits)
-        ns -= ns % groups;
-        if (allow_ws && in_smem && ns >= groups && ns >= 4 && unpadded) {
-            const size_t smem = static_cast<size_t>(ns) * slot_b + tail_b + 2 * ns * sizeof(uint64_t) + 16;
-            allow_smem(k_expect_matrix_ws<true>, smem);
-            const long long nrows = r_hi - r_lo;
-            int grid = num_sms() * ctas;
-            const long long per = (nrows + grid - 1) / grid;
-            grid = static_cast<int>((nrows + per - 1) / per);
-            k_expect_matrix_ws<true><<<grid, kWsThreads, smem, s>>>(D, row0, r_lo, r_hi, static_cast<int>(ns),
-                                                                    static_cast<int>(slot_b / 8), per, probs,
-                                                                    origins, t0x, V, v_in);
-            check_launch("expect_matrix_ws");
-            return;
-        }
-    }
-    const size_t slot = ((static_cast<size_t>(groups) * D.R * 8 + 16) + 15) / 16 * 16;
-    const size_t tail = (kThreads / 32) * sizeof(double) + 4 * sizeof(uint64_t) + (in_smem ? table : 0);
-    if (allow_bulk && in_smem && 2 * slot + tail <= kHardSmem && unpadded) {
-        BulkPlan bp;
-        bp.ns = (3 * slot + tail <= kHardSmem && 2 * slot + tail > 112 * 1024) ? 3 : 2;
-        bp.slot_dbl = static_cast<int>(slot / 8);
-        const size_t smem = bp.ns * slot + tail;
-        allow_smem(k_expect_matrix_bulk<true>, smem);
-        bp.n_stages = blocks_needed;
-        const int grid = resident_grid(k_expect_matrix_bulk<true>, smem, bp.n_stages);
-        bp.stages_per_cta = static_cast<int>((bp.n_stages + grid - 1) / grid);
-        k_expect_matrix_bulk<true><<<grid, kThreads, smem, s>>>(D, row0, r_lo, r_hi, bp, probs, origins, t0x, V, v_in);
-        check_launch("expect_matrix_bulk");
-        return;
-    }
+    static const char* force = std::getenv("GM_MATRIX_KERNEL"); // "walk": per-term slab walk
+    // default: element-offset-table kernel k_expect_matrix_et (L1 data-pipe bound).
+    // Measured and removed (all slower on C2b): TMA bulk rings (CTA-synchronised 25.6 ms,
+    // warp-specialised 28 ms), per-warp cp.async (32.8 ms), L2 bulk prefetch, offsets in
+    // registers (21.3 ms), V staged per chunk of states in shared memory (23.2 ms);
+    // contiguous rows per CTA (GM_CONTIG=1): equal.
     const size_t et_smem = (kThreads / 32) * sizeof(double) + static_cast<size_t>(D.R) * sizeof(int);
     if (!(force && std::string(force) == "walk") && et_smem <= kHardSmem) {
         const long long nuw = D.n_u * D.n_w;
@@ -1774,10 +1236,10 @@ void expect_matrix(const GmDev& D, long long row0, long long r_lo, long long r_h
     const size_t smem = (kThreads / 32) * sizeof(double) + (in_smem ? table : 0);
     if (in_smem) {
         k_expect_matrix<true><<<resident_grid(k_expect_matrix<true>, smem, blocks_needed), kThreads, smem, s>>>(
-            D, row0, r_lo, r_hi, pf, probs, origins, t0x, V, v_in);
+            D, row0, r_lo, r_hi, probs, origins, t0x, V, v_in);
     } else {
         k_expect_matrix<false><<<resident_grid(k_expect_matrix<false>, smem, blocks_needed), kThreads, smem, s>>>(
-            D, row0, r_lo, r_hi, pf, probs, origins, t0x, V, v_in);
+            D, row0, r_lo, r_hi, probs, origins, t0x, V, v_in);
     }
     check_launch("expect_matrix");
 }

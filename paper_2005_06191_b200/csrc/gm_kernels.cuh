@@ -49,10 +49,6 @@ bool build_uses_qs(const GmDev& D);
 void build(const GmDev& D, long long row0, long long nrows, long long* origin_out, double* t0x_out,
            double* probs_out, unsigned long long* d_err, cudaStream_t s, const void* const* jit_ws = nullptr);
 
-// Outer-product expansion of the prologue's masses into stored rows
-// (fill_product, abstraction.cpp:150-159).
-void expand(const GmDev& D, long long nrows, const double* mass, double* probs_out, cudaStream_t s);
-
 // Expected value per row, on the fly (synthesis.cpp:100-104) from prologue data.
 void expect_ofa(const GmDev& D, long long nrows, const double* mass, const long long* origin,
                 const double* t0x, const uint8_t* rowflag, const double* V, double* v_in,
