@@ -11,8 +11,8 @@ runs the 32 backward Bellman steps (all-gather of V between ranks).
              device time with CUDA events on the engine's stream, max over ranks)
   sweep_s    Bellman sweep seconds per synthesis (device time, max over ranks)
   e2e        the same metric through the public C ABI from host data: config text
-             parsed on the host, model uploaded, shard built (gm_build_shard),
-             origins + target-hit vector read back into pinned host memory
+             parsed on the host, model uploaded, shard built (gm_build_shard_host),
+             origins + target-hit vector streamed into pinned host memory
              (wall clock, max over ranks); e2e_synthesize = one full
              gridmdp.synthesize (value/policy tables on the host)
   cpu_baseline        the reference's row kernel on a bounded sample (probs/s)
@@ -330,8 +330,8 @@ def main():
     # e2e: the same metric (MDP probs/s of stage (i)) through the public C ABI from
     # host data: each step parses the configuration text on the host, uploads the
     # model (bytecode, line table, absorbing flags), builds this rank's shard with
-    # gm_build_shard and reads the shard's origins + target-hit vector back into
-    # pinned host memory; wall clock, max over ranks.
+    # gm_build_shard_host, which streams the shard's origins + target-hit vector into
+    # pinned host memory slice by slice; wall clock, max over ranks.
     if not args.no_e2e:
         import ctypes as C
 
@@ -342,12 +342,10 @@ def main():
         def e2e_step():
             m3 = g.parse_config(cfg_text, args.workload)
             h = C.c_void_p()
-            _capi.call("gm_build_shard", m3.handle, C.c_int64(plan.x0), C.c_int64(plan.x1), C.byref(h))
-            _capi.call("gm_matrix_copy_rows", h, C.c_int64(plan.x0 * nuw), C.c_int64(plan.x1 * nuw),
-                       C.c_void_p(h_org.data_ptr()), None)
-            if reach:
-                _capi.call("gm_matrix_copy_t0x", h, C.c_int64(plan.x0 * nuw), C.c_int64(plan.x1 * nuw),
-                           C.c_void_p(h_t0x.data_ptr()))
+            # build in slices; each slice's origins / T0x reach the pinned host buffers
+            # while the next slice builds
+            _capi.call("gm_build_shard_host", m3.handle, C.c_int64(plan.x0), C.c_int64(plan.x1), C.byref(h),
+                       C.c_void_p(h_org.data_ptr()), C.c_void_p(h_t0x.data_ptr()) if reach else None)
             _capi.lib.gm_matrix_free(h)
             return m3
 
@@ -372,7 +370,7 @@ def main():
         line["e2e"] = {"value": probs_per_step / statistics.median(e2e), "unit": "probs/s",
                        "seconds_per_step": statistics.median(e2e), "h2d_bytes_per_step": h2d,
                        "d2h_bytes_per_step": d2h,
-                       "note": "config text -> gm_build_shard -> origins/T0x to pinned host, wall clock"}
+                       "note": "config text -> gm_build_shard_host (origins/T0x to pinned host, overlapped) , wall clock"}
         # the full user-facing synthesis (rank 0, one GPU): host text -> value/policy tables on host
         if world == 1:
             t = time.perf_counter()

@@ -206,6 +206,12 @@ gm_code gm_step_device(gm_model* m, gm_matrix* tm, int64_t x_begin, int64_t x_en
  * reusing its device buffers. */
 gm_code gm_build_shard(gm_model* m, int64_t x_begin, int64_t x_end, gm_matrix** out,
                        gm_status* st);
+/* gm_build_shard that also delivers the shard's origins (and, for reach specs, the
+ * target-hit vector) into host memory: the rows are built in slices and each
+ * slice's metadata is copied to the host while the next slice builds (pass
+ * pinned buffers for the copies to overlap). Either output may be NULL. */
+gm_code gm_build_shard_host(gm_model* m, int64_t state_begin, int64_t state_end, gm_matrix** out,
+                            int64_t* origins_out, double* t0x_out, gm_status* st);
 /* Per-row expected values of the model's most recent step (the v_in workspace of
  * bellman_impl, synthesis.cpp:69-109), rows of the stepped states; n doubles. */
 gm_code gm_copy_row_values(gm_model* m, double* out, int64_t n, gm_status* st);

@@ -884,6 +884,71 @@ gm_code gm_build_shard(gm_model* m, int64_t x0, int64_t x1, gm_matrix** out, gm_
     });
 }
 
+gm_code gm_build_shard_host(gm_model* m, int64_t x0, int64_t x1, gm_matrix** out, int64_t* origins_host,
+                            double* t0x_host, gm_status* st) {
+    return guarded(st, [&] {
+        if (x0 < 0 || x1 > m->M.n_x() || x0 > x1) throw std::out_of_range("build_shard: state range outside the grid");
+        check_spec(m->M.spec, m->M.X);
+        prepare(m);
+        const int64_t nuw = m->M.n_u() * m->M.n_w();
+        const int64_t r0 = x0 * nuw, n = (x1 - x0) * nuw;
+        const bool reach = m->M.spec.reach();
+        std::unique_ptr<gm_matrix> fresh;
+        gm_matrix* tm = *out;
+        if (!tm) {
+            fresh = std::make_unique<gm_matrix>();
+            tm = fresh.get();
+        }
+        tm->device = m->device;
+        tm->row_begin = r0;
+        tm->row_end = r0 + n;
+        tm->R = m->M.R;
+        tm->pitch = m->D.pitch;
+        tm->masked = false;
+        tm->has_t0x = false;
+        tm->probs.ensure(mul_checked(static_cast<uint64_t>(n), static_cast<uint64_t>(tm->pitch), "matrix size"),
+                         "matrix payload");
+        tm->origins.ensure(static_cast<size_t>(n), "matrix origins");
+        if (reach) {
+            tm->t0x.ensure(static_cast<size_t>(n), "target-hit vector");
+            tm->has_t0x = true;
+        }
+        ensure_scratch(m, 4096); // the aux stream and events of the producer pipeline
+        const gmj::Kernels* J =
+            jit_kernels(m, gmk::build_uses_qs(m->D) ? gmj::WANT_BUILD_QS : gmj::WANT_BUILD_NOQS, n);
+        // the rows in a few slices: slice k's origins / T0x travel to the host on the aux
+        // stream while slice k+1 builds
+        const int64_t slices = n >= (int64_t(1) << 16) ? 4 : 1;
+        const int64_t per = (n + slices - 1) / slices;
+        cudaEvent_t ev[4];
+        for (int64_t k = 0; k < slices; ++k) ck(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming), "event");
+        for (int64_t k = 0; k < slices; ++k) {
+            const int64_t c0 = k * per, cn = std::min(per, n - c0);
+            if (cn <= 0) break;
+            {
+                Launch L(gmk::KF_EXPAND, m->stream);
+                gmk::build(m->D, r0 + c0, cn, tm->origins.p + c0, reach ? tm->t0x.p + c0 : nullptr,
+                           tm->probs.p + c0 * tm->pitch, m->d_err.p, m->stream, J ? J->build_ws : nullptr);
+            }
+            ck(cudaEventRecord(ev[k], m->stream), "slice event");
+            ck(cudaStreamWaitEvent(m->aux, ev[k], 0), "slice wait");
+            if (origins_host)
+                ck(cudaMemcpyAsync(origins_host + c0, tm->origins.p + c0, static_cast<size_t>(cn) * 8,
+                                   cudaMemcpyDeviceToHost, m->aux),
+                   "origins");
+            if (t0x_host && reach)
+                ck(cudaMemcpyAsync(t0x_host + c0, tm->t0x.p + c0, static_cast<size_t>(cn) * 8, cudaMemcpyDeviceToHost,
+                                   m->aux),
+                   "t0x");
+        }
+        ck(cudaStreamSynchronize(m->stream), "build");
+        ck(cudaStreamSynchronize(m->aux), "copies");
+        for (int64_t k = 0; k < slices; ++k) cudaEventDestroy(ev[k]);
+        raise_device_error(m);
+        if (fresh) *out = fresh.release();
+    });
+}
+
 gm_code gm_mask_absorbing(gm_model* m, gm_matrix* tm, gm_status* st) {
     return guarded(st, [&] {
         if (!m->M.spec.reach()) return; // abstraction.cpp:323

@@ -105,3 +105,33 @@ def test_smoke_entry():
     import __graft_entry__
 
     __graft_entry__.smoke()
+
+
+def test_build_shard_host_matches_build_and_copy():
+    """gm_build_shard_host (sliced build, origins / T0x streamed to the host) gives the same
+    rows and metadata as gm_build_shard followed by the copies."""
+    import ctypes as C
+
+    from paper_2005_06191_b200 import _capi
+    from paper_2005_06191_b200 import workloads as W
+    m = g.parse_config(W.WORKLOADS["C2a"](), "C2a")
+    s = m.sizes()
+    nx, nuw, R = int(s.n_states), int(s.n_inputs) * int(s.n_disturbances), int(s.row_width)
+    x0, x1 = 3, nx - 5
+    rows = (x1 - x0) * nuw
+    org = np.empty(rows, np.int64)
+    t0x = np.empty(rows, np.float64)
+    h = C.c_void_p()
+    _capi.call("gm_build_shard_host", m.handle, C.c_int64(x0), C.c_int64(x1), C.byref(h), _capi.ptr(org),
+               _capi.ptr(t0x))
+    p1 = np.empty(rows * R)
+    _capi.call("gm_matrix_copy_rows", h, C.c_int64(x0 * nuw), C.c_int64(x1 * nuw), None, _capi.ptr(p1))
+    _capi.lib.gm_matrix_free(h)
+    h2 = C.c_void_p()
+    _capi.call("gm_build_shard", m.handle, C.c_int64(x0), C.c_int64(x1), C.byref(h2))
+    org2, t0x2, p2 = np.empty(rows, np.int64), np.empty(rows), np.empty(rows * R)
+    _capi.call("gm_matrix_copy_rows", h2, C.c_int64(x0 * nuw), C.c_int64(x1 * nuw), _capi.ptr(org2), _capi.ptr(p2))
+    _capi.call("gm_matrix_copy_t0x", h2, C.c_int64(x0 * nuw), C.c_int64(x1 * nuw), _capi.ptr(t0x2))
+    _capi.lib.gm_matrix_free(h2)
+    assert np.array_equal(org, org2) and np.array_equal(t0x.view(np.uint64), t0x2.view(np.uint64))
+    assert np.array_equal(p1.view(np.uint64), p2.view(np.uint64))
