@@ -482,8 +482,14 @@ void build_rows(gm_model* m, int64_t r0, int64_t r1, gm_matrix* tm, bool want_t0
         jit_kernels(m, gmk::build_uses_qs(m->D) ? gmj::WANT_BUILD_QS : gmj::WANT_BUILD_NOQS, n);
     {
         Launch L(gmk::KF_EXPAND, m->stream);
-        gmk::build(m->D, r0, n, tm->origins.p, want_t0x ? tm->t0x.p : nullptr, tm->probs.p, m->d_err.p, m->stream,
-                   J ? J->build_ws : nullptr);
+        static const char* sl = std::getenv("GM_BUILD_SLICES");
+        const int64_t slices = sl ? std::max(1, std::atoi(sl)) : 1;
+        const int64_t per = (n + slices - 1) / slices;
+        for (int64_t c0 = 0; c0 < n; c0 += per) {
+            const int64_t cn = std::min(per, n - c0);
+            gmk::build(m->D, r0 + c0, cn, tm->origins.p + c0, want_t0x ? tm->t0x.p + c0 : nullptr,
+                       tm->probs.p + c0 * tm->pitch, m->d_err.p, m->stream, J ? J->build_ws : nullptr);
+        }
     }
     ck(cudaStreamSynchronize(m->stream), "build");
     raise_device_error(m);
