@@ -1582,8 +1582,6 @@ gm_code gm_simulate(gm_model* m, const gm_result* res, const double* x0, int32_t
                     int32_t worst_case, int32_t want_traj, gm_sim** out, gm_status* st) {
     return guarded(st, [&] {
         const Model& M = m->M;
-        if (M.noise.family == GM_CUSTOM)
-            throw ConfigErr("simulate: custom densities are not supported by the GPU simulator");
         const SpecV& spec = res->meta.spec; // cmd_simulate passes res.spec (gridmdp_main.cpp:130)
         check_spec(spec, M.X);               // validate_spec, sim.cpp:88
         if (runs < 1) throw ConfigErr("simulate: need at least one run");
@@ -1600,6 +1598,31 @@ gm_code gm_simulate(gm_model* m, const gm_result* res, const double* x0, int32_t
         A.has_avoid = spec.avoid.dim() > 0 ? 1 : 0;
         A.worst_case = worst_case ? 1 : 0;
         A.seed = seed;
+        if (M.noise.family == GM_CUSTOM) { // custom_sup_estimate (noise.cpp:307-333) on the host
+            const int nd = M.X.dim();
+            int per_dim = 17;
+            int64_t total = 1;
+            for (int d = 0; d < nd; ++d) total *= per_dim;
+            if (total > 100000) per_dim = 5;
+            std::vector<double> pt(static_cast<size_t>(nd));
+            std::vector<int64_t> idx(static_cast<size_t>(nd), 0);
+            double sup = 0.0;
+            for (;;) {
+                for (int d = 0; d < nd; ++d) {
+                    const double t = per_dim == 1 ? 0.5 : static_cast<double>(idx[d]) / (per_dim - 1);
+                    pt[d] = M.noise.p1[d] + t * (M.noise.p2[d] - M.noise.p1[d]);
+                }
+                sup = std::max(sup, eval_expr(M.noise.pdf, pt.data(), nullptr, nullptr));
+                int d = nd - 1;
+                for (; d >= 0; --d) {
+                    if (++idx[d] < per_dim) break;
+                    idx[d] = 0;
+                }
+                if (d < 0) break;
+            }
+            if (!(sup > 0.0)) throw DomainErr("sample: custom density appears to be zero on its support");
+            A.custom_sup = sup * 1.5;
+        }
         for (int d = 0; d < n; ++d) {
             A.x0[d] = x[d];
             if (spec.target.dim() == n) { A.tlo[d] = spec.target.lo[d]; A.thi[d] = spec.target.hi[d]; }

@@ -783,13 +783,30 @@ __global__ void __launch_bounds__(128) k_simulate(GmDev D, SimArgs A) {
                 case GM_NORMAL: v = D.s[d] * 0.70710678118654752440 * rng.normal(); break; // s = sigma*sqrt2
                 case GM_UNIFORM: v = D.s[d] + (D.p2[d] - D.s[d]) * rng.uniform(); break;
                 case GM_EXPONENTIAL: v = -log1p(-rng.uniform()) / D.s[d]; break;
+                case GM_CUSTOM: v = 0.0; break; // joint draw below
                 default: {
                     const double ga = rng.gamma(D.s[d]), gb = rng.gamma(D.p2[d]);
                     v = ga / (ga + gb);
                 }
             }
-            xi[d] = D.mult ? v * x[d] : v;
+            xi[d] = v;
         }
+        if (D.family == GM_CUSTOM) { // rejection sampling over the support (noise.cpp:335-352)
+            bool acc = false;
+            for (int tries = 0; tries < 1000000 && !acc; ++tries) {
+                for (int d = 0; d < n; ++d) xi[d] = D.sup_lo[d] + rng.uniform() * (D.sup_hi[d] - D.sup_lo[d]);
+                double pv = 0.0;
+                if (!run_expr(D, sprog, slits, n, xi, nullptr, nullptr, pv)) break;
+                acc = rng.uniform() * A.custom_sup <= pv;
+            }
+            if (!acc) {
+                atomicMin(A.err, static_cast<unsigned long long>(r));
+                state = 2;
+                break;
+            }
+        }
+        for (int d = 0; d < n; ++d)
+            if (D.mult) xi[d] *= x[d];
         if (!run_dynamics(D, sprog, slits, x, u, w, mu)) {
             atomicMin(A.err, static_cast<unsigned long long>(r));
             state = 2;

@@ -77,6 +77,7 @@ void mask(const GmDev& D, long long r_lo, long long nrows, double* probs, const 
 // the model's (GmDev: dynamics, noise, disturbance grid, region check).
 struct SimArgs {
     int runs, T, reach, has_avoid, worst_case;
+    double custom_sup; // custom densities: rejection envelope (custom_sup_estimate, noise.cpp:307-333)
     unsigned long long seed;
     double x0[GMD_MAXD];
     double tlo[GMD_MAXD], thi[GMD_MAXD], alo[GMD_MAXD], ahi[GMD_MAXD]; // result spec boxes

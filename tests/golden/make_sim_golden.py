@@ -29,7 +29,30 @@ REF_BIN = HERE.parents[1] / "oracle" / "_ref" / "gridmdp_ref"
 RUNS = 20000
 SEED = 20240
 CASES = ["fixture2d_ra", "fixture2d_safety", "ref_vehicle3_T8", "ref_robot_reachavoid_T2", "room5_exp",
-         "room5_beta", "mult1d", "chain09", "reach_uniform"]
+         "room5_beta", "mult1d", "chain09", "reach_uniform", "custom_tri1d", "custom_tri2d"]
+
+
+def ref_case(cfgp: Path, tmp: Path):
+    """(reference config, flags): custom-density cases run through ref_driver --custom-* on the
+    same config with a placeholder noise (as tests/golden/make_golden.py)."""
+    import re
+    text = cfgp.read_text()
+    if "noise.type = custom;" not in text:
+        return cfgp, []
+    kv, keep = {}, []
+    for raw in text.splitlines():
+        line = raw.split("#", 1)[0].strip()
+        k = line.split("=", 1)[0].strip() if "=" in line else ""
+        if k in ("noise.type", "noise.pdf", "noise.support.lb", "noise.support.ub"):
+            kv[k] = line.split("=", 1)[1].strip().rstrip(";").strip()
+        else:
+            keep.append(raw)
+    n = int(re.search(r"states.dim = (\d+);", text).group(1))
+    keep += ["noise.type = normal;", "noise.sigma = {" + ", ".join(["1.0"] * n) + "};"]
+    rp = tmp / f"{cfgp.stem}.ref.cfg"
+    rp.write_text("\n".join(keep) + "\n")
+    return rp, ["--custom-pdf", kv["noise.pdf"], "--custom-lb", kv["noise.support.lb"], "--custom-ub",
+                kv["noise.support.ub"]]
 
 
 def grid_point(kv: dict, prefix: str, flat: int) -> list:
@@ -61,7 +84,8 @@ def main() -> None:
             rpath.write_bytes(G.load(e["results"]))
             entry = {"x0": x0, "x0_index": ix, "value_at_x0": float(v0[ix]), "modes": {}}
             for dm in ("random", "worst-case"):
-                args = [str(REF_BIN), "simulate", "-c", str(G.case_cfg(case)), "--results", str(rpath),
+                cfg_ref, custom = ref_case(G.case_cfg(case), Path(d))
+                args = [str(REF_BIN), "simulate", "-c", str(cfg_ref), *custom, "--results", str(rpath),
                         "--x0", "{" + ", ".join(repr(v) for v in x0) + "}", "--runs", str(RUNS), "--seed",
                         str(SEED), "--dist-mode", dm, "--threads", "0", *e.get("overrides", [])]
                 txt = subprocess.run(args, capture_output=True, text=True, check=True).stdout
