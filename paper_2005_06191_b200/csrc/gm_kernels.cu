@@ -475,15 +475,14 @@ struct RowSched {
     }
 };
 
-template <int TPR>
-__global__ void __launch_bounds__(kThreads) k_expect_matrix_et(GmDev D, long long row0, long long r_lo,
+template <int TPR, int U, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_expect_matrix_et(GmDev D, long long row0, long long r_lo,
                                                               long long r_hi, GmFastDiv div_nuw, int flags,
                                                               const double* __restrict__ probs,
                                                               const long long* __restrict__ origins,
                                                               const double* __restrict__ t0x,
                                                               const double* __restrict__ V,
                                                               double* __restrict__ v_in) {
-    constexpr int U = 8;
     constexpr int groups = kThreads / TPR;
     const int R = static_cast<int>(D.R);
     int* E = reinterpret_cast<int*>(g_sm + kThreads / 32); // after the group partials
@@ -1237,18 +1236,33 @@ void expect_matrix(const GmDev& D, long long row0, long long r_lo, long long r_h
         const GmFastDiv dn = gm_fastdiv(static_cast<uint32_t>(div32 ? nuw : 1));
         static const char* cg = std::getenv("GM_CONTIG");
         const int flags = div32 | ((cg && std::atoi(cg)) ? 2 : 0);
+        // loads in flight per lane (U) and residency (MINB, the register cap): default
+        // U = 12 at 6 CTAs/SM (C2b 16.3 ms); GM_ET_VARIANT=1 (8, 6) 17.1 ms, 2 (16, 4)
+        // 17.7 ms, 3 (10, 6) 17.3 ms, 4 (14, 6) 17.3 ms; (8, 8) 21.4, (16, 3) 19.2, (12, 7) 18.2
+        static const char* ev = std::getenv("GM_ET_VARIANT");
+        const int var = ev ? std::atoi(ev) : 0;
+#define GM_ET1(T, UU, MB)                                                                                   \
+    {                                                                                                       \
+        auto k = k_expect_matrix_et<T, UU, MB>;                                                             \
+        allow_smem(k, et_smem);                                                                             \
+        k<<<resident_grid(k, et_smem, blocks_needed), kThreads, et_smem, s>>>(D, row0, r_lo, r_hi, dn, flags, \
+                                                                             probs, origins, t0x, V, v_in); \
+        check_launch("expect_matrix");                                                                      \
+        return;                                                                                             \
+    }
+#define GM_ET(T)                                                                                            \
+    case T:                                                                                                 \
+        if (var == 1) GM_ET1(T, 8, 6)                                                                       \
+        if (var == 2) GM_ET1(T, 16, 4)                                                                      \
+        if (var == 3) GM_ET1(T, 10, 6)                                                                      \
+        if (var == 4) GM_ET1(T, 14, 6)                                                                      \
+        GM_ET1(T, 12, 6)
         switch (D.tpr) {
-#define GM_ET(T)                                                                                          \
-    case T:                                                                                               \
-        allow_smem(k_expect_matrix_et<T>, et_smem);                                                       \
-        k_expect_matrix_et<T><<<resident_grid(k_expect_matrix_et<T>, et_smem, blocks_needed), kThreads,   \
-                                et_smem, s>>>(D, row0, r_lo, r_hi, dn, flags, probs, origins, t0x, V, v_in); \
-        check_launch("expect_matrix");                                                                    \
-        return;
             GM_ET(1) GM_ET(2) GM_ET(4) GM_ET(8) GM_ET(16) GM_ET(32) GM_ET(64) GM_ET(128)
-#undef GM_ET
         default: break;
         }
+#undef GM_ET
+#undef GM_ET1
     }
     const size_t smem = (kThreads / 32) * sizeof(double) + (in_smem ? table : 0);
     if (in_smem) {
