@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_build(GmDev D, long long row0, 
 
 // Stage (ii), on the fly (synthesis.cpp:100-104 + dot_slab :18-47): row groups
 // of tpr threads recompute each row from the staged masses and dot it with V.
-template <int TAB, bool LS>
+template <int TAB, bool LS, int U = 4>
 __global__ void __launch_bounds__(kThreads) k_expect_ofa(GmDev D, long long nrows, int rb, GmFastDiv div_rb,
                                                         const double* __restrict__ mass,
                                                         const long long* __restrict__ origin,
@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(kThreads) k_expect_ofa(GmDev D, long long nrow
             const uint8_t fl = valid ? rowflag[row] : RF_ABSORBED;
             double s = 0.0;
             if (!(fl & (RF_ABSORBED | RF_ERROR))) {
-                s = row_dot<TAB == TAB_Q ? 1 : 2, 4, LS>(D, lane, tpr, nullptr, Y.offQ + i * D.n_lines,
+                s = row_dot<TAB == TAB_Q ? 1 : 2, U, LS>(D, lane, tpr, nullptr, Y.offQ + i * D.n_lines,
                                                          Y.offP + i * D.P_size, i * Y.mw + D.mm_off,
                                                          i * Y.mw + D.ml_off, V + origin[row], D.line_off, Y.offL);
             }
@@ -1194,10 +1194,13 @@ template <int TAB, bool LS>
 static void launch_ofa(const GmDev& D, const BatchPlan& b, long long nrows, const double* mass,
                        const long long* origin, const double* t0x, const uint8_t* rowflag, const double* V,
                        double* v_in, cudaStream_t s) {
-    allow_smem(k_expect_ofa<TAB, LS>, b.smem);
     const long long batches = (nrows + b.rb - 1) / b.rb;
-    k_expect_ofa<TAB, LS><<<resident_grid(k_expect_ofa<TAB, LS>, b.smem, batches), kThreads, b.smem, s>>>(
-        D, nrows, b.rb, gm_fastdiv(b.rb), mass, origin, t0x, rowflag, V, v_in);
+    static const char* ou = std::getenv("GM_OFA_U"); // terms in flight per lane (tuning)
+    const int u = ou ? std::atoi(ou) : 6; // C5: U = 4 1.23 s, 6 1.14 s, 8 1.14 s
+    auto k = u == 8 ? k_expect_ofa<TAB, LS, 8> : (u == 6 ? k_expect_ofa<TAB, LS, 6> : k_expect_ofa<TAB, LS, 4>);
+    allow_smem(k, b.smem);
+    k<<<resident_grid(k, b.smem, batches), kThreads, b.smem, s>>>(D, nrows, b.rb, gm_fastdiv(b.rb), mass, origin,
+                                                                 t0x, rowflag, V, v_in);
 }
 
 void expect_ofa(const GmDev& D, long long nrows, const double* mass, const long long* origin,
