@@ -1117,7 +1117,9 @@ void build(const GmDev& D, long long row0, long long nrows, long long* origin_ou
         const size_t fixed_d = D.n_ins + D.n_lits + 3 + (qs ? (D.pitch + 1) / 2 + (kThreads / 32) * D.n_lines : 0);
         // two table buffers + two prologue buffers (pro_doubles: <= (5n + 2) rb + 2 for both)
         const size_t per_d = 2 * (mw + D.P_size) + 5 * static_cast<size_t>(D.n) + 2;
-        const size_t budget_d = 54 * 1024 / sizeof(double); // 4 CTAs/SM
+        static const char* bc = std::getenv("GM_BUILD_CTAS"); // resident CTAs per SM (tuning; AOT kernels)
+        const int ctas = bc ? std::max(2, std::min(6, std::atoi(bc))) : 3; // 3: 2-4 % faster than 4 on C2b
+        const size_t budget_d = (216 / ctas) * 1024 / sizeof(double);
         if (fixed_d < budget_d) {
             long long rb = std::min<long long>(64, static_cast<long long>((budget_d - fixed_d) / per_d));
             // consumers: one (row, axis) item per thread; at least 2 filler warps
@@ -1134,8 +1136,12 @@ void build(const GmDev& D, long long row0, long long nrows, long long* origin_ou
                 const size_t smem = (fixed_d + per_d * static_cast<size_t>(rb)) * sizeof(double);
                 const long long batches = (nrows + rb - 1) / rb;
                 const void* k = (jit_ws && jit_ws[qs ? 1 : 0]) ? jit_ws[qs ? 1 : 0]
-                                       : (qs ? reinterpret_cast<const void*>(&k_build_ws<true>)
-                                             : reinterpret_cast<const void*>(&k_build_ws<false>));
+                                       : (ctas == 4 ? (qs ? reinterpret_cast<const void*>(&k_build_ws<true, 4>)
+                                                          : reinterpret_cast<const void*>(&k_build_ws<false, 4>))
+                                          : ctas == 5 ? (qs ? reinterpret_cast<const void*>(&k_build_ws<true, 5>)
+                                                            : reinterpret_cast<const void*>(&k_build_ws<false, 5>))
+                                          : (qs ? reinterpret_cast<const void*>(&k_build_ws<true, 3>)
+                                                : reinterpret_cast<const void*>(&k_build_ws<false, 3>)));
                 if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                 int per_sm = 0;
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, smem);

@@ -564,8 +564,8 @@ __device__ __forceinline__ void build_prologue(const GmDev& D, const GmIns* spro
 // QS = per-warp Q scratch + element table (n_lines and W_last small enough);
 // otherwise rows are expanded by the incremental slab walk, q = P[a]*mm[j] per term.
 #if !defined(__CUDACC_RTC__) || defined(GM_JIT_BUILD)
-template <bool QS>
-__global__ void __launch_bounds__(kThreads, 4) k_build_ws(GmDev D, long long row0, long long nrows, int rb,
+template <bool QS, int MINB = 3>
+__global__ void __launch_bounds__(kThreads, MINB) k_build_ws(GmDev D, long long row0, long long nrows, int rb,
                                                       int npw, int ncw, int opts,
                                                       long long* __restrict__ origin_out,
                                                       double* __restrict__ t0x_out, double* __restrict__ probs,
