@@ -301,12 +301,12 @@ def main():
     roofline["frac"] = roofline["achieved"] / hbm
     if not matrix:
         roofline["note"] = "OFA: HBM-equivalent bytes (8 per recomputed term), SURVEY.md §8d"
-    exp_ms = fam_ms["expand"] / max(fam_n["expand"], 1)
+    exp_ms = fam_ms["build"] / max(fam_n["build"], 1)
     build_bytes = my_rows * (R * 8 + 8 + (8 if reach else 0))  # rows written + origins (+ T0x)
-    roofline_build = {"kernel": "k_build", "bound": "hbm",
+    roofline_build = {"kernel": "k_build_ws", "bound": "hbm",
                       "achieved": build_bytes / (exp_ms / 1e3) / 1e9 if exp_ms > 0 else None, "peak": hbm,
                       "unit": "GB/s", "algorithmic_bytes_per_launch": build_bytes, "avg_launch_ms": exp_ms,
-                      "traffic": ncu_traffic("k_build", args.workload)}
+                      "traffic": ncu_traffic("k_build_ws", args.workload)}
     if roofline_build["achieved"]:
         roofline_build["frac"] = roofline_build["achieved"] / hbm
 

@@ -20,8 +20,8 @@ GM_MODE_MATRIX, GM_MODE_OFA = 0, 1
 GM_SAFETY, GM_REACH, GM_REACH_AVOID = 0, 1, 2
 
 # kernel families (gm_kernels.cuh)
-KF_PROLOGUE, KF_EXPAND, KF_MASK, KF_EXPECT_MATRIX, KF_EXPECT_OFA, KF_MAXMIN, KF_MISC = range(7)
-KF_NAMES = ["prologue", "expand", "mask", "expect_matrix", "expect_ofa", "maxmin", "misc"]
+KF_PROLOGUE, KF_BUILD, KF_MASK, KF_EXPECT_MATRIX, KF_EXPECT_OFA, KF_MAXMIN, KF_MISC = range(7)
+KF_NAMES = ["prologue", "build", "mask", "expect_matrix", "expect_ofa", "maxmin", "misc"]
 
 
 class Status(C.Structure):

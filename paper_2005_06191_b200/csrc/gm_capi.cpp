@@ -481,7 +481,7 @@ void build_rows(gm_model* m, int64_t r0, int64_t r1, gm_matrix* tm, bool want_t0
     const gmj::Kernels* J =
         jit_kernels(m, gmk::build_uses_qs(m->D) ? gmj::WANT_BUILD_QS : gmj::WANT_BUILD_NOQS, n);
     {
-        Launch L(gmk::KF_EXPAND, m->stream);
+        Launch L(gmk::KF_BUILD, m->stream);
         static const char* sl = std::getenv("GM_BUILD_SLICES");
         const int64_t slices = sl ? std::max(1, std::atoi(sl)) : 1;
         const int64_t per = (n + slices - 1) / slices;
@@ -932,7 +932,7 @@ gm_code gm_build_shard_host(gm_model* m, int64_t x0, int64_t x1, gm_matrix** out
             const int64_t c0 = k * per, cn = std::min(per, n - c0);
             if (cn <= 0) break;
             {
-                Launch L(gmk::KF_EXPAND, m->stream);
+                Launch L(gmk::KF_BUILD, m->stream);
                 gmk::build(m->D, r0 + c0, cn, tm->origins.p + c0, reach ? tm->t0x.p + c0 : nullptr,
                            tm->probs.p + c0 * tm->pitch, m->d_err.p, m->stream, J ? J->build_ws : nullptr);
             }

@@ -15,7 +15,7 @@ enum : uint8_t { RF_ABSORBED = 1, RF_ERROR = 2 };
 enum : int { PF_SKIP_ABSORBED = 1, PF_T0X = 2, PF_MASSES = 4 };
 
 // kernel families (timing / launch accounting)
-enum Family { KF_PROLOGUE = 0, KF_EXPAND = 1, KF_MASK = 2, KF_EXPECT_MATRIX = 3, KF_EXPECT_OFA = 4,
+enum Family { KF_PROLOGUE = 0, KF_BUILD = 1, KF_MASK = 2, KF_EXPECT_MATRIX = 3, KF_EXPECT_OFA = 4,
               KF_MAXMIN = 5, KF_MISC = 6, KF_COUNT = 7 };
 
 struct BatchPlan {
