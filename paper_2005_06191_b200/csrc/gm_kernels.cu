@@ -1114,7 +1114,7 @@ void build(const GmDev& D, long long row0, long long nrows, long long* origin_ou
         static const char* bo2 = std::getenv("GM_BUILD_OPTS");
         const int wopts = bo2 ? std::atoi(bo2) : 0;
         const bool qs = build_uses_qs(D);
-        const size_t fixed_d = D.n_ins + D.n_lits + 3 + (qs ? (D.pitch + 1) / 2 + (kThreads / 32) * D.n_lines : 0);
+        const size_t fixed_d = D.n_ins + D.n_lits + 3 + (qs ? (D.pitch + 1) / 2 + (kThreads / 32) * (D.n_lines + 1) : 0);
         // two table buffers + two prologue buffers (pro_doubles: <= (5n + 2) rb + 2 for both)
         const size_t per_d = 2 * (mw + D.P_size) + 5 * static_cast<size_t>(D.n) + 2;
         static const char* bc = std::getenv("GM_BUILD_CTAS"); // resident CTAs per SM (tuning; AOT kernels)

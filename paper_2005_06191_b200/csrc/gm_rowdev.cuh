@@ -575,7 +575,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_build_ws(GmDev D, long long 
     const int nl = D.n_lines;
     const int tsz = rb * (mw + D.P_size), psz = pro_doubles(rb, D.n);
     const int offT = 0, offPro = offT + 2 * tsz, offQs = offPro + 2 * psz;
-    const int offProg = offQs + (QS ? (kThreads / 32) * nl : 0);
+    const int offProg = offQs + (QS ? (kThreads / 32) * (nl + 1) : 0); // per-warp Q[nl] + a zero slot
     GmIns* sprog = reinterpret_cast<GmIns*>(g_sm + offProg);
     double* slits = g_sm + offProg + D.n_ins;
     int* claim = reinterpret_cast<int*>(slits + D.n_lits); // fill-row counters by batch parity
@@ -583,11 +583,14 @@ __global__ void __launch_bounds__(kThreads, MINB) k_build_ws(GmDev D, long long 
     for (int c = threadIdx.x; c < D.n_ins; c += blockDim.x) sprog[c] = D.prog[c];
     for (int c = threadIdx.x; c < D.n_lits; c += blockDim.x) slits[c] = D.lits[c];
     if (threadIdx.x < 2) claim[threadIdx.x] = 0;
-    if (QS)
-        for (int t = threadIdx.x; t < D.pitch; t += blockDim.x) { // entries past R: padding (unused)
+    if (QS) {
+        // entries past R (row padding) point at the warp's zero slot Q[nl]: 0 * ml[0] = +0.0
+        for (int t = threadIdx.x; t < D.pitch; t += blockDim.x) {
             const int L = D.div_Wl.div(t < R ? t : 0);
-            ET[t] = t < R ? (L * 8) | ((t - L * D.Wl) * 8) << 16 : 0;
+            ET[t] = t < R ? (L * 8) | ((t - L * D.Wl) * 8) << 16 : nl * 8;
         }
+        if (threadIdx.x < kThreads / 32) g_sm[offQs + threadIdx.x * (nl + 1) + nl] = 0.0;
+    }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int np = npw * 32, nc = ncw * 32;
     const int role = warp < npw ? 0 : (warp < npw + ncw ? 1 : 2); // producer, consumer, filler
@@ -650,7 +653,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_build_ws(GmDev D, long long 
             const long long b0 = first_row(i);
             const double* tb = g_sm + offT + static_cast<int>(i & 1) * tsz;
             const double* P = tb + rb * mw;
-            double* Qs = g_sm + offQs + warp * nl;
+            double* Qs = g_sm + offQs + warp * (nl + 1);
             for (;;) {
                 int r = 0;
                 if (lane == 0) r = atomicAdd(&claim[i & 1], 1);
@@ -674,13 +677,15 @@ __global__ void __launch_bounds__(kThreads, MINB) k_build_ws(GmDev D, long long 
                     __syncwarp();
                     const char* qb = reinterpret_cast<const char*>(Qs);
                     const char* mb = reinterpret_cast<const char*>(m + D.ml_off);
-                    auto val = [&](int t) {
-                        const int e = ET[t];
-                        return *reinterpret_cast<const double*>(qb + (e & 0xffff)) *
-                               *reinterpret_cast<const double*>(mb + (e >> 16));
-                    };
+                    const int* e = ET + lane;
+                    double* o = out + lane;
+                    const int n_it = (pitch - lane + 31) >> 5;
 #pragma unroll 4
-                    for (int t = lane; t < pitch; t += 32) __stcs(out + t, t < R ? val(t) : 0.0);
+                    for (int k = 0; k < n_it; ++k, e += 32, o += 32) {
+                        const int ev = *e;
+                        __stcs(o, *reinterpret_cast<const double*>(qb + (ev & 0xffff)) *
+                                      *reinterpret_cast<const double*>(mb + (ev >> 16)));
+                    }
                     __syncwarp();
                 } else {
                     Walk wk = wk0;
