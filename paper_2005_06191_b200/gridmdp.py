@@ -226,7 +226,7 @@ class SystemModel:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and lib is not None:  # module globals may already be cleared at interpreter exit
             lib.gm_model_free(h)
             self._h = None
 
@@ -396,7 +396,7 @@ class TransitionMatrix:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and lib is not None:
             lib.gm_matrix_free(h)
             self._h = None
 
@@ -507,7 +507,7 @@ class SynthesisResult:
     _h: Optional[C.c_void_p] = field(default=None, repr=False)
 
     def __del__(self):
-        if self._h:
+        if getattr(self, "_h", None) and lib is not None:
             lib.gm_result_free(self._h)
             self._h = None
 
@@ -635,7 +635,7 @@ class TrajectoryBatch:
     _h: Optional[C.c_void_p] = field(default=None, repr=False)
 
     def __del__(self):
-        if self._h:
+        if getattr(self, "_h", None) and lib is not None:
             lib.gm_sim_free(self._h)
             self._h = None
 

@@ -77,7 +77,7 @@ class DeviceBackend:
             lib.gm_matrix_free(tm)
 
     def release(self) -> None:
-        if self._tm:
+        if self._tm and lib is not None:
             lib.gm_matrix_free(self._tm)
             self._tm = C.c_void_p()
 

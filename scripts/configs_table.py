@@ -4,7 +4,7 @@
 for the FP64-utilisation column. Not a bench line: a table for profiles/.
 
 GPU: one full synthesis (build + T steps in matrix mode, T OFA steps otherwise)
-after a warm-up run at T = 1, device-timed with CUDA events on the engine's
+after a warm-up run of the same model (T = 1 for the traffic cases), device-timed with CUDA events on the engine's
 stream. CPU: the reference's `synthesize` (time_synthesize_s) where the whole
 horizon takes seconds, else one reference `bellman_step` over all rows x T
 (steps cost the same, synthesis.cpp:165-195). `--threads 1` runs give per-core
@@ -70,13 +70,18 @@ def gpu_run(name, text, stream, dev):
     from paper_2005_06191_b200 import sharded as S
 
     lib = _capi.lib
-    mw = g.parse_config(with_horizon(text, 1), name)  # warm-up: JIT, allocations
-    bw = S.DeviceBackend(mw, stream)
-    S.synthesize_sharded(bw, int(mw.sizes().n_states), 1, mw.spec.is_reach(), mw.options.mode == "matrix", dev)
-    bw.release()
     m = g.parse_config(text, name)
     s = m.sizes()
     be = S.DeviceBackend(m, stream)
+    # warm-up: JIT, the model's device buffers and matrix allocation (a few ms of one-time
+    # setup that dominates the small configs); the 7-step traffic OFA cases warm at T = 1
+    big = int(s.rows) * int(s.row_width) * int(s.horizon) > 2e12
+    mw = g.parse_config(with_horizon(text, 1), name) if big else m
+    bw = S.DeviceBackend(mw, stream) if big else be
+    S.synthesize_sharded(bw, int(s.n_states), int(mw.sizes().horizon), m.spec.is_reach(),
+                         m.options.mode == "matrix", dev)
+    if big:
+        bw.release()
     ev = {}
 
     def mark(k):
@@ -166,7 +171,7 @@ def main():
             "# SURVEY §8.0 workloads on one B200 vs the reference on the host CPU\n\n"
             f"`python scripts/configs_table.py --out {a.out}`. HBM = {hbm} GB/s ({peak_kind}); FP64 DFMA peak "
             f"{f64:.2f} TFLOP/s measured by scripts/fp64_peak.cu on the same box. GPU: one full synthesis after a "
-            "T = 1 warm-up, CUDA events on the engine's stream (build = stage i of matrix mode; sweep = the T "
+            "warm-up run of the same model (T = 1 for C4/C4p), CUDA events on the engine's stream (build = stage i of matrix mode; sweep = the T "
             "Bellman steps; OFA has no build). G terms/s = rows·R·T / sweep; HBM-equiv = 8 B per term against "
             "HBM (the bytes matrix mode would stream); FP64 util = 2 flops per term against the DFMA peak. "
             "CPU: the reference compiled from its sources (oracle/_ref), all host threads.\n\n" + table
