@@ -194,6 +194,8 @@ def main():
     ap.add_argument("--extra", default="C5", help="comma list of extra OFA workloads timed once (sweep only)")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "halo", "allgather"],
+                    help="V exchange between ranks (N > 1)")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
 
@@ -234,6 +236,10 @@ def main():
     my_rows = (plan.x1 - plan.x0) * nuw
     stream = torch.cuda.current_stream()
     be = S.DeviceBackend(m, stream)
+    # V exchange for N > 1, planned once per model: the shards' cutoff-bounded halos
+    # (point-to-point) when they are at most half the all-gather, else the all-gather
+    xplan = S.exchange_plan(be, plan, None, args.exchange) if world > 1 else None
+    exchange = xplan if xplan is not None else "allgather"
 
     def one_step():
         ev = {}
@@ -243,7 +249,7 @@ def main():
             e.record(stream)
             ev[name] = e
 
-        S.synthesize_sharded(be, n_x, T, reach, matrix, dev, None, mark)
+        S.synthesize_sharded(be, n_x, T, reach, matrix, dev, None, mark, exchange=exchange)
         return ev
 
     for _ in range(args.warmup):
@@ -318,6 +324,9 @@ def main():
         "config": {"workload": args.workload, "model": "vehicle3-eta/4 reach-avoid (stored MDP)",
                    "states": n_x, "rows": rows_all, "row_width": R, "horizon": T,
                    "matrix_bytes": rows_all * R * 8, "parallelism": f"state-shard x{world}",
+                   "v_exchange": ("none" if world == 1 else
+                                  f"halo p2p ({xplan.halo_states} of {xplan.allgather_states} all-gather states)"
+                                  if xplan is not None else "all-gather per step"),
                    "l2": "inputs larger than L2 (108 GB matrix streamed per step)"},
         "build_ms_per_step": bsum / args.steps, "sweep_s": sweep_s,
         "sweep_terms_per_s": terms_per_step / sweep_s if sweep_s > 0 else None,

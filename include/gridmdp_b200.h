@@ -212,6 +212,15 @@ gm_code gm_build_shard(gm_model* m, int64_t x_begin, int64_t x_end, gm_matrix** 
  * pinned buffers for the copies to overlap). Either output may be NULL. */
 gm_code gm_build_shard_host(gm_model* m, int64_t state_begin, int64_t state_end, gm_matrix** out,
                             int64_t* origins_out, double* t0x_out, gm_status* st);
+/* Halo of a shard (SURVEY.md §8 e): the flat state interval [*lo, *hi) that the
+ * backward step of states [x_begin, x_end) reads from v_next. Slab origins do not
+ * depend on the step (abstraction.cpp:103-120), so the interval is the rows'
+ * [min origin, max origin + last slab offset]; rows of absorbed states (skipped
+ * by the step for reach specs, synthesis.cpp:86-89) do not count. Drives the
+ * multi-GPU V exchange: ranks send each other only these ranges when they are
+ * much smaller than the grid, otherwise the V shards are all-gathered. */
+gm_code gm_shard_reach(gm_model* m, int64_t x_begin, int64_t x_end, int64_t* lo, int64_t* hi,
+                       gm_status* st);
 /* Per-row expected values of the model's most recent step (the v_in workspace of
  * bellman_impl, synthesis.cpp:69-109), rows of the stepped states; n doubles. */
 gm_code gm_copy_row_values(gm_model* m, double* out, int64_t n, gm_status* st);

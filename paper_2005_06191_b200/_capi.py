@@ -113,6 +113,7 @@ SIGNATURES = {
     "gm_step_device": (C.c_int, [_VP, _VP, _I64, _I64, _VP, _VP, _VP, _VP, _VP, _PS]),
     "gm_build_shard": (C.c_int, [_VP, _I64, _I64, C.POINTER(_VP), _PS]),
     "gm_build_shard_host": (C.c_int, [_VP, _I64, _I64, C.POINTER(_VP), _VP, _VP, _PS]),
+    "gm_shard_reach": (C.c_int, [_VP, _I64, _I64, C.POINTER(_I64), C.POINTER(_I64), _PS]),
     "gm_check_device_errors": (C.c_int, [_VP, _PS]),
     "gm_copy_row_values": (C.c_int, [_VP, _VP, _I64, _PS]),
     "gm_zero_absorbing_device": (C.c_int, [_VP, _VP, _VP, _PS]),

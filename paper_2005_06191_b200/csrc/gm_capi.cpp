@@ -266,6 +266,7 @@ struct gm_model {
     DevBuf<double> d_mass[2], d_t0x[2], d_vin, d_chunk;
     DevBuf<long long> d_origin[2];
     DevBuf<uint8_t> d_rowflag[2];
+    DevBuf<long long> d_reach; // origin min / max (gm_shard_reach)
     cudaStream_t aux = nullptr; // producer stream of the row-prologue pipeline
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_ready[2] = {}, ev_used[2] = {};
     bool dev_ready = false;
@@ -952,6 +953,46 @@ gm_code gm_build_shard_host(gm_model* m, int64_t x0, int64_t x1, gm_matrix** out
         for (int64_t k = 0; k < slices; ++k) cudaEventDestroy(ev[k]);
         raise_device_error(m);
         if (fresh) *out = fresh.release();
+    });
+}
+
+gm_code gm_shard_reach(gm_model* m, int64_t x0, int64_t x1, int64_t* lo, int64_t* hi, gm_status* st) {
+    return guarded(st, [&] {
+        if (x0 < 0 || x1 > m->M.n_x() || x0 > x1) throw std::out_of_range("shard_reach: state range outside the grid");
+        prepare(m);
+        *lo = *hi = x0;
+        if (x1 == x0) return;
+        if (m->M.noise.family == GM_CUSTOM) { // conservative: the whole grid
+            *lo = 0;
+            *hi = m->M.n_x();
+            return;
+        }
+        const int64_t nuw = m->M.n_u() * m->M.n_w();
+        const int64_t r0 = x0 * nuw, n = (x1 - x0) * nuw;
+        const int64_t chunk = std::min(chunk_rows(m), n);
+        ensure_scratch(m, chunk);
+        m->d_reach.ensure(2, "reach bounds");
+        const long long init[2] = {LLONG_MAX, -1};
+        ck(cudaMemcpyAsync(m->d_reach.p, init, sizeof init, cudaMemcpyHostToDevice, m->stream), "reach init");
+        const gmj::Kernels* J = jit_kernels(m, gmj::WANT_PROLOGUE, n);
+        // rows of absorbed states are skipped by the step for reach specs (synthesis.cpp:86-89)
+        const int flags = m->M.spec.reach() ? gmk::PF_SKIP_ABSORBED : 0;
+        for (int64_t c0 = 0; c0 < n; c0 += chunk) {
+            const int64_t cn = std::min(chunk, n - c0);
+            Launch L(gmk::KF_MISC, m->stream);
+            gmk::prologue(m->D, r0 + c0, cn, flags, m->d_origin[0].p, nullptr, m->d_rowflag[0].p, nullptr, m->d_err.p,
+                          m->stream, J ? J->prologue : nullptr);
+            gmk::origin_minmax(m->d_origin[0].p, m->d_rowflag[0].p, cn, m->d_reach.p, m->stream);
+        }
+        long long mm[2];
+        ck(cudaMemcpyAsync(mm, m->d_reach.p, sizeof mm, cudaMemcpyDeviceToHost, m->stream), "reach bounds");
+        ck(cudaStreamSynchronize(m->stream), "shard reach");
+        raise_device_error(m);
+        if (mm[1] < 0) return; // every row absorbed: the step reads nothing
+        int64_t span = 0; // the slab's last post-state relative to its origin
+        for (int d = 0; d < m->D.n; ++d) span += (m->D.W[d] - 1) * m->D.xstride[d];
+        *lo = mm[0];
+        *hi = std::min<int64_t>(m->M.n_x(), mm[1] + span + 1);
     });
 }
 

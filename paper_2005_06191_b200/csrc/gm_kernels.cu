@@ -1098,6 +1098,35 @@ void build_custom(const GmDev& D, long long row0, long long nrows, long long* or
     check_launch("build_custom");
 }
 
+namespace {
+__global__ void k_origin_minmax(const long long* __restrict__ o, const uint8_t* __restrict__ f, long long n,
+                                long long* mm) {
+    long long lo = LLONG_MAX, hi = -1;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        if (f[i] == 0) {
+            lo = o[i] < lo ? o[i] : lo;
+            hi = o[i] > hi ? o[i] : hi;
+        }
+    for (int off = 16; off >= 1; off >>= 1) {
+        const long long ol = __shfl_xor_sync(0xffffffffu, lo, off), oh = __shfl_xor_sync(0xffffffffu, hi, off);
+        lo = ol < lo ? ol : lo;
+        hi = oh > hi ? oh : hi;
+    }
+    if ((threadIdx.x & 31) == 0 && hi >= 0) {
+        atomicMin(mm, lo);
+        atomicMax(mm + 1, hi);
+    }
+}
+} // namespace
+
+void origin_minmax(const long long* origins, const uint8_t* rowflag, long long n, long long* mm, cudaStream_t s) {
+    if (n <= 0) return;
+    const long long blocks = std::min<long long>((n + kThreads - 1) / kThreads, 148 * 8);
+    k_origin_minmax<<<static_cast<int>(blocks), kThreads, 0, s>>>(origins, rowflag, n, mm);
+    check_launch("origin_minmax");
+}
+
 bool build_uses_qs(const GmDev& D) { return D.n_lines <= 512 && D.n_lines * 8 < 65536 && D.Wl * 8 < 32768; }
 
 void build(const GmDev& D, long long row0, long long nrows, long long* origin_out, double* t0x_out,

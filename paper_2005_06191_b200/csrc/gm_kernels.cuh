@@ -45,6 +45,9 @@ void build_custom(const GmDev& D, long long row0, long long nrows, long long* or
                   double* probs_out, unsigned long long* d_err, cudaStream_t s);
 // Whether build() uses the per-warp line-prefix variant k_build_ws<true>.
 bool build_uses_qs(const GmDev& D);
+// min / max of the flat slab origins of rows whose flag is 0 (not absorbed, no error);
+// mm[0] (init LLONG_MAX) and mm[1] (init -1) accumulate across calls
+void origin_minmax(const long long* origins, const uint8_t* rowflag, long long n, long long* mm, cudaStream_t s);
 // jit_ws: run-time compiled k_build_ws<false>, k_build_ws<true> (gm_jit.cpp) or nullptr.
 void build(const GmDev& D, long long row0, long long nrows, long long* origin_out, double* t0x_out,
            double* probs_out, unsigned long long* d_err, cudaStream_t s, const void* const* jit_ws = nullptr);

@@ -1,13 +1,16 @@
 """Multi-GPU synthesis: one process per GPU, state space sharded into
-contiguous flat-index ranges, V exchanged with one NCCL
-all-gather per Bellman step (the only data-path collective; stage (i) needs
-none).
+contiguous flat-index ranges; stage (i) needs no communication.
 
 Rows of a state are reduced only within that state (synthesis.cpp:112-142), so
 each rank owns the rows of its states and writes V_k for them; the next step
-needs V_{k+1} wherever its slabs reach, which the all-gather provides. Per-row
-arithmetic does not depend on the sharding, so results are bit-identical for
-any number of ranks.
+needs V_{k+1} wherever its slabs reach. That reach is fixed (slab origins do not
+depend on the step), so it is computed once per shard (`gm_shard_reach`, the
+cutoff-bounded halo): when the halos are much smaller than the grid each step
+exchanges only them (NCCL point-to-point, `batch_isend_irecv`) and the value
+table is all-gathered once after the sweep; otherwise (wide cutoffs, e.g. BMW
+slabs spanning four full axes) V is all-gathered after every step. Per-row
+arithmetic does not depend on the sharding or the exchange, so results are
+bit-identical for any number of ranks.
 
 The per-shard compute is a backend object with `build(x0, x1)` and
 `step(tm, x0, x1, v_next, v_out, pol, wst)`; the product backend is
@@ -93,17 +96,85 @@ class DeviceBackend:
     def check(self) -> None:
         call("gm_check_device_errors", self.model.handle)
 
+    def reach(self, x0: int, x1: int) -> tuple[int, int]:
+        """Flat interval of V_{k+1} read by the step of states [x0, x1) (gm_shard_reach)."""
+        lo, hi = C.c_int64(), C.c_int64()
+        call("gm_shard_reach", self.model.handle, C.c_int64(x0), C.c_int64(x1), C.byref(lo), C.byref(hi))
+        return lo.value, hi.value
+
+
+@dataclass
+class HaloPlan:
+    """Point-to-point V exchange of one rank: `sends` / `recvs` are (peer, a, b)
+    flat-state ranges; `halo` False means the all-gather is used instead."""
+
+    halo: bool
+    sends: list
+    recvs: list
+    halo_states: int
+    allgather_states: int
+
+
+def halo_plan(plan: ShardPlan, reach: list, threshold: float = 0.5) -> HaloPlan:
+    """Exchange plan from every rank's reach interval (`reach[r] = (lo, hi)`): rank j
+    sends rank r the part of its own states inside r's interval. The halo exchange
+    is used when it moves at most `threshold` of the all-gather's states."""
+    world, rank = plan.world, plan.rank
+    pieces = {}
+    for r in range(world):
+        lo, hi = reach[r]
+        for j in range(world):
+            if j == r:
+                continue
+            a, b = plan.bounds(j)
+            a, b = max(a, lo), min(b, hi)
+            if a < b:
+                pieces[(j, r)] = (a, b)
+    halo_states = sum(b - a for a, b in pieces.values())
+    ag_states = sum(plan.n_x - (plan.bounds(r)[1] - plan.bounds(r)[0]) for r in range(world))
+    sends = [(r, a, b) for (j, r), (a, b) in sorted(pieces.items()) if j == rank]
+    recvs = [(j, a, b) for (j, r), (a, b) in sorted(pieces.items()) if r == rank]
+    return HaloPlan(halo_states <= threshold * ag_states, sends, recvs, halo_states, ag_states)
+
+
+def exchange_plan(backend, plan: ShardPlan, group=None, exchange: str = "auto") -> Optional[HaloPlan]:
+    """The V exchange of a sharded sweep: None = all-gather after every step
+    (`exchange="allgather"`, one rank, or halos too wide under "auto"), else the
+    halo plan (`"halo"` forces it)."""
+    if exchange == "allgather" or not dist.is_initialized() or plan.world == 1 or not hasattr(backend, "reach"):
+        return None
+    lo, hi = backend.reach(plan.x0, plan.x1)
+    t = torch.tensor([lo, hi], dtype=torch.int64)
+    if dist.get_backend(group) == "nccl":
+        t = t.cuda()
+    allr = [torch.empty_like(t) for _ in range(plan.world)]
+    dist.all_gather(allr, t, group=group)
+    hp = halo_plan(plan, [tuple(int(v) for v in x.tolist()) for x in allr])
+    return hp if (hp.halo or exchange == "halo") else None
+
+
+def _exchange_halo(hp: HaloPlan, v: torch.Tensor, group=None) -> None:
+    ops = [dist.P2POp(dist.isend, v[a:b], peer, group) for peer, a, b in hp.sends]
+    ops += [dist.P2POp(dist.irecv, v[a:b], peer, group) for peer, a, b in hp.recvs]
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+
 
 def synthesize_sharded(backend, n_x: int, horizon: int, reach: bool, matrix: bool, device,
-                       group=None, timer=None):
+                       group=None, timer=None, exchange: str = "auto"):
     """run_backward (synthesis.cpp:165-195) over a sharded state space.
 
     Returns (values (T+1, n_x) on every rank, policy (T, n_x) and worst (T, n_x)
-    gathered on every rank). `timer(name)` is called at phase boundaries."""
+    gathered on every rank). `timer(name)` is called at phase boundaries.
+    `exchange`: "auto" (halo when it is at most half the all-gather), "halo",
+    "allgather", or a plan from `exchange_plan` (computed once per model: it
+    costs one row-prologue pass)."""
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     plan = ShardPlan(n_x, world, rank)
     per, x0, x1 = plan.per, plan.x0, plan.x1
+    hp = exchange if isinstance(exchange, HaloPlan) else exchange_plan(backend, plan, group, exchange)
     T = horizon
     vals = torch.zeros((T + 1, per * world), dtype=torch.float64, device=device)
     pol = torch.zeros((T, per * world), dtype=torch.int32, device=device)
@@ -121,7 +192,9 @@ def synthesize_sharded(backend, n_x: int, horizon: int, reach: bool, matrix: boo
         for k in range(T - 1, -1, -1):
             backend.step(tm, x0, x1, vals[k + 1], vals[k, lo:lo + per], pol[k, lo:lo + per],
                          wst[k, lo:lo + per])
-            if dist.is_initialized():  # V exchange: in-place all-gather of the shards (NCCL)
+            if hp is not None:  # V exchange: only the ranges the peers' slabs read (NCCL P2P)
+                _exchange_halo(hp, vals[k], group)
+            elif dist.is_initialized():  # V exchange: in-place all-gather of the shards (NCCL)
                 dist.all_gather_into_tensor(vals[k], vals[k, lo:lo + per].clone() if vals.device.type == "cpu"
                                             else vals[k, lo:lo + per], group=group)
             if k == T - 1 and hasattr(backend, "check"):
@@ -132,6 +205,11 @@ def synthesize_sharded(backend, n_x: int, horizon: int, reach: bool, matrix: boo
             backend.free(tm)
     if timer:
         timer("sweep_end")
+    if hp is not None:  # complete the value table: one all-gather of the shards' columns
+        mine = vals[:T, lo:lo + per].contiguous()
+        full = torch.empty((world * T, per), dtype=mine.dtype, device=mine.device)
+        dist.all_gather_into_tensor(full, mine, group=group)
+        vals[:T] = full.view(world, T, per).permute(1, 0, 2).reshape(T, world * per)
     if dist.is_initialized():
         pol_full = torch.empty_like(pol)
         wst_full = torch.empty_like(wst)

@@ -32,6 +32,23 @@ class OracleBackend:
             t0 = self.om.target_hit(x0 * nuw, x1 * nuw)
         return (o, p, t0)
 
+    def reach(self, x0, x1):
+        """gm_shard_reach restated on the oracle: [min origin, max origin + last slab
+        offset] over the rows the step reads (absorbed states skipped for reach specs)."""
+        st, om = self.om.st, self.om
+        nuw = om.n_u * om.n_w
+        o, _ = om.build_matrix(x0 * nuw, x1 * nuw)
+        if om.reach:
+            live = np.repeat(om.absorbing()[x0:x1] == 0, nuw)
+            o = o[live]
+        if o.size == 0:
+            return x0, x0
+        vec = lambda k: [float(v) for v in st[f"states.{k}"].strip("{}").split(",")]  # noqa: E731
+        counts = [int(np.floor((u - l) / e + 1e-9)) + 1 for l, u, e in zip(vec("lb"), vec("ub"), vec("eta"))]
+        stride = np.cumprod([1] + counts[::-1])[:-1][::-1]
+        span = int(sum((w - 1) * s for w, s in zip(om.extents, stride)))
+        return int(o.min()), min(om.n_x, int(o.max()) + span + 1)
+
     def step(self, tm, x0, x1, v_next, v_out, pol, wst):
         kw = {}
         if tm is not None:
@@ -43,15 +60,17 @@ class OracleBackend:
         wst[:n] = torch.from_numpy(w.astype(np.int32))
 
 
-def _worker(rank, world, port, case, matrix, q):
+def _worker(rank, world, port, case, matrix, q, exchange="auto"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     e = G.manifest()["cases"][case]
     om = O.load(str(G.case_cfg(case)), **G.case_overrides(e))
-    vals, pol, wst = S.synthesize_sharded(OracleBackend(om), om.n_x, om.horizon, om.reach, matrix,
-                                          torch.device("cpu"))
+    be = OracleBackend(om)
+    hp = S.exchange_plan(be, S.ShardPlan(om.n_x, world, rank), None, exchange)
+    vals, pol, wst = S.synthesize_sharded(be, om.n_x, om.horizon, om.reach, matrix, torch.device("cpu"),
+                                          exchange=exchange)
     if rank == 0:
-        q.put((vals.numpy().copy(), pol.numpy().copy(), wst.numpy().copy()))
+        q.put((vals.numpy().copy(), pol.numpy().copy(), wst.numpy().copy(), hp is not None))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -71,7 +90,7 @@ def test_two_rank_sharded_synthesis_is_bit_identical(case, matrix):
     procs = [ctx.Process(target=_worker, args=(r, 2, port, case, matrix, q)) for r in range(2)]
     for p in procs:
         p.start()
-    vals, pol, wst = q.get(timeout=120)
+    vals, pol, wst, _ = q.get(timeout=120)
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
@@ -89,3 +108,46 @@ def test_shard_plan_covers_states_exactly():
             assert covered == n_x
             assert all(p.x0 == min(n_x, r * p.per) for r, p in enumerate(plans))
             assert plans[-1].x1 == n_x or n_x < world
+
+
+def _run(world, case, matrix, exchange):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, matrix, q, exchange)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = q.get(timeout=180)
+    for p in procs:
+        p.join(timeout=180)
+        assert p.exitcode == 0
+    return out
+
+
+@pytest.mark.parametrize("case,matrix,world", [("fixture2d_ra", True, 2), ("ref_vehicle3_desk", False, 3),
+                                               ("exp_dist", True, 2)])
+def test_halo_exchange_is_bit_identical(case, matrix, world):
+    """V exchanged only over the shards' cutoff-bounded halos (point-to-point) gives the
+    reference's results bit for bit, like the per-step all-gather."""
+    vals, pol, wst, used = _run(world, case, matrix, "halo")
+    assert used
+    ref = G.golden_results(case)
+    assert np.array_equal(vals.T.view(np.uint64), np.ascontiguousarray(ref["values"]).view(np.uint64))
+    assert np.array_equal(pol.T.astype(np.uint32), ref["policy"])
+    assert np.array_equal(wst.T.astype(np.uint32), ref["worst"])
+
+
+def test_halo_plan_ranges():
+    plan = [S.ShardPlan(100, 4, r) for r in range(4)]
+    reach = [(0, 30), (20, 55), (45, 80), (70, 100)]  # each shard reads +-5 states around its own
+    hps = [S.halo_plan(p, reach) for p in plan]
+    assert hps[0].sends == [(1, 20, 25)] and hps[0].recvs == [(1, 25, 30)]
+    assert hps[1].sends == [(0, 25, 30), (2, 45, 50)] and hps[1].recvs == [(0, 20, 25), (2, 50, 55)]
+    assert hps[3].recvs == [(2, 70, 75)] and hps[3].sends == [(2, 75, 80)]
+    assert all(h.halo for h in hps) and hps[0].halo_states == 30 and hps[0].allgather_states == 300
+    # every received range is sent by its owner
+    sent = {(r, p.rank, a, b) for p, h in zip(plan, hps) for r, a, b in h.sends}
+    recv = {(p.rank, j, a, b) for p, h in zip(plan, hps) for j, a, b in h.recvs}
+    assert {(d, s_, a, b) for (d, s_, a, b) in sent} == {(r, j, a, b) for (r, j, a, b) in recv}
+    wide = [S.halo_plan(p, [(0, 100)] * 4) for p in plan]
+    assert not any(h.halo for h in wide)  # the all-gather fallback
