@@ -243,6 +243,10 @@ gm_code gm_result_shape(const gm_result* r, int64_t* n_states, int32_t* horizon,
                         int32_t* has_absorbing, int32_t* mode, gm_status* st);
 gm_code gm_result_copy(const gm_result* r, double* values, uint32_t* policy, uint32_t* worst,
                        uint8_t* absorbing, gm_status* st);
+/* The result's own tables (same layouts as gm_result_copy), valid until
+ * gm_result_free: zero-copy access for bindings (absorbing NULL if empty). */
+gm_code gm_result_data(const gm_result* r, const double** values, const uint32_t** policy,
+                       const uint32_t** worst, const uint8_t** absorbing, gm_status* st);
 /* Builds a result from caller tables (e.g. a multi-GPU driver's gathered tables). */
 gm_code gm_result_from_tables(const gm_model* m, const double* values, const uint32_t* policy,
                               const uint32_t* worst, gm_result** out, gm_status* st);

@@ -122,6 +122,7 @@ SIGNATURES = {
     "gm_result_shape": (C.c_int, [_VP, C.POINTER(_I64), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                   C.POINTER(C.c_int32), _PS]),
     "gm_result_copy": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _PS]),
+    "gm_result_data": (C.c_int, [_VP, C.POINTER(_VP), C.POINTER(_VP), C.POINTER(_VP), C.POINTER(_VP), _PS]),
     "gm_result_from_tables": (C.c_int, [_VP, _VP, _VP, _VP, C.POINTER(_VP), _PS]),
     "gm_result_write": (C.c_int, [_VP, C.c_char_p, _PS]),
     "gm_result_free": (None, [_VP]),

@@ -18,6 +18,7 @@
 #include <memory>
 #include <mutex>
 #include <sstream>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -311,15 +312,39 @@ struct gm_matrix {
     bool masked = false;
 };
 
+// Host tables that are filled by copies: resize() leaves the elements
+// uninitialised (no zero pass over hundreds of MB before the device copy).
+template <class T>
+struct NoInitAlloc : std::allocator<T> {
+    using value_type = T;
+    template <class U>
+    struct rebind {
+        using other = NoInitAlloc<U>;
+    };
+    NoInitAlloc() = default;
+    template <class U>
+    NoInitAlloc(const NoInitAlloc<U>&) noexcept {}
+    template <class U>
+    void construct(U* p) noexcept {
+        ::new (static_cast<void*>(p)) U;
+    }
+    template <class U, class... A>
+    void construct(U* p, A&&... a) {
+        ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+    }
+};
+template <class T>
+using HostVec = std::vector<T, NoInitAlloc<T>>;
+
 struct gm_result {
     Model meta; // grids, spec, gamma for the container
     int mode = 0;
     int64_t n_x = 0;
     int T = 0;
-    std::vector<double> values;      // n_x x (T+1), column-major
-    std::vector<uint32_t> policy;    // n_x x T, column-major
-    std::vector<uint32_t> worst;     // n_x x T, column-major
-    std::vector<uint8_t> absorbing;  // n_x (reach) or empty
+    HostVec<double> values;      // n_x x (T+1), column-major
+    HostVec<uint32_t> policy;    // n_x x T, column-major
+    HostVec<uint32_t> worst;     // n_x x T, column-major
+    HostVec<uint8_t> absorbing;  // n_x (reach) or empty
 };
 
 namespace {
@@ -575,50 +600,80 @@ void ensure_t0x(gm_model* m, gm_matrix* tm) {
     tm->has_t0x = true;
 }
 
-// run_backward (synthesis.cpp:165-195) over all states on one device.
+// run_backward (synthesis.cpp:165-195) over all states on one device. The host
+// tables are sized by a helper thread while the device builds and sweeps, and
+// each column goes to the host (aux stream) as soon as its step is done, under
+// the next step's kernels: the result is ready shortly after the last step.
 gm_result* run_backward(gm_model* m, gm_matrix* tm) {
     const int64_t n_x = m->M.n_x();
     const int T = m->M.spec.horizon;
     const bool reach = m->M.spec.reach();
+    const size_t nx = static_cast<size_t>(n_x);
     DevBuf<double> vals;
     DevBuf<uint32_t> pol, wst;
-    vals.ensure(static_cast<size_t>(n_x) * (T + 1), "value table");
-    pol.ensure(static_cast<size_t>(n_x) * T, "policy table");
-    wst.ensure(static_cast<size_t>(n_x) * T, "worst-disturbance table");
-    {
-        std::vector<double> term(static_cast<size_t>(n_x), reach ? 0.0 : 1.0);
-        ck(cudaMemcpy(vals.p + static_cast<size_t>(n_x) * T, term.data(), term.size() * 8, cudaMemcpyHostToDevice),
-           "terminal column");
-    }
-    for (int k = T - 1; k >= 0; --k) {
-        step_states(m, tm, 0, n_x, vals.p + static_cast<size_t>(n_x) * (k + 1), vals.p + static_cast<size_t>(n_x) * k,
-                    pol.p + static_cast<size_t>(n_x) * k, wst.p + static_cast<size_t>(n_x) * k, m->stream);
-        if (k == T - 1) {
-            ck(cudaStreamSynchronize(m->stream), "bellman step");
-            raise_device_error(m);
-        }
-    }
-    ck(cudaStreamSynchronize(m->stream), "bellman sweep");
-    raise_device_error(m);
-    auto* r = new gm_result;
+    vals.ensure(nx * (T + 1), "value table");
+    pol.ensure(nx * T, "policy table");
+    wst.ensure(nx * T, "worst-disturbance table");
+    std::unique_ptr<gm_result> r(new gm_result);
     r->meta = m->M;
     r->mode = tm ? GM_MODE_MATRIX : GM_MODE_OFA;
     r->n_x = n_x;
     r->T = T;
-    r->values.resize(static_cast<size_t>(n_x) * (T + 1));
-    r->policy.resize(static_cast<size_t>(n_x) * T);
-    r->worst.resize(static_cast<size_t>(n_x) * T);
-    ck(cudaMemcpy(r->values.data(), vals.p, r->values.size() * 8, cudaMemcpyDeviceToHost), "values");
-    if (T > 0) {
-        ck(cudaMemcpy(r->policy.data(), pol.p, r->policy.size() * 4, cudaMemcpyDeviceToHost), "policy");
-        ck(cudaMemcpy(r->worst.data(), wst.p, r->worst.size() * 4, cudaMemcpyDeviceToHost), "worst");
+    std::thread sizer([&] {
+        r->values.resize(nx * (T + 1));
+        r->policy.resize(nx * T);
+        r->worst.resize(nx * T);
+        std::fill(r->values.begin() + static_cast<std::ptrdiff_t>(nx) * T, r->values.end(), reach ? 0.0 : 1.0);
+    });
+    struct Joiner {
+        std::thread& t;
+        ~Joiner() {
+            if (t.joinable()) t.join();
+        }
+    } joiner{sizer};
+    {
+        std::vector<double> term(nx, reach ? 0.0 : 1.0);
+        ck(cudaMemcpy(vals.p + nx * T, term.data(), term.size() * 8, cudaMemcpyHostToDevice), "terminal column");
     }
+    ensure_scratch(m, 4096); // the aux stream
+    cudaEvent_t done[2];
+    for (cudaEvent_t& e : done) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "step events");
+    struct EvFree {
+        cudaEvent_t* e;
+        ~EvFree() {
+            cudaEventDestroy(e[0]);
+            cudaEventDestroy(e[1]);
+        }
+    } evfree{done};
+    auto copy_column = [&](int k, cudaEvent_t ready) {
+        if (sizer.joinable()) sizer.join();
+        ck(cudaStreamWaitEvent(m->aux, ready, 0), "column wait");
+        ck(cudaMemcpyAsync(r->values.data() + nx * k, vals.p + nx * k, nx * 8, cudaMemcpyDeviceToHost, m->aux),
+           "values");
+        ck(cudaMemcpyAsync(r->policy.data() + nx * k, pol.p + nx * k, nx * 4, cudaMemcpyDeviceToHost, m->aux),
+           "policy");
+        ck(cudaMemcpyAsync(r->worst.data() + nx * k, wst.p + nx * k, nx * 4, cudaMemcpyDeviceToHost, m->aux), "worst");
+        ck(cudaStreamSynchronize(m->aux), "column copy");
+    };
+    for (int k = T - 1; k >= 0; --k) {
+        step_states(m, tm, 0, n_x, vals.p + nx * (k + 1), vals.p + nx * k, pol.p + nx * k, wst.p + nx * k, m->stream);
+        ck(cudaEventRecord(done[k & 1], m->stream), "step event");
+        if (k == T - 1) {
+            ck(cudaStreamSynchronize(m->stream), "bellman step");
+            raise_device_error(m);
+        } else {
+            copy_column(k + 1, done[(k + 1) & 1]); // step k runs meanwhile
+        }
+    }
+    ck(cudaStreamSynchronize(m->stream), "bellman sweep");
+    raise_device_error(m);
+    if (T > 0) copy_column(0, done[0]);
+    if (sizer.joinable()) sizer.join();
     if (reach) {
-        r->absorbing.resize(static_cast<size_t>(n_x));
-        ck(cudaMemcpy(r->absorbing.data(), m->d_absorb.p, static_cast<size_t>(n_x), cudaMemcpyDeviceToHost),
-           "absorbing");
+        r->absorbing.resize(nx);
+        ck(cudaMemcpy(r->absorbing.data(), m->d_absorb.p, nx, cudaMemcpyDeviceToHost), "absorbing");
     }
-    return r;
+    return r.release();
 }
 
 // ---------------------------------------------------------------- containers
@@ -1358,6 +1413,16 @@ gm_code gm_result_copy(const gm_result* r, double* values, uint32_t* policy, uin
     });
 }
 
+gm_code gm_result_data(const gm_result* r, const double** values, const uint32_t** policy, const uint32_t** worst,
+                       const uint8_t** absorbing, gm_status* st) {
+    return guarded(st, [&] {
+        if (values) *values = r->values.data();
+        if (policy) *policy = r->policy.data();
+        if (worst) *worst = r->worst.data();
+        if (absorbing) *absorbing = r->absorbing.empty() ? nullptr : r->absorbing.data();
+    });
+}
+
 gm_code gm_result_from_tables(const gm_model* m, const double* values, const uint32_t* policy, const uint32_t* worst,
                               gm_result** out, gm_status* st) {
     return guarded(st, [&] {
@@ -1585,7 +1650,7 @@ gm_code gm_result_read(const char* path, gm_result** out, gm_status* st) {
         for (size_t i = 0; i < nx; ++i)
             for (int k = 0; k <= T; ++k)
                 std::memcpy(&r->values[static_cast<size_t>(k) * nx + i], &buf[(i * (T + 1) + k) * 8], 8);
-        for (std::vector<uint32_t>* dst : {&r->policy, &r->worst}) {
+        for (HostVec<uint32_t>* dst : {&r->policy, &r->worst}) {
             get(nx * T * 4);
             dst->resize(nx * T);
             for (size_t i = 0; i < nx; ++i)

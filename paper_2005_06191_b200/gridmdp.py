@@ -504,16 +504,20 @@ class SynthesisResult:
     mode: str
     spec: Spec
     model: SystemModel = field(repr=False)
-    _h: Optional[C.c_void_p] = field(default=None, repr=False)
+    _h: Optional[C.c_void_p] = field(default=None, repr=False)  # built from tables by write()
+    _owner: Optional["_ResultOwner"] = field(default=None, repr=False)  # engine result the arrays view
 
     def __del__(self):
         if getattr(self, "_h", None) and lib is not None:
             lib.gm_result_free(self._h)
             self._h = None
 
+    def _handle(self) -> Optional[C.c_void_p]:
+        return self._owner.h if self._owner is not None else self._h
+
     def write(self, path: str) -> None:
         """write_results (io.cpp:142-179)."""
-        h = self._h
+        h = self._handle()
         if not h:
             h = C.c_void_p()
             v = np.asfortranarray(self.values, dtype=np.float64)
@@ -525,16 +529,47 @@ class SynthesisResult:
         call("gm_result_write", h, str(path).encode())
 
 
+class _ResultOwner:
+    """Owns an engine result; the SynthesisResult arrays are views of its tables and
+    keep it alive (through their ctypes buffers)."""
+
+    def __init__(self, h: C.c_void_p):
+        self.h = h
+
+    def __del__(self):
+        if self.h and lib is not None:
+            lib.gm_result_free(self.h)
+            self.h = None
+
+
+def _table(owner: _ResultOwner, addr: Optional[int], ctype, shape: tuple, dtype) -> np.ndarray:
+    """Column-major (n_x, k) view of an engine table, or an empty array."""
+    n = int(np.prod(shape))
+    if n == 0 or not addr:
+        return np.zeros(shape, dtype=dtype, order="F")
+    buf = (ctype * n).from_address(addr)
+    buf._owner = owner  # the view's base chain keeps the engine result alive
+    a = np.frombuffer(buf, dtype=dtype)
+    return a.reshape(shape[::-1]).T if len(shape) == 2 else a
+
+
+_VPT = C.c_void_p
+
+
 def _result_from_handle(m: SystemModel, spec: Spec, h: C.c_void_p) -> SynthesisResult:
+    """Zero-copy: the returned arrays view the engine result's host tables."""
+    owner = _ResultOwner(h)
     n_x, T, has_abs, mode = C.c_int64(), C.c_int32(), C.c_int32(), C.c_int32()
     call("gm_result_shape", h, C.byref(n_x), C.byref(T), C.byref(has_abs), C.byref(mode))
     nx, t = n_x.value, T.value
-    vals = np.empty((nx, t + 1), dtype=np.float64, order="F")
-    pol = np.empty((nx, t), dtype=np.uint32, order="F")
-    wst = np.empty((nx, t), dtype=np.uint32, order="F")
-    ab = np.zeros(nx if has_abs.value else 0, dtype=np.uint8)
-    call("gm_result_copy", h, ptr(vals), ptr(pol), ptr(wst), ptr(ab) if has_abs.value else None)
-    return SynthesisResult(vals, pol, wst, ab, "ofa" if mode.value == _capi.GM_MODE_OFA else "matrix", spec, m, h)
+    pv, pp, pw, pa = _VPT(), _VPT(), _VPT(), _VPT()
+    call("gm_result_data", h, C.byref(pv), C.byref(pp), C.byref(pw), C.byref(pa))
+    vals = _table(owner, pv.value, C.c_double, (nx, t + 1), np.float64)
+    pol = _table(owner, pp.value, C.c_uint32, (nx, t), np.uint32)
+    wst = _table(owner, pw.value, C.c_uint32, (nx, t), np.uint32)
+    ab = _table(owner, pa.value, C.c_uint8, (nx,), np.uint8) if has_abs.value else np.zeros(0, dtype=np.uint8)
+    mode_s = "ofa" if mode.value == _capi.GM_MODE_OFA else "matrix"
+    return SynthesisResult(vals, pol, wst, ab, mode_s, spec, m, None, owner)
 
 
 def synthesize(m: SystemModel, spec: Optional[Spec] = None, opts: Optional[SynthesisOptions] = None
@@ -616,7 +651,7 @@ def value_at(res: SynthesisResult, x, k: int = 0) -> float:
     """values(point_to_index(state_grid, x), k) (gridmdp_main.cpp:133-134)."""
     x = np.ascontiguousarray(x, dtype=np.float64)
     v = C.c_double()
-    call("gm_result_value_at", res._h, ptr(x), C.c_int32(x.size), C.c_int32(k), C.byref(v))
+    call("gm_result_value_at", res._handle(), ptr(x), C.c_int32(x.size), C.c_int32(k), C.byref(v))
     return v.value
 
 
@@ -660,7 +695,7 @@ def simulate(m: SystemModel, spec: Optional[Spec], res: SynthesisResult, x0, run
     call("gm_model_sim_defaults", m.handle, C.byref(r0), C.byref(s0))
     runs = r0.value if runs is None else int(runs)
     seed = s0.value if seed is None else int(seed)
-    if res._h is None:  # tables built in Python: hand them to the engine
+    if res._handle() is None:  # tables built in Python: hand them to the engine
         h0 = C.c_void_p()
         v = np.asfortranarray(res.values, dtype=np.float64)
         p = np.asfortranarray(res.policy, dtype=np.uint32)
@@ -670,7 +705,7 @@ def simulate(m: SystemModel, spec: Optional[Spec], res: SynthesisResult, x0, run
         res._h = h0
     x = np.ascontiguousarray(x0, dtype=np.float64)
     h = C.c_void_p()
-    call("gm_simulate", m.handle, res._h, ptr(x), C.c_int32(x.size), C.c_int32(runs), C.c_uint64(seed),
+    call("gm_simulate", m.handle, res._handle(), ptr(x), C.c_int32(x.size), C.c_int32(runs), C.c_uint64(seed),
          C.c_int32(1 if dmode != "random" else 0), C.c_int32(1 if trajectories else 0), C.byref(h))
     n_runs, sat_n, rate = C.c_int32(), C.c_int64(), C.c_double()
     call("gm_sim_summary", h, C.byref(n_runs), C.byref(sat_n), C.byref(rate))
