@@ -80,3 +80,38 @@ def test_jit_auto_policy_small_launch_uses_interpreter(monkeypatch):
     g.build_matrix(m)
     used, _, why = jit_status(m)
     assert used == 0 and "2^21" in why
+
+
+_PROBE = r"""
+import ctypes as C, hashlib, sys
+sys.path.insert(0, {repo!r}); sys.path.insert(0, {tests!r})
+import golden_io as G
+from paper_2005_06191_b200 import _capi, gridmdp as g
+e = G.manifest()["cases"]["chain09"]
+m = g.load_config(str(G.case_cfg("chain09")), **G.case_overrides(e))
+tm = g.build_matrix(m)
+s = C.c_double(); why = C.create_string_buffer(512)
+used = _capi.lib.gm_model_jit_status(m.handle, C.byref(s), why, 512)
+print(used, s.value, hashlib.sha256(tm.payload().tobytes()).hexdigest())
+"""
+
+
+def test_jit_disk_cache_reuses_compiled_kernels(tmp_path):
+    """Compiled dynamics are cached on disk (GM_JIT_CACHE): a second process loads the
+    cubin instead of recompiling and builds the same rows."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    tests = Path(__file__).resolve().parent
+    code = _PROBE.format(repo=str(tests.parent), tests=str(tests))
+    env = dict(os.environ, GM_JIT="1", GM_JIT_CACHE=str(tmp_path / "jit"))
+    runs = []
+    for _ in range(2):
+        out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, check=True)
+        used, secs, digest = out.stdout.split()
+        runs.append((int(used), float(secs), digest))
+    assert runs[0][0] == 1 and runs[1][0] == 1
+    assert list((tmp_path / "jit").glob("*.jit"))
+    assert runs[1][1] < 0.5 * runs[0][1], runs  # loaded, not recompiled
+    assert runs[0][2] == runs[1][2]
