@@ -1276,7 +1276,8 @@ void expect_matrix(const GmDev& D, long long row0, long long r_lo, long long r_h
         const int flags = div32 | ((cg && std::atoi(cg)) ? 2 : 0);
         // loads in flight per lane (U) and residency (MINB, the register cap): default
         // U = 12 at 6 CTAs/SM (C2b 16.3 ms); GM_ET_VARIANT=1 (8, 6) 17.1 ms, 2 (16, 4)
-        // 17.7 ms, 3 (10, 6) 17.3 ms, 4 (14, 6) 17.3 ms; (8, 8) 21.4, (16, 3) 19.2, (12, 7) 18.2
+        // 17.7 ms, 3 (10, 6) 17.3 ms, 4 (14, 6) 17.3 ms; (8, 8) 21.4, (16, 3) 19.2, (12, 7) 18.2,
+        // (12, 5) equal (17.4 vs 17.4 at 1.5 GHz), (20, 4) 20.4
         static const char* ev = std::getenv("GM_ET_VARIANT");
         const int var = ev ? std::atoi(ev) : 0;
 #define GM_ET1(T, UU, MB)                                                                                   \
