@@ -361,7 +361,9 @@ def main():
         for _ in range(args.warmup):
             e2e_step()
         e2e = []
+        m3 = None
         for _ in range(args.steps):
+            m3 = None  # the previous step's model is torn down outside the timed region
             torch.cuda.synchronize()
             if dist.is_initialized():
                 dist.barrier()
