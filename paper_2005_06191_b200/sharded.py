@@ -203,13 +203,13 @@ def synthesize_sharded(backend, n_x: int, horizon: int, reach: bool, matrix: boo
     finally:
         if matrix and hasattr(backend, "free"):
             backend.free(tm)
-    if timer:
-        timer("sweep_end")
     if hp is not None:  # complete the value table: one all-gather of the shards' columns
         mine = vals[:T, lo:lo + per].contiguous()
         full = torch.empty((world * T, per), dtype=mine.dtype, device=mine.device)
         dist.all_gather_into_tensor(full, mine, group=group)
         vals[:T] = full.view(world, T, per).permute(1, 0, 2).reshape(T, world * per)
+    if timer:
+        timer("sweep_end")
     if dist.is_initialized():
         pol_full = torch.empty_like(pol)
         wst_full = torch.empty_like(wst)
