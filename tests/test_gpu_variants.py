@@ -1,0 +1,70 @@
+"""Every alternative kernel behind an environment knob keeps the
+canonical reduction order and product association, so it must reproduce the
+default path bit for bit: the per-term slab-walk matrix kernel (the automatic
+fallback for rows too wide for the offset table), the single-role build (the
+fallback when the pipelined build's buffers do not fit), the offset-table
+residency variants, the OFA in-flight variants, contiguous row schedules, other
+build residencies and row pitches, and the compiled dynamics at small sizes.
+The knobs are read once per process, so each setting runs in a subprocess."""
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+TESTS = Path(__file__).resolve().parent
+CASES = ["fixture2d_ra", "ref_vehicle3_desk", "exp_dist"]
+
+_PROBE = r"""
+import hashlib, sys
+sys.path.insert(0, {repo!r}); sys.path.insert(0, {tests!r})
+import numpy as np
+import golden_io as G
+from paper_2005_06191_b200 import gridmdp as g
+for case in {cases!r}:
+    e = G.manifest()["cases"][case]
+    h = hashlib.sha256()
+    m = g.load_config(str(G.case_cfg(case)), **G.case_overrides(e))
+    tm = g.build_matrix(m)
+    h.update(tm.origins().tobytes()); h.update(tm.payload().tobytes())
+    for mode in ("matrix", "ofa"):
+        r = g.synthesize(m, m.spec, g.SynthesisOptions(mode=mode))
+        h.update(np.ascontiguousarray(r.values).tobytes()); h.update(np.ascontiguousarray(r.policy).tobytes())
+        h.update(np.ascontiguousarray(r.worst_dist).tobytes())
+    print(case, h.hexdigest())
+"""
+
+SETTINGS = [
+    {"GM_MATRIX_KERNEL": "walk"},
+    {"GM_BUILD_WS": "0"},
+    {"GM_ET_VARIANT": "2", "GM_OFA_U": "4", "GM_CONTIG": "1"},
+    {"GM_BUILD_CTAS": "5", "GM_OFA_U": "8"},
+    {"GM_JIT": "1"},
+]
+
+
+def digests(env_extra):
+    code = _PROBE.format(repo=str(TESTS.parent), tests=str(TESTS), cases=CASES)
+    env = dict(os.environ, **env_extra)
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    return dict(line.split() for line in out.stdout.strip().splitlines())
+
+
+@pytest.fixture(scope="module")
+def default():
+    return digests({"GM_JIT": "0"})
+
+
+@pytest.mark.parametrize("knob", SETTINGS, ids=lambda d: ",".join(f"{k}={v}" for k, v in d.items()))
+def test_variant_bit_identical_to_default(default, knob):
+    env = {"GM_JIT": "0", **knob}
+    assert digests(env) == default
+
+
+def test_row_pitch_does_not_change_results(default):
+    """Rows padded to another granule (GM_PITCH_GRANULE) change the layout only."""
+    got = digests({"GM_JIT": "0", "GM_PITCH_GRANULE": "1"})
+    assert got == default
