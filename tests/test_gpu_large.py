@@ -3,9 +3,9 @@ oracle on sampled rows/states, plus size-independent properties:
 
   * C2b (108 GB stored matrix): sampled rows' origins bit-exact, probabilities
     within 1e-9 rel + 1e-15 abs, row sums <= 1 + 1e-9;
-  * C5 (BMW 320i, 7-d, OFA): one Bellman step from a seeded random V on a
-    sampled state range equals the oracle's (values within tolerance, policy
-    equal except on ties);
+  * C5 (BMW 320i, 7-d, OFA) and the traffic rings C4 / C4' (7-d / 5-d, OFA):
+    one Bellman step from a seeded random V on a sampled state range equals the
+    oracle's (values within tolerance, policy equal except on ties);
   * sharding invariance: stepping the state space as 1, 2, 3 or 8 shards gives
     bit-identical V, policies and worst disturbances (the property multi-GPU
     runs rely on);
@@ -57,6 +57,24 @@ def test_c5_bmw_step_matches_oracle_on_sampled_states():
     v_out, pol, wst = g.bellman_step(m, m.spec, None, None, v)
     q = g.q_values(m)
     x0, x1 = 60000, 62000
+    vo, po, wo, _ = om.bellman_step(v, x0, x1)
+    assert G.tol_ok(v_out[x0:x1], vo).all(), np.abs(v_out[x0:x1] - vo).max()
+    ok, n = G.policy_ok(q[x0:x1], pol[x0:x1], po)
+    assert ok, n
+
+
+@pytest.mark.parametrize("wl,x0", [("C4", 2391000), ("C4p", 8605000)])
+def test_traffic_ofa_step_matches_oracle_on_sampled_states(wl, x0):
+    """BASELINE's sharded traffic workloads at full size (C4: 7 cells, R = 78,125;
+    C4': traffic5, R = 16,807): one OFA Bellman step from a seeded random V on a
+    sampled state range equals the oracle's."""
+    text = W.WORKLOADS[wl]()
+    m = g.parse_config(text, wl)
+    om = O.load(text)
+    v = np.random.default_rng(20240).uniform(0, 1, m.n_states)
+    v_out, pol, wst = g.bellman_step(m, m.spec, None, None, v)
+    q = g.q_values(m)
+    x1 = x0 + 96
     vo, po, wo, _ = om.bellman_step(v, x0, x1)
     assert G.tol_ok(v_out[x0:x1], vo).all(), np.abs(v_out[x0:x1] - vo).max()
     ok, n = G.policy_ok(q[x0:x1], pol[x0:x1], po)
