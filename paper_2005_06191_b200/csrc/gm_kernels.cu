@@ -545,6 +545,95 @@ __global__ void __launch_bounds__(kThreads, MINB) k_expect_matrix_et(GmDev D, lo
     }
 }
 
+// One row's lane-strided partial sum of k_expect_matrix_et (canonical order: terms
+// t = lane, lane+TPR, ... with fma in increasing t; the zero-padded tail adds +0).
+template <int TPR, int U>
+__device__ __forceinline__ double et_row_partial(const double* __restrict__ pr, const double* vb, const int* e,
+                                                 int n_full, int rem) {
+    double s = 0.0;
+    for (int b = 0; b < n_full; b += U) {
+        double p[U], v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            p[u] = __ldcs(pr + u * TPR);
+            v[u] = ldg_at(vb, e[u * TPR]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) s = fma(p[u], v[u], s);
+        pr += U * TPR;
+        e += U * TPR;
+    }
+    if (rem) {
+        double p[U], v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            p[u] = 0.0;
+            v[u] = 0.0;
+            if (u < rem) {
+                p[u] = __ldcs(pr + u * TPR);
+                v[u] = ldg_at(vb, e[u * TPR]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) s = fma(p[u], v[u], s);
+    }
+    return s;
+}
+
+// k_expect_matrix_et for TPR = 32 with two consecutive rows per warp: each row's
+// partial sums are the one-row kernel's, and one transposed butterfly reduces
+// both (level 16 sends the other half's row: lanes 0-15 continue with row A,
+// 16-31 with row B, so lane 0 / lane 16 end with exactly the canonical lane-0
+// sums of A / B, a + b == b + a in IEEE). Halves the reduction and the per-row
+// schedule overhead.
+template <int U, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_expect_matrix_et2(GmDev D, long long row0, long long r_lo,
+                                                               long long r_hi, GmFastDiv div_nuw, int flags,
+                                                               const double* __restrict__ probs,
+                                                               const long long* __restrict__ origins,
+                                                               const double* __restrict__ t0x,
+                                                               const double* __restrict__ V,
+                                                               double* __restrict__ v_in) {
+    constexpr int W = kThreads / 32;
+    const int R = static_cast<int>(D.R);
+    int* E = reinterpret_cast<int*>(g_sm + kThreads / 32);
+    for (int t = threadIdx.x; t < R; t += kThreads) {
+        const int L = D.div_Wl.div(t);
+        E[t] = D.line_off[L] + (t - L * D.Wl);
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool reach = D.spec_kind != GM_SPEC_SAFETY;
+    const long long nrows = r_hi - r_lo, npairs = (nrows + 1) / 2;
+    const long long nuw = D.n_u * D.n_w;
+    const int n_it = lane < R ? (R - lane + 31) / 32 : 0;
+    const int n_full = n_it - n_it % U, rem = n_it - n_full;
+    auto absorbed = [&](long long r) {
+        const long long row = row0 + r;
+        return D.absorb[(flags & 1) ? static_cast<long long>(div_nuw.div(static_cast<int>(row))) : row / nuw] != 0;
+    };
+    for (long long pi = static_cast<long long>(blockIdx.x) * W + warp; pi < npairs;
+         pi += static_cast<long long>(gridDim.x) * W) {
+        const long long rlA = 2 * pi, rlB = rlA + 1;
+        const bool hasB = rlB < nrows;
+        const long long rA = r_lo + rlA, rB = rA + 1;
+        bool skA = false, skB = !hasB;
+        if (reach && D.absorb != nullptr) {
+            skA = absorbed(rA);
+            if (hasB) skB = absorbed(rB);
+        }
+        const double sA = skA ? 0.0
+                              : et_row_partial<32, U>(probs + rA * D.pitch + lane, V + origins[rA], E + lane, n_full, rem);
+        const double sB = skB ? 0.0
+                              : et_row_partial<32, U>(probs + rB * D.pitch + lane, V + origins[rB], E + lane, n_full, rem);
+        const bool hi = lane >= 16;
+        double s = (hi ? sB : sA) + __shfl_xor_sync(0xffffffffu, hi ? sA : sB, 16);
+        for (int off = 8; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0) v_in[rlA] = skA ? 0.0 : (reach ? s + t0x[rA] : s);
+        if (lane == 16 && hasB) v_in[rlB] = skB ? 0.0 : (reach ? s + t0x[rB] : s);
+    }
+}
+
 // min over w (strict <, ascending), then max over u (strict >, ascending):
 // lowest-index ties (synthesis.cpp:112-142). L lanes per state.
 template <int L>
@@ -1296,6 +1385,17 @@ void expect_matrix(const GmDev& D, long long row0, long long r_lo, long long r_h
         if (var == 3) GM_ET1(T, 10, 6)                                                                      \
         if (var == 4) GM_ET1(T, 14, 6)                                                                      \
         GM_ET1(T, 12, 6)
+        // TPR = 32 (R in [512, 1024)): two rows per warp by default (C2b step 17.5 -> 16.9 ms
+        // on a 1.45-1.5 GHz capped box); GM_ET_VARIANT=5 = the one-row kernel
+        if (D.tpr == 32 && var == 0) {
+            auto k = k_expect_matrix_et2<12, 6>;
+            allow_smem(k, et_smem);
+            const long long pairs = (r_hi - r_lo + 1) / 2;
+            k<<<resident_grid(k, et_smem, (pairs + kThreads / 32 - 1) / (kThreads / 32)), kThreads, et_smem, s>>>(
+                D, row0, r_lo, r_hi, dn, flags, probs, origins, t0x, V, v_in);
+            check_launch("expect_matrix");
+            return;
+        }
         switch (D.tpr) {
             GM_ET(1) GM_ET(2) GM_ET(4) GM_ET(8) GM_ET(16) GM_ET(32) GM_ET(64) GM_ET(128)
         default: break;

@@ -34,12 +34,30 @@ for case in {cases!r}:
         h.update(np.ascontiguousarray(r.values).tobytes()); h.update(np.ascontiguousarray(r.policy).tobytes())
         h.update(np.ascontiguousarray(r.worst_dist).tobytes())
     print(case, h.hexdigest())
+# R = 729 rows (a warp per row in the stored-matrix sweep): vehicle3 at eta/4 on a
+# 2 x 2 x 3 m corner of its grid
+from paper_2005_06191_b200 import workloads as W
+text = W.vehicle3(eta=(0.125, 0.125, 0.0625), T=3)
+for a, b in (("states.ub = {{10.0, 10.0, 3.5}};", "states.ub = {{2.0, 2.0, 1.5}};"),
+             ("target.lb = {{8.0, 0.0, -3.5}};", "target.lb = {{1.5, 0.0, -3.5}};"),
+             ("target.ub = {{10.0, 2.0, 3.5}};", "target.ub = {{2.0, 0.5, 1.5}};"),
+             ("avoid.lb = {{4.0, 4.0, -3.5}};", "avoid.lb = {{0.75, 0.75, -3.5}};"),
+             ("avoid.ub = {{6.0, 6.0, 3.5}};", "avoid.ub = {{1.25, 1.25, 1.5}};")):
+    assert a in text
+    text = text.replace(a, b)
+m = g.parse_config(text, "vehicle_r729")
+assert m.sizes().row_width == 729
+h = hashlib.sha256()
+r = g.synthesize(m)
+h.update(np.ascontiguousarray(r.values).tobytes()); h.update(np.ascontiguousarray(r.policy).tobytes())
+print("vehicle_r729", h.hexdigest())
 """
 
 SETTINGS = [
     {"GM_MATRIX_KERNEL": "walk"},
     {"GM_BUILD_WS": "0"},
     {"GM_ET_VARIANT": "2", "GM_OFA_U": "4", "GM_CONTIG": "1"},
+    {"GM_ET_VARIANT": "5"},  # one row per warp at TPR = 32 (default: two)
     {"GM_BUILD_CTAS": "5", "GM_OFA_U": "8"},
     {"GM_JIT": "1"},
 ]
