@@ -13,6 +13,7 @@
 #include <charconv>
 #include <climits>
 #include <cstring>
+#include <exception>
 #include <fstream>
 #include <map>
 #include <memory>
@@ -619,11 +620,16 @@ gm_result* run_backward(gm_model* m, gm_matrix* tm) {
     r->mode = tm ? GM_MODE_MATRIX : GM_MODE_OFA;
     r->n_x = n_x;
     r->T = T;
+    std::exception_ptr sizer_err; // e.g. std::bad_alloc: rethrown on this thread after the join
     std::thread sizer([&] {
-        r->values.resize(nx * (T + 1));
-        r->policy.resize(nx * T);
-        r->worst.resize(nx * T);
-        std::fill(r->values.begin() + static_cast<std::ptrdiff_t>(nx) * T, r->values.end(), reach ? 0.0 : 1.0);
+        try {
+            r->values.resize(nx * (T + 1));
+            r->policy.resize(nx * T);
+            r->worst.resize(nx * T);
+            std::fill(r->values.begin() + static_cast<std::ptrdiff_t>(nx) * T, r->values.end(), reach ? 0.0 : 1.0);
+        } catch (...) {
+            sizer_err = std::current_exception();
+        }
     });
     struct Joiner {
         std::thread& t;
@@ -645,8 +651,12 @@ gm_result* run_backward(gm_model* m, gm_matrix* tm) {
             cudaEventDestroy(e[1]);
         }
     } evfree{done};
-    auto copy_column = [&](int k, cudaEvent_t ready) {
+    auto join_sizer = [&] {
         if (sizer.joinable()) sizer.join();
+        if (sizer_err) std::rethrow_exception(sizer_err);
+    };
+    auto copy_column = [&](int k, cudaEvent_t ready) {
+        join_sizer();
         ck(cudaStreamWaitEvent(m->aux, ready, 0), "column wait");
         ck(cudaMemcpyAsync(r->values.data() + nx * k, vals.p + nx * k, nx * 8, cudaMemcpyDeviceToHost, m->aux),
            "values");
@@ -668,7 +678,7 @@ gm_result* run_backward(gm_model* m, gm_matrix* tm) {
     ck(cudaStreamSynchronize(m->stream), "bellman sweep");
     raise_device_error(m);
     if (T > 0) copy_column(0, done[0]);
-    if (sizer.joinable()) sizer.join();
+    join_sizer();
     if (reach) {
         r->absorbing.resize(nx);
         ck(cudaMemcpy(r->absorbing.data(), m->d_absorb.p, nx, cudaMemcpyDeviceToHost), "absorbing");
