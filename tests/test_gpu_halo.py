@@ -37,3 +37,21 @@ def test_shard_reach_matches_stored_origins(case):
             o = org[p.x0 * nuw:p.x1 * nuw][np.repeat(absorbed[p.x0:p.x1] == 0, nuw)]
             want = (p.x0, p.x0) if o.size == 0 else (int(o.min()), min(n_x, int(o.max()) + span + 1))
             assert got == want, (case, world, r)
+
+
+def test_shard_reach_edge_cases():
+    """Custom densities read the whole grid (conservative); a shard whose states are
+    all absorbed reads nothing; an empty shard reads nothing."""
+    e = MAN["cases"]["custom_tri1d"]
+    m = g.load_config(str(G.case_cfg("custom_tri1d")), **G.case_overrides(e))
+    n_x = int(m.sizes().n_states)
+    assert S.DeviceBackend(m).reach(0, n_x) == (0, n_x)
+    e = MAN["cases"]["fixture2d_ra"]
+    m = g.load_config(str(G.case_cfg("fixture2d_ra")), **G.case_overrides(e))
+    ab = g.absorbing_states(m, m.spec)
+    be = S.DeviceBackend(m)
+    runs = np.flatnonzero(ab)
+    assert runs.size
+    x = int(runs[0])
+    assert be.reach(x, x + 1) == (x, x)  # one absorbed state: its rows are skipped
+    assert be.reach(5, 5) == (5, 5)

@@ -151,3 +151,5 @@ def test_halo_plan_ranges():
     assert {(d, s_, a, b) for (d, s_, a, b) in sent} == {(r, j, a, b) for (r, j, a, b) in recv}
     wide = [S.halo_plan(p, [(0, 100)] * 4) for p in plan]
     assert not any(h.halo for h in wide)  # the all-gather fallback
+    empty = [S.halo_plan(p, [(p2.x0, p2.x0) for p2 in plan]) for p in plan]  # every shard absorbed
+    assert all(h.halo and not h.sends and not h.recvs and h.halo_states == 0 for h in empty)
