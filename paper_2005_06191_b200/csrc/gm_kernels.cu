@@ -1236,7 +1236,7 @@ void build(const GmDev& D, long long row0, long long nrows, long long* origin_ou
         // two table buffers + two prologue buffers (pro_doubles: <= (5n + 2) rb + 2 for both)
         const size_t per_d = 2 * (mw + D.P_size) + 5 * static_cast<size_t>(D.n) + 2;
         static const char* bc = std::getenv("GM_BUILD_CTAS"); // resident CTAs per SM (tuning; AOT kernels)
-        const int ctas = bc ? std::max(2, std::min(6, std::atoi(bc))) : 3; // 3: 2-4 % faster than 4 on C2b
+        const int ctas = bc ? std::max(2, std::min(6, std::atoi(bc))) : 3; // C2b: 3 beats 4 by 2-4 %, 2 is 19 % slower
         const size_t budget_d = (216 / ctas) * 1024 / sizeof(double);
         if (fixed_d < budget_d) {
             long long rb = std::min<long long>(64, static_cast<long long>((budget_d - fixed_d) / per_d));
