@@ -301,7 +301,11 @@ def main():
         ab = g.absorbing_states(m, m.spec)[plan.x0:plan.x1]
         live_rows = int((ab == 0).sum()) * nuw
     dom_bytes = live_rows * (R * 8 + 8 + (8 if reach else 0))
-    roofline = {"kernel": dom, "bound": "hbm", "achieved": dom_bytes / (dom_ms / 1e3) / 1e9, "peak": hbm,
+    tpr = 1  # threads per row (tpr_for_width, gm_host.cpp): a power of two ~R/16 in [1, 128]
+    while tpr * 2 <= R // 16 and tpr < 128:
+        tpr *= 2
+    kname = ("k_expect_matrix_et2" if tpr == 32 else "k_expect_matrix_et") if matrix else "k_expect_ofa"
+    roofline = {"kernel": kname, "family": dom, "bound": "hbm", "achieved": dom_bytes / (dom_ms / 1e3) / 1e9, "peak": hbm,
                 "peak_kind": peak_kind, "unit": "GB/s", "traffic": ncu_traffic(dom, args.workload),
                 "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_ms": dom_ms, "launches": fam_n[dom]}
     roofline["frac"] = roofline["achieved"] / hbm
