@@ -394,32 +394,47 @@ def main():
                 "seconds": time.perf_counter() - t,
                 "d2h_bytes": int(res.values.nbytes + res.policy.nbytes + res.worst_dist.nbytes + res.absorbing.nbytes)}
 
-    # extra OFA workloads (north-star BMW C5): sweep time only, one run after one warm run
-    if rank == 0 and world == 1 and args.extra:
+    # extra OFA workloads (north-star BMW C5): sweep time only, one run after one warm
+    # run; under torchrun the states are sharded over the N ranks like the main
+    # workload (same V exchange policy) and the time is the max over ranks
+    if args.extra:
         extra = {}
         for wname in [w for w in args.extra.split(",") if w]:
             mt = g.parse_config(W.WORKLOADS[wname](), wname)
             st = mt.sizes()
+            nxt = int(st.n_states)
             bet = S.DeviceBackend(mt, stream)
-            S.synthesize_sharded(bet, int(st.n_states), int(st.horizon), mt.spec.is_reach(), False, dev)
+            xp = S.exchange_plan(bet, S.ShardPlan(nxt, world, rank), None, args.exchange) if world > 1 else None
+            ex = xp if xp is not None else "allgather"
+            S.synthesize_sharded(bet, nxt, int(st.horizon), mt.spec.is_reach(), False, dev, exchange=ex)
+            torch.cuda.synchronize()
+            if dist.is_initialized():
+                dist.barrier()
             lib.gm_reset_kernel_stats()
             lib.gm_enable_kernel_timing(1)
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            S.synthesize_sharded(bet, int(st.n_states), int(st.horizon), mt.spec.is_reach(), False, dev)
+            S.synthesize_sharded(bet, nxt, int(st.horizon), mt.spec.is_reach(), False, dev, exchange=ex)
             b.record(stream)
             torch.cuda.synchronize()
             lib.gm_enable_kernel_timing(0)
-            ms = a.elapsed_time(b)
+            tms = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+            if dist.is_initialized():
+                dist.all_reduce(tms, op=dist.ReduceOp.MAX)
+            ms = float(tms.item())
             terms = int(st.rows) * int(st.row_width) * int(st.horizon)
             ofa_ms = lib.gm_kernel_ms_total(_capi.KF_EXPECT_OFA)
-            extra[wname] = {"sweep_s": ms / 1e3, "terms_per_s": terms / (ms / 1e3),
-                            "hbm_equiv_frac": terms * 8 / (ms / 1e3) / 1e9 / hbm,
+            extra[wname] = {"sweep_s": ms / 1e3, "terms_per_s": terms / (ms / 1e3), "n_gpus": world,
+                            "hbm_equiv_frac": terms * 8 / (ms / 1e3) / 1e9 / (hbm * world),
                             "kernel_ms": {n: lib.gm_kernel_ms_total(i) for i, n in enumerate(_capi.KF_NAMES)
-                                          if lib.gm_kernel_ms_total(i)},
-                            "expect_ofa_terms_per_s": terms / (ofa_ms / 1e3) if ofa_ms else None,
+                                          if lib.gm_kernel_ms_total(i)},  # rank 0
+                            "expect_ofa_terms_per_s": (terms / world) / (ofa_ms / 1e3) if ofa_ms else None,
+                            "v_exchange": ("none" if world == 1 else
+                                           f"halo p2p ({xp.halo_states} of {xp.allgather_states} states)"
+                                           if xp is not None else "all-gather per step"),
                             "rows": int(st.rows), "row_width": int(st.row_width), "horizon": int(st.horizon)}
+            bet.release()
         line["extra"] = extra
 
     if rank == 0 and world == 1 and not args.no_cpu and value:
