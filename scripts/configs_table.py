@@ -53,6 +53,16 @@ def ref_synthesize(text, threads):
         return float(out.split("time_synthesize_s:")[1].split()[0])
 
 
+def live_fraction(text):
+    """Share of rows the sweep reads: all but the absorbed states' rows (reach specs),
+    from the CPU oracle's absorbing flags."""
+    from oracle import oracle_py as O
+    om = O.load(text)
+    if not om.reach:
+        return 1.0
+    return float((om.absorbing() == 0).mean())
+
+
 def fp64_peak():
     exe = REPO / "scripts" / "_fp64_peak"
     if not exe.exists():
@@ -129,10 +139,11 @@ def main():
         mode = "matrix" if "exec.mode = matrix;" in text else "ofa"
         terms = rows_n * R * T
         tps = terms / sweep_s
+        live = live_fraction(text)  # rows of absorbed states are never read (synthesis.cpp:86-89)
         rec = {"workload": name, "mode": mode, "states": nx, "rows": rows_n, "R": R, "T": T,
                "gpu_build_s": build_s, "gpu_sweep_s": sweep_s, "gpu_total_s": build_s + sweep_s,
-               "terms_per_s": tps, "hbm_equiv_frac": tps * 8 / 1e9 / hbm,
-               "fp64_util": 2 * tps / (f64 * 1e12), "kernel_ms": fam}
+               "terms_per_s": tps, "live_fraction": live, "hbm_equiv_frac": tps * live * 8 / 1e9 / hbm,
+               "fp64_util": 2 * tps * live / (f64 * 1e12), "kernel_ms": fam}
         if mode == "matrix" and build_s > 0:
             rec["build_probs_per_s"] = rows_n * R / build_s
         if not a.no_cpu and REF_BIN.exists():
@@ -172,8 +183,9 @@ def main():
             f"`python scripts/configs_table.py --out {a.out}`. HBM = {hbm} GB/s ({peak_kind}); FP64 DFMA peak "
             f"{f64:.2f} TFLOP/s measured by scripts/fp64_peak.cu on the same box. GPU: one full synthesis after a "
             "warm-up run of the same model (T = 1 for C4/C4p), CUDA events on the engine's stream (build = stage i of matrix mode; sweep = the T "
-            "Bellman steps; OFA has no build). G terms/s = rows·R·T / sweep; HBM-equiv = 8 B per term against "
-            "HBM (the bytes matrix mode would stream); FP64 util = 2 flops per term against the DFMA peak. "
+            "Bellman steps; OFA has no build). G terms/s = rows·R·T / sweep; HBM-equiv = 8 B per term of the "
+            "rows the sweep reads (absorbed states' rows excluded) against HBM (the bytes matrix mode streams); "
+            "FP64 util = 2 flops per such term against the DFMA peak. "
             "CPU: the reference compiled from its sources (oracle/_ref), all host threads.\n\n" + table
             + "\n```\n" + "\n".join(json.dumps(r) for r in recs) + "\n```\n")
 
