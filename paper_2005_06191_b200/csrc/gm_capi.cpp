@@ -97,7 +97,7 @@ void ck(cudaError_t e, const char* what) {
 // reused by the next allocation of a similar size on the same device, so
 // repeated synthesize/build calls do not pay cudaMalloc/cudaFree of the matrix
 // (hundreds of ms at 100 GB). On allocation failure the cache is flushed first.
-constexpr size_t kCacheMin = 64ULL << 20;
+constexpr size_t kCacheMin = 1ULL << 20; // smaller blocks: cudaMalloc/cudaFree (cudaFree synchronises the device)
 std::mutex g_cache_mu;
 std::multimap<size_t, std::pair<int, void*>> g_cache; // bytes -> (device, ptr)
 

@@ -35,12 +35,14 @@ def main():
         text = g.benchmark_chain_config(n)
         m = g.parse_config(text)
         s = m.sizes()
-        g.synthesize(m)  # warm-up (device buffers, first launches)
-        reps = 3
-        t = time.perf_counter()
-        for _ in range(reps):
+        for _ in range(2):  # warm-up (device buffers, first launches, clocks)
             g.synthesize(m)
-        gpu_s = (time.perf_counter() - t) / reps
+        times = []
+        for _ in range(7):
+            t = time.perf_counter()
+            g.synthesize(m)
+            times.append(time.perf_counter() - t)
+        gpu_s = sorted(times)[len(times) // 2]  # median: ms-scale calls see host jitter
         cpu_s, th = None, os.cpu_count()
         if REF_BIN.exists():
             with tempfile.TemporaryDirectory() as d:
@@ -56,7 +58,7 @@ def main():
     text = "\n".join(rows) + "\n"
     if a.out:
         Path(a.out).write_text("# Table-3 family (benchmark_chain_config), one B200 vs the reference on the host CPU\n\n"
-                               "Wall-clock per `gridmdp.synthesize` call (mean of 3 after a warm-up), matrix mode,\n"
+                               "Wall-clock per `gridmdp.synthesize` call (median of 7 after two warm-up calls), matrix mode,\n"
                                "host tables included; the reference's `time_synthesize_s` with all host threads.\n\n"
                                + text)
 
