@@ -1387,6 +1387,7 @@ void expect_matrix(const GmDev& D, long long row0, long long r_lo, long long r_h
         GM_ET1(T, 12, 6)
         // TPR = 32 (R in [512, 1024)): two rows per warp by default (C2b step 17.5 -> 16.9 ms
         // on a 1.45-1.5 GHz capped box); GM_ET_VARIANT=5 = the one-row kernel
+        // (et2 at (14, 6) 17.3 ms, (12, 7) 17.2, (8, 8) 17.1 vs (12, 6) 16.8)
         if (D.tpr == 32 && var == 0) {
             auto k = k_expect_matrix_et2<12, 6>;
             allow_smem(k, et_smem);
