@@ -206,10 +206,14 @@ __device__ __forceinline__ double ldg_at(const double* vb, int off) {
 // MODE 0: stored row; MODE 1: recompute from Q; MODE 2: recompute from P.
 // Term sources: stored row `prow` (global); Q row at g_sm[qo]; P row at g_sm[po];
 // masses mm at g_sm[mmo], ml at g_sm[mlo]; line table `lines` (smem ints or global).
-template <int MODE, int U, bool LS>
+// LS: line offsets from the global table (0), from the table staged in shared
+// memory (1), or (MODE 2 only) from a shared table of the leading-prefix offsets
+// plus j * (stride of the middle axis) (2): line_off[a*Wm + j] == pre[a] + j*sM.
+template <int MODE, int U, int LS>
 __device__ __forceinline__ double row_dot(const GmDev& D, int lane, int tpr, const double* __restrict__ prow,
                                           int qo, int po, int mmo, int mlo, const double* __restrict__ vb,
-                                          const int* __restrict__ gl, int lo) {
+                                          const int* __restrict__ gl, int lo, int sM = 0) {
+    static_assert(LS != 2 || MODE == 2, "prefix offset table needs the (a, j, k) walk");
     const int R = static_cast<int>(D.R);
     const int n_it = lane < R ? (R - lane + tpr - 1) / tpr : 0;
     Walk w;
@@ -223,7 +227,7 @@ __device__ __forceinline__ double row_dot(const GmDev& D, int lane, int tpr, con
         else if (MODE == 1) p = g_sm[qo + w.L] * g_sm[mlo + w.k];
         else if (MODE == 2) p = (g_sm[po + w.a] * g_sm[mmo + w.j]) * g_sm[mlo + w.k];
         else p = g_sm[pi];
-        const int off = (LS ? si[lo + w.L] : __ldg(gl + w.L)) + w.k;
+        const int off = (LS == 2 ? si[lo + w.a] + w.j * sM : (LS == 1 ? si[lo + w.L] : __ldg(gl + w.L))) + w.k;
         v = ldg_at(vb, off);
         pp += tpr;
         pi += tpr;
@@ -364,7 +368,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_build(GmDev D, long long row0, 
 
 // Stage (ii), on the fly (synthesis.cpp:100-104 + dot_slab :18-47): row groups
 // of tpr threads recompute each row from the staged masses and dot it with V.
-template <int TAB, bool LS, int U = 4>
+template <int TAB, int LS, int U = 4>
 __global__ void __launch_bounds__(kThreads) k_expect_ofa(GmDev D, long long nrows, int rb, GmFastDiv div_rb,
                                                         const double* __restrict__ mass,
                                                         const long long* __restrict__ origin,
@@ -373,10 +377,14 @@ __global__ void __launch_bounds__(kThreads) k_expect_ofa(GmDev D, long long nrow
                                                         const double* __restrict__ V,
                                                         double* __restrict__ v_in) {
     const Layout Y(D, rb, TAB);
-    if (LS) {
+    if (LS == 1) {
         int* si = reinterpret_cast<int*>(g_sm);
         for (int c = threadIdx.x; c < D.n_lines; c += blockDim.x) si[Y.offL + c] = D.line_off[c];
+    } else if (LS == 2) { // offsets of the leading prefixes a (j = 0 lines)
+        int* si = reinterpret_cast<int*>(g_sm);
+        for (int c = threadIdx.x; c < D.P_size; c += blockDim.x) si[Y.offL + c] = D.line_off[c * D.Wm];
     }
+    const int sM = (LS == 2 && D.Wm > 1) ? D.line_off[1] - D.line_off[0] : 0;
     const int tpr = D.tpr;
     const int groups = kThreads / tpr;
     const int g = threadIdx.x / tpr, lane = threadIdx.x - g * tpr;
@@ -396,7 +404,8 @@ __global__ void __launch_bounds__(kThreads) k_expect_ofa(GmDev D, long long nrow
             if (!(fl & (RF_ABSORBED | RF_ERROR))) {
                 s = row_dot<TAB == TAB_Q ? 1 : 2, U, LS>(D, lane, tpr, nullptr, Y.offQ + i * D.n_lines,
                                                          Y.offP + i * D.P_size, i * Y.mw + D.mm_off,
-                                                         i * Y.mw + D.ml_off, V + origin[row], D.line_off, Y.offL);
+                                                         i * Y.mw + D.ml_off, V + origin[row], D.line_off, Y.offL,
+                                                         sM);
             }
             s = group_reduce(s, tpr, Y.offR, g * tpr);
             if (valid && lane == 0) {
@@ -1080,6 +1089,7 @@ __global__ void __launch_bounds__(128) k_build_custom(GmDev D, long long row0, l
 
 namespace {
 constexpr size_t kSoftSmem = 56 * 1024;   // several CTAs per SM
+constexpr size_t kMidSmem = 74 * 1024;    // three CTAs per SM
 constexpr size_t kHardSmem = 200 * 1024;  // one CTA per SM, last resort
 }
 
@@ -1090,16 +1100,24 @@ BatchPlan plan_batches(const GmDev& D, bool ofa) {
     const size_t mw = static_cast<size_t>(D.sumW + 1);
     const size_t fixed = (kThreads / 32) * sizeof(double);
     const size_t table = ofa ? static_cast<size_t>(D.n_lines) * sizeof(int) : 0;
+    const size_t ptable = ofa ? static_cast<size_t>(D.P_size) * sizeof(int) : 0;
     const size_t q_row = (mw + D.P_size + D.n_lines) * sizeof(double);
     const size_t p_row = (mw + D.P_size) * sizeof(double);
     const long long want = std::max(b.groups, ofa ? 2 : 8);
     struct Opt { int tab; int lsmem; size_t budget; };
+    // lsmem 2: the leading-prefix offset table (P_size ints) replaces the line table
+    // when the latter does not fit (C4: 62.5 KB of lines vs 12.5 KB of prefixes).
+    // GM_OFA_TABLE (tuning / tests): "global" or "prefix" forces TAB_P with that table.
+    static const char* ft = std::getenv("GM_OFA_TABLE");
+    const int force = !ft ? -1 : (std::string(ft) == "global" ? 0 : (std::string(ft) == "prefix" ? 2 : -1));
     const Opt opts[] = {{TAB_Q, 1, kSoftSmem}, {TAB_Q, 0, kSoftSmem}, {TAB_P, 1, kSoftSmem},
-                        {TAB_P, 0, kSoftSmem}, {TAB_P, 0, kHardSmem}};
+                        {TAB_P, 2, kSoftSmem}, {TAB_P, 2, kMidSmem}, {TAB_P, 0, kSoftSmem}, {TAB_P, 2, kHardSmem},
+                        {TAB_P, 0, kHardSmem}};
     for (const Opt& o : opts) {
         const size_t per = o.tab == TAB_Q ? q_row : p_row;
-        const size_t tb = (ofa && o.lsmem) ? table : 0;
+        const size_t tb = (ofa && o.lsmem) ? (o.lsmem == 2 ? ptable : table) : 0;
         if (!ofa && o.lsmem) continue;
+        if (ofa && force >= 0 && (o.tab != TAB_P || o.lsmem != force)) continue;
         if (fixed + tb >= o.budget) continue;
         long long rb = static_cast<long long>((o.budget - fixed - tb) / per);
         if (rb < (o.budget == kHardSmem ? 1 : want)) continue;
@@ -1107,7 +1125,7 @@ BatchPlan plan_batches(const GmDev& D, bool ofa) {
         if (rb >= b.groups) rb -= rb % b.groups;
         b.rb = static_cast<int>(rb);
         b.tab = o.tab;
-        b.table_in_smem = (ofa && o.lsmem) ? 1 : 0;
+        b.table_in_smem = ofa ? o.lsmem : 0;
         b.smem = fixed + per * static_cast<size_t>(b.rb) + tb;
         return b;
     }
@@ -1314,7 +1332,7 @@ void build(const GmDev& D, long long row0, long long nrows, long long* origin_ou
     check_launch("build");
 }
 
-template <int TAB, bool LS>
+template <int TAB, int LS>
 static void launch_ofa(const GmDev& D, const BatchPlan& b, long long nrows, const double* mass,
                        const long long* origin, const double* t0x, const uint8_t* rowflag, const double* V,
                        double* v_in, cudaStream_t s) {
@@ -1333,11 +1351,12 @@ void expect_ofa(const GmDev& D, long long nrows, const double* mass, const long 
     if (nrows <= 0) return;
     const BatchPlan b = plan_batches(D, true);
     if (b.tab == TAB_Q) {
-        if (b.table_in_smem) launch_ofa<TAB_Q, true>(D, b, nrows, mass, origin, t0x, rowflag, V, v_in, s);
-        else launch_ofa<TAB_Q, false>(D, b, nrows, mass, origin, t0x, rowflag, V, v_in, s);
+        if (b.table_in_smem) launch_ofa<TAB_Q, 1>(D, b, nrows, mass, origin, t0x, rowflag, V, v_in, s);
+        else launch_ofa<TAB_Q, 0>(D, b, nrows, mass, origin, t0x, rowflag, V, v_in, s);
     } else {
-        if (b.table_in_smem) launch_ofa<TAB_P, true>(D, b, nrows, mass, origin, t0x, rowflag, V, v_in, s);
-        else launch_ofa<TAB_P, false>(D, b, nrows, mass, origin, t0x, rowflag, V, v_in, s);
+        if (b.table_in_smem == 1) launch_ofa<TAB_P, 1>(D, b, nrows, mass, origin, t0x, rowflag, V, v_in, s);
+        else if (b.table_in_smem == 2) launch_ofa<TAB_P, 2>(D, b, nrows, mass, origin, t0x, rowflag, V, v_in, s);
+        else launch_ofa<TAB_P, 0>(D, b, nrows, mass, origin, t0x, rowflag, V, v_in, s);
     }
     check_launch("expect_ofa");
 }

@@ -21,7 +21,7 @@ enum Family { KF_PROLOGUE = 0, KF_BUILD = 1, KF_MASK = 2, KF_EXPECT_MATRIX = 3, 
 struct BatchPlan {
     int tpr, groups, rb;     // threads per row, row groups per CTA, rows per CTA batch
     int tab;                 // 0: line-prefix table per row, 1: leading-prefix table per row
-    int table_in_smem;       // line-offset table staged in shared memory
+    int table_in_smem;       // 0: global line table; 1: line table in smem; 2: prefix table in smem
     size_t smem;             // dynamic shared memory bytes
 };
 BatchPlan plan_batches(const GmDev& D, bool ofa);
