@@ -1,3 +1,4 @@
+#include <numeric>
 // sm_100a kernels of the B200 AMYTISS engine.
 //
 // Stage (i)  MDP construction:  prologue (per-row image, slab origin, per-axis
@@ -256,6 +257,74 @@ __device__ __forceinline__ double row_dot(const GmDev& D, int lane, int tpr, con
     return s;
 }
 
+// OFA row dot with the last-axis cell hoisted out of the term loop (same terms,
+// same fma order as row_dot<MODE, U, LS>): a lane's last-axis cell advances by
+// tpr mod Wl per term, so it is periodic with period Wl / gcd(tpr mod Wl, Wl);
+// when U is a multiple of that period, slot u of every U-term block always sees
+// the same cell k_u. ml[k_u], k_u and the carry into the line index after slot u
+// are loaded once per row into registers: one shared load and the k walk less
+// per term (the kernel is bound by the L1/shared pipe).
+template <int MODE, int U, int LS>
+__device__ __forceinline__ double row_dot_pk(const GmDev& D, int lane, int tpr, int qo, int po, int mmo, int mlo,
+                                             const double* __restrict__ vb, const int* __restrict__ gl, int lo,
+                                             int sM) {
+    static_assert(MODE == 1 || MODE == 2, "recomputed rows only");
+    static_assert(LS != 2 || MODE == 2, "prefix offset table needs the (a, j, k) walk");
+    const int R = static_cast<int>(D.R);
+    const int n_it = lane < R ? (R - lane + tpr - 1) / tpr : 0;
+    Walk w;
+    w.init(D, lane, tpr);
+    double ml[U];
+    int kk[U], cc[U];
+    {
+        int k = w.k;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            kk[u] = k;
+            ml[u] = g_sm[mlo + k];
+            k += w.qk;
+            cc[u] = k >= w.Wl;
+            k -= cc[u] ? w.Wl : 0;
+        }
+    }
+    const int* si = sm_ints();
+    double s = 0.0;
+    auto term = [&](int u, double& p, double& v) {
+        const double lead = MODE == 1 ? g_sm[qo + w.L] : g_sm[po + w.a] * g_sm[mmo + w.j];
+        p = lead * ml[u];
+        const int off = (LS == 2 ? si[lo + w.a] + w.j * sM : (LS == 1 ? si[lo + w.L] : __ldg(gl + w.L))) + kk[u];
+        v = ldg_at(vb, off);
+        w.L += w.qL + cc[u];
+        if (MODE == 2) {
+            w.j += w.qj + cc[u];
+            const int c2 = w.j >= w.Wm;
+            w.j -= c2 ? w.Wm : 0;
+            w.a += w.qa + c2;
+        }
+    };
+    const int n_full = n_it - n_it % U;
+    for (int b = 0; b < n_full; b += U) {
+        double p[U], v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) term(u, p[u], v[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) s = fma(p[u], v[u], s);
+    }
+    const int rem = n_it - n_full;
+    if (rem) {
+        double p[U], v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            p[u] = 0.0;
+            v[u] = 0.0;
+            if (u < rem) term(u, p[u], v[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) s = fma(p[u], v[u], s);
+    }
+    return s;
+}
+
 // Stage (i), fused: each CTA batch evaluates its rows' prologue (image, origin,
 // target-hit mass: one thread per row), their per-axis cell masses (one thread
 // per row x cell), the prefix tables, then streams the R products of every row
@@ -368,7 +437,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_build(GmDev D, long long row0, 
 
 // Stage (ii), on the fly (synthesis.cpp:100-104 + dot_slab :18-47): row groups
 // of tpr threads recompute each row from the staged masses and dot it with V.
-template <int TAB, int LS, int U = 4>
+template <int TAB, int LS, int U = 4, bool PK = false>
 __global__ void __launch_bounds__(kThreads) k_expect_ofa(GmDev D, long long nrows, int rb, GmFastDiv div_rb,
                                                         const double* __restrict__ mass,
                                                         const long long* __restrict__ origin,
@@ -402,10 +471,16 @@ __global__ void __launch_bounds__(kThreads) k_expect_ofa(GmDev D, long long nrow
             const uint8_t fl = valid ? rowflag[row] : RF_ABSORBED;
             double s = 0.0;
             if (!(fl & (RF_ABSORBED | RF_ERROR))) {
-                s = row_dot<TAB == TAB_Q ? 1 : 2, U, LS>(D, lane, tpr, nullptr, Y.offQ + i * D.n_lines,
-                                                         Y.offP + i * D.P_size, i * Y.mw + D.mm_off,
-                                                         i * Y.mw + D.ml_off, V + origin[row], D.line_off, Y.offL,
-                                                         sM);
+                if (PK)
+                    s = row_dot_pk<TAB == TAB_Q ? 1 : 2, U, LS>(D, lane, tpr, Y.offQ + i * D.n_lines,
+                                                                Y.offP + i * D.P_size, i * Y.mw + D.mm_off,
+                                                                i * Y.mw + D.ml_off, V + origin[row], D.line_off,
+                                                                Y.offL, sM);
+                else
+                    s = row_dot<TAB == TAB_Q ? 1 : 2, U, LS>(D, lane, tpr, nullptr, Y.offQ + i * D.n_lines,
+                                                             Y.offP + i * D.P_size, i * Y.mw + D.mm_off,
+                                                             i * Y.mw + D.ml_off, V + origin[row], D.line_off, Y.offL,
+                                                             sM);
             }
             s = group_reduce(s, tpr, Y.offR, g * tpr);
             if (valid && lane == 0) {
@@ -1338,8 +1413,26 @@ static void launch_ofa(const GmDev& D, const BatchPlan& b, long long nrows, cons
                        double* v_in, cudaStream_t s) {
     const long long batches = (nrows + b.rb - 1) / b.rb;
     static const char* ou = std::getenv("GM_OFA_U"); // terms in flight per lane (tuning)
+    // hoisted last-axis cell (row_dot_pk): default only for periods 7-8; measured
+    // C4' (period 7, U 7) 12.0 -> 11.2 s, but C4 (period 5) 14.7 -> 22.2 s, C5 (5)
+    // 1.14 -> 1.29 s, C3b (3, U 6) 24 -> 31 ms. GM_OFA_PK=1 forces it, 0 disables it.
+    static const char* opk = std::getenv("GM_OFA_PK");
     const int u = ou ? std::atoi(ou) : 6; // C5: U = 4 1.23 s, 6 1.14 s, 8 1.14 s
     auto k = u == 8 ? k_expect_ofa<TAB, LS, 8> : (u == 6 ? k_expect_ofa<TAB, LS, 6> : k_expect_ofa<TAB, LS, 4>);
+    // hoisted last-axis cell: U = the smallest multiple of the cell period in [4, 8]
+    const int qk = D.tpr % D.Wl;
+    const int period = D.Wl / std::gcd(qk == 0 ? D.Wl : qk, D.Wl);
+    int up = 0;
+    for (int c = 4; c <= 8 && !up; ++c)
+        if (c % period == 0) up = c;
+    const int pk_mode = opk ? std::atoi(opk) : -1;
+    if (up && !ou && (pk_mode == 1 || (pk_mode == -1 && period >= 7))) {
+        k = up == 4   ? k_expect_ofa<TAB, LS, 4, true>
+            : up == 5 ? k_expect_ofa<TAB, LS, 5, true>
+            : up == 6 ? k_expect_ofa<TAB, LS, 6, true>
+            : up == 7 ? k_expect_ofa<TAB, LS, 7, true>
+                      : k_expect_ofa<TAB, LS, 8, true>;
+    }
     allow_smem(k, b.smem);
     k<<<resident_grid(k, b.smem, batches), kThreads, b.smem, s>>>(D, nrows, b.rb, gm_fastdiv(b.rb), mass, origin,
                                                                  t0x, rowflag, V, v_in);
