@@ -302,13 +302,30 @@ __device__ __forceinline__ double row_dot_pk(const GmDev& D, int lane, int tpr, 
             w.a += w.qa + c2;
         }
     };
+    // software-pipelined by one block: the U gathers of block b+1 are issued
+    // before the fma chain of block b (ptxas otherwise places each gather right
+    // before its fma at some U: one load in flight)
     const int n_full = n_it - n_it % U;
-    for (int b = 0; b < n_full; b += U) {
-        double p[U], v[U];
+    double pc[U], vc[U];
+    if (n_full > 0) {
 #pragma unroll
-        for (int u = 0; u < U; ++u) term(u, p[u], v[u]);
+        for (int u = 0; u < U; ++u) term(u, pc[u], vc[u]);
+    }
+    for (int b = U; b < n_full; b += U) {
+        double pn[U], vn[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) s = fma(p[u], v[u], s);
+        for (int u = 0; u < U; ++u) term(u, pn[u], vn[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) s = fma(pc[u], vc[u], s);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            pc[u] = pn[u];
+            vc[u] = vn[u];
+        }
+    }
+    if (n_full > 0) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) s = fma(pc[u], vc[u], s);
     }
     const int rem = n_it - n_full;
     if (rem) {
@@ -437,8 +454,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_build(GmDev D, long long row0, 
 
 // Stage (ii), on the fly (synthesis.cpp:100-104 + dot_slab :18-47): row groups
 // of tpr threads recompute each row from the staged masses and dot it with V.
-template <int TAB, int LS, int U = 4, bool PK = false>
-__global__ void __launch_bounds__(kThreads) k_expect_ofa(GmDev D, long long nrows, int rb, GmFastDiv div_rb,
+template <int TAB, int LS, int U, bool PK>
+__device__ __forceinline__ void expect_ofa_body(GmDev D, long long nrows, int rb, GmFastDiv div_rb,
                                                         const double* __restrict__ mass,
                                                         const long long* __restrict__ origin,
                                                         const double* __restrict__ t0x,
@@ -490,6 +507,29 @@ __global__ void __launch_bounds__(kThreads) k_expect_ofa(GmDev D, long long nrow
             }
         }
     }
+}
+
+// separate entry points: the pipelined hoisted-cell body needs the 3-CTA register
+// cap (80), the plain body keeps the compiler's own choice (48 registers)
+template <int TAB, int LS, int U = 4>
+__global__ void __launch_bounds__(kThreads) k_expect_ofa(GmDev D, long long nrows, int rb, GmFastDiv div_rb,
+                                                        const double* __restrict__ mass,
+                                                        const long long* __restrict__ origin,
+                                                        const double* __restrict__ t0x,
+                                                        const uint8_t* __restrict__ rowflag,
+                                                        const double* __restrict__ V,
+                                                        double* __restrict__ v_in) {
+    expect_ofa_body<TAB, LS, U, false>(D, nrows, rb, div_rb, mass, origin, t0x, rowflag, V, v_in);
+}
+template <int TAB, int LS, int U>
+__global__ void __launch_bounds__(kThreads, 3) k_expect_ofa_pk(GmDev D, long long nrows, int rb, GmFastDiv div_rb,
+                                                              const double* __restrict__ mass,
+                                                              const long long* __restrict__ origin,
+                                                              const double* __restrict__ t0x,
+                                                              const uint8_t* __restrict__ rowflag,
+                                                              const double* __restrict__ V,
+                                                              double* __restrict__ v_in) {
+    expect_ofa_body<TAB, LS, U, true>(D, nrows, rb, div_rb, mass, origin, t0x, rowflag, V, v_in);
 }
 
 // Stage (ii), stored matrix (synthesis.cpp:95-99): row groups stream each row
@@ -1413,9 +1453,8 @@ static void launch_ofa(const GmDev& D, const BatchPlan& b, long long nrows, cons
                        double* v_in, cudaStream_t s) {
     const long long batches = (nrows + b.rb - 1) / b.rb;
     static const char* ou = std::getenv("GM_OFA_U"); // terms in flight per lane (tuning)
-    // hoisted last-axis cell (row_dot_pk): default only for periods 7-8; measured
-    // C4' (period 7, U 7) 12.0 -> 11.2 s, but C4 (period 5) 14.7 -> 22.2 s, C5 (5)
-    // 1.14 -> 1.29 s, C3b (3, U 6) 24 -> 31 ms. GM_OFA_PK=1 forces it, 0 disables it.
+    // hoisted last-axis cell (row_dot_pk, software-pipelined, 3 CTAs/SM register
+    // cap): C4 14.7 -> 12.3 s, C4' 12.0 -> 10.7 s. GM_OFA_PK=1 / 0 forces it on / off.
     static const char* opk = std::getenv("GM_OFA_PK");
     const int u = ou ? std::atoi(ou) : 6; // C5: U = 4 1.23 s, 6 1.14 s, 8 1.14 s
     auto k = u == 8 ? k_expect_ofa<TAB, LS, 8> : (u == 6 ? k_expect_ofa<TAB, LS, 6> : k_expect_ofa<TAB, LS, 4>);
@@ -1426,12 +1465,15 @@ static void launch_ofa(const GmDev& D, const BatchPlan& b, long long nrows, cons
     for (int c = 4; c <= 8 && !up; ++c)
         if (c % period == 0) up = c;
     const int pk_mode = opk ? std::atoi(opk) : -1;
-    if (up && !ou && (pk_mode == 1 || (pk_mode == -1 && period >= 7))) {
-        k = up == 4   ? k_expect_ofa<TAB, LS, 4, true>
-            : up == 5 ? k_expect_ofa<TAB, LS, 5, true>
-            : up == 6 ? k_expect_ofa<TAB, LS, 6, true>
-            : up == 7 ? k_expect_ofa<TAB, LS, 7, true>
-                      : k_expect_ofa<TAB, LS, 8, true>;
+    // per-row setup (U shared loads, pipeline fill) pays off on long rows only:
+    // C5 (27 terms per lane) 1.154 vs 1.137 s without it
+    const long long per_lane = D.R / std::max(D.tpr, 1);
+    if (up && !ou && (pk_mode == 1 || (pk_mode == -1 && per_lane >= 64))) {
+        k = up == 4   ? k_expect_ofa_pk<TAB, LS, 4>
+            : up == 5 ? k_expect_ofa_pk<TAB, LS, 5>
+            : up == 6 ? k_expect_ofa_pk<TAB, LS, 6>
+            : up == 7 ? k_expect_ofa_pk<TAB, LS, 7>
+                      : k_expect_ofa_pk<TAB, LS, 8>;
     }
     allow_smem(k, b.smem);
     k<<<resident_grid(k, b.smem, batches), kThreads, b.smem, s>>>(D, nrows, b.rb, gm_fastdiv(b.rb), mass, origin,

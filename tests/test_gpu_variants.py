@@ -62,7 +62,7 @@ SETTINGS = [
     {"GM_JIT": "1"},
     {"GM_OFA_TABLE": "prefix"},  # OFA from the leading-prefix table + prefix offset table
     {"GM_OFA_TABLE": "global", "GM_OFA_U": "4"},  # same table, line offsets from global memory
-    {"GM_OFA_PK": "1"},  # OFA with the hoisted last-axis cell (row_dot_pk) at every period
+    {"GM_OFA_PK": "1"},  # OFA with the hoisted last-axis cell (row_dot_pk; default only for long rows)
     {"GM_OFA_PK": "1", "GM_OFA_TABLE": "prefix"},
 ]
 
