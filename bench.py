@@ -110,6 +110,53 @@ class Clocks:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def load_workloads():
+    """paper_2005_06191_b200/workloads.py by file path: importing the package would
+    load the engine library, which the reference arm must not map."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("_gm_workloads", REPO / "paper_2005_06191_b200" / "workloads.py")
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def ref_sizes(cfg_text: str) -> dict:
+    """Sizes of a workload from the reference itself (`gridmdp_ref estimate`:
+    print_sizes, tools/gridmdp_main.cpp:43-54) plus the horizon of its spec."""
+    import re
+
+    if not REF_BIN.exists():
+        raise FileNotFoundError(f"{REF_BIN} missing (make -C oracle ref)")
+    with tempfile.NamedTemporaryFile("w", suffix=".cfg", delete=False) as f:
+        f.write(cfg_text)
+        path = f.name
+    try:
+        out = subprocess.run([str(REF_BIN), "estimate", "-c", path], capture_output=True, text=True,
+                             check=True).stdout
+    finally:
+        os.unlink(path)
+    d = {}
+    for line in out.splitlines():
+        k, v = line.split(":", 1)
+        d[k.strip()] = [int(x) for x in v.split()] if k.strip() == "window" else int(v)
+    d["horizon"] = int(re.search(r"spec\.time_steps\s*=\s*(\d+)\s*;", cfg_text).group(1))
+    return d
+
+
+MODEL_NAMES = {"C2b": "vehicle3-eta/4 reach-avoid (stored MDP)", "C2a": "vehicle3 reach-avoid (stored MDP)",
+               "C1": "robot 2-d reach-avoid (stored MDP)"}
+
+
+def bench_config(workload: str, sz: dict, world: int) -> dict:
+    """The `config` object of the JSON line; byte-identical in both arms."""
+    return {"workload": workload, "model": MODEL_NAMES.get(workload, workload), "states": sz["states"],
+            "rows": sz["rows"], "row_width": sz["row_width"], "horizon": sz["horizon"],
+            "matrix_bytes": sz["rows"] * sz["row_width"] * 8, "parallelism": f"state-shard x{world}",
+            "l2": "inputs larger than L2 (108 GB matrix streamed per step)" if workload == "C2b"
+            else "inputs smaller than L2 are re-read every step"}
+
+
 def cpu_sample(cfg_text: str, rows_total: int, target_s: float, threads: int = 0, cal_rows: int = 20000):
     """Times the reference's row kernel (RowKernel::compute + fill_row) on a bounded
     contiguous sample of rows; returns (probs/s, rows, R, threads, seconds)."""
@@ -159,29 +206,60 @@ def cpu_sweep_step(cfg_text: str, n_x: int, threads: int = 0):
         subprocess.run(["rm", "-rf", d])
 
 
-def reference_arm(args, cfg_text, sizes):
+def reference_arm(args, cfg_text, sz):
+    """The reference's own CPU implementation of stage (i) (oracle/_ref: the
+    unmodified reference sources), all host threads, on bounded samples of the
+    workload's rows. Imports nothing from the engine package."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     vals = []
     last = None
     for i in range(args.warmup + args.steps):
-        v, n, R, th, s = cpu_sample(cfg_text, int(sizes.rows), args.cpu_seconds / 2)
+        v, n, R, th, s = cpu_sample(cfg_text, sz["rows"], args.cpu_seconds / 2)
         if i >= args.warmup:
             vals.append(v)
         last = (n, R, th, s)
     n, R, th, s = last
     value = statistics.median(vals)
-    sample = f"{n} contiguous rows (of {int(sizes.rows)}) x R={R} via RowKernel::compute+fill_row, {s:.2f} s"
+    sample = f"{n} contiguous rows (of {sz['rows']}) x R={R} via RowKernel::compute+fill_row, {s:.2f} s"
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "probs/s", "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "probs/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": n * R / value * 1e3,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.workload, "rows": int(sizes.rows), "row_width": R},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (config-defined grids; no external data)",
+        "config": bench_config(args.workload, sz, world),
         "cpu_baseline": {"value": value, "unit": "probs/s", "cores": th, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": "probs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def cpu_legs(args, cfg_text, sz) -> dict:
+    """The GPU arm's CPU baselines, run before any CUDA work in this process (the
+    reference in its own processes, the host otherwise idle): the reference arm's
+    row-kernel sample (one warm-up sample, then the timed one) and one reference
+    Bellman step over the whole workload."""
+    out = {}
+    try:
+        cpu_sample(cfg_text, sz["rows"], args.cpu_seconds / 2)
+        v, n, Rr, th, s = cpu_sample(cfg_text, sz["rows"], args.cpu_seconds / 2)
+        out["cpu_baseline"] = {"value": v, "unit": "probs/s", "cores": th, "kind": "reference",
+                               "sample": f"{n} contiguous rows (of {sz['rows']}) x R={Rr} via "
+                                         f"RowKernel::compute+fill_row, {s:.2f} s (before any CUDA work)"}
+    except Exception as e:  # noqa: BLE001
+        out["cpu_baseline"] = {"value": None, "error": str(e)}
+    try:  # the sweep half of the metric: one reference Bellman step on the same workload
+        secs, th = cpu_sweep_step(cfg_text, sz["states"])
+        T = sz["horizon"]
+        out["cpu_baseline_sweep"] = {
+            "value": secs * T, "unit": "s", "cores": th, "kind": "reference", "step_s": secs,
+            "sample": f"one OFA bellman_step over all {sz['rows']} rows (x{T} steps = a sweep); the stored-matrix "
+                      f"mode needs the {sz['rows'] * sz['row_width'] * 8 / 1e9:.0f} GB matrix in host RAM"}
+    except Exception as e:  # noqa: BLE001
+        out["cpu_baseline_sweep"] = {"value": None, "error": str(e)}
+    return out
 
 
 def main():
@@ -199,15 +277,17 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
 
-    from paper_2005_06191_b200 import workloads as W
-
+    W = load_workloads()
     cfg_text = W.WORKLOADS[args.workload]()
     if args.impl == "reference":
-        from paper_2005_06191_b200 import gridmdp as g
-
-        m = g.parse_config(cfg_text, args.workload)
-        reference_arm(args, cfg_text, m.sizes())
+        reference_arm(args, cfg_text, ref_sizes(cfg_text))
         return
+    cpu = {}
+    if int(os.environ.get("RANK", "0")) == 0 and int(os.environ.get("WORLD_SIZE", "1")) == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_legs(args, cfg_text, ref_sizes(cfg_text))
+        except Exception as e:  # noqa: BLE001
+            cpu = {"cpu_baseline": {"value": None, "error": str(e)}}
 
     import torch
     import torch.distributed as dist
@@ -325,13 +405,10 @@ def main():
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",  # C2b's states sharded over the ranks
         "data": "synthetic (config-defined grids; no external data)",
-        "config": {"workload": args.workload, "model": "vehicle3-eta/4 reach-avoid (stored MDP)",
-                   "states": n_x, "rows": rows_all, "row_width": R, "horizon": T,
-                   "matrix_bytes": rows_all * R * 8, "parallelism": f"state-shard x{world}",
-                   "v_exchange": ("none" if world == 1 else
-                                  f"halo p2p ({xplan.halo_states} of {xplan.allgather_states} all-gather states)"
-                                  if xplan is not None else "all-gather per step"),
-                   "l2": "inputs larger than L2 (108 GB matrix streamed per step)"},
+        "config": bench_config(args.workload, {"states": n_x, "rows": rows_all, "row_width": R, "horizon": T}, world),
+        "v_exchange": ("none" if world == 1 else
+                       f"halo p2p ({xplan.halo_states} of {xplan.allgather_states} all-gather states)"
+                       if xplan is not None else "all-gather per step"),
         "build_ms_per_step": bsum / args.steps, "sweep_s": sweep_s,
         "sweep_terms_per_s": terms_per_step / sweep_s if sweep_s > 0 else None,
         "kernel_ms_per_step": {k: v / args.steps for k, v in fam_ms.items() if v},
@@ -437,22 +514,9 @@ def main():
             bet.release()
         line["extra"] = extra
 
-    if rank == 0 and world == 1 and not args.no_cpu and value:
-        try:
-            v, n, Rr, th, s = cpu_sample(cfg_text, rows_all, args.cpu_seconds)
-            line["cpu_baseline"] = {"value": v, "unit": "probs/s", "cores": th, "kind": "reference",
-                                    "sample": f"{n} rows x R={Rr} (RowKernel::compute+fill_row), {s:.1f} s"}
-        except Exception as e:  # noqa: BLE001
-            line["cpu_baseline"] = {"value": None, "error": str(e)}
-        try:  # the sweep half of the metric: one reference Bellman step on the same workload
-            secs, th = cpu_sweep_step(cfg_text, n_x)
-            line["cpu_baseline_sweep"] = {
-                "value": secs * T, "unit": "s", "cores": th, "kind": "reference", "step_s": secs,
-                "sample": f"one OFA bellman_step over all {rows_all} rows (x{T} steps = a sweep); the stored-matrix "
-                          f"mode needs the {rows_all * R * 8 / 1e9:.0f} GB matrix in host RAM",
-                "gpu_speedup_sweep": secs * T / sweep_s if sweep_s else None}
-        except Exception as e:  # noqa: BLE001
-            line["cpu_baseline_sweep"] = {"value": None, "error": str(e)}
+    line.update(cpu)
+    if line.get("cpu_baseline_sweep", {}).get("value") and sweep_s:
+        line["cpu_baseline_sweep"]["gpu_speedup_sweep"] = line["cpu_baseline_sweep"]["value"] / sweep_s
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist.is_initialized():

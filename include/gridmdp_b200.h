@@ -232,6 +232,9 @@ gm_code gm_zero_absorbing_device(gm_model* m, double* d_v, void* stream, gm_stat
 
 /* synthesize (synthesis.hpp:46, synthesis.cpp:214-228) in the model's mode. */
 gm_code gm_synthesize(gm_model* m, gm_result** out, gm_status* st);
+/* Device time (CUDA events on the model's stream) of the model's last gm_synthesize:
+ * stage (i) (0 in OFA mode) and the T backward steps, ms. */
+gm_code gm_model_last_times(const gm_model* m, double* build_ms, double* sweep_ms, gm_status* st);
 /* synthesize_with_matrix (synthesis.hpp:51, synthesis.cpp:199-212); t0x may be NULL
  * (built on demand), host array of tm rows otherwise. */
 gm_code gm_synthesize_with_matrix(gm_model* m, gm_matrix* tm, const double* t0x,
@@ -280,6 +283,45 @@ gm_code gm_sim_copy(const gm_sim* s, uint8_t* satisfied, int32_t* steps, double*
 /* write_trajectory_csv (sim.hpp:48-50, sim.cpp:117-154). */
 gm_code gm_sim_write_csv(const gm_sim* s, const char* path, gm_status* st);
 void gm_sim_free(gm_sim* s);
+
+/* ------------------------------------------------ multi-GPU, one process */
+
+/* The reference's execution substrate is parallel_for over contiguous row
+ * ranges (include/gridmdp/parallel.hpp:23-51) under run_backward
+ * (src/synthesis.cpp:165-195); the engine's multi-GPU equivalent shards the
+ * states into contiguous flat-index ranges, one host thread and one stream per
+ * device, and exchanges V between steps (SURVEY.md §8 e). */
+typedef enum gm_exchange {
+    GM_XCHG_AUTO = 0,      /* halo when it moves at most half the all-gather's states */
+    GM_XCHG_HALO = 1,      /* only the cutoff-bounded halos (gm_shard_reach) */
+    GM_XCHG_ALLGATHER = 2  /* every shard to every device after each step */
+} gm_exchange;
+typedef enum gm_transport {
+    GM_XPORT_NCCL = 0,     /* ncclAllGather / ncclSend+ncclRecv (NVLink / NVSwitch); distinct devices */
+    GM_XPORT_PEER = 1      /* cudaMemcpyPeerAsync after a host barrier; any device list, repeats allowed */
+} gm_transport;
+
+typedef struct gm_multi_stats {
+    double build_ms;           /* stage (i) device time, max over devices (matrix mode) */
+    double sweep_ms;           /* T backward steps incl. V exchanges, device time, max over devices */
+    int64_t halo_states;       /* V entries one step moves with the halo plan (all devices) */
+    int64_t allgather_states;  /* V entries one step moves with the all-gather */
+    int32_t exchange_used;     /* GM_XCHG_HALO or GM_XCHG_ALLGATHER (0 for one device) */
+    int32_t transport_used;    /* gm_transport */
+    int32_t n_devices;
+} gm_multi_stats;
+
+/* A copy of the model's host description (grids, dynamics, noise, spec, options);
+ * its device state is created on the device current at its first device call. */
+gm_code gm_model_clone(const gm_model* m, gm_model** out, gm_status* st);
+
+/* synthesize (synthesis.hpp:46, synthesis.cpp:214-228) over n_dev devices of this
+ * process (devices[i], NULL = 0..n_dev-1): states split into n_dev equal
+ * contiguous ranges, each device builds its rows (matrix mode) and steps its
+ * states; V_{k+1} is exchanged per step by `exchange` over `transport`.
+ * Results are bit-identical to gm_synthesize for any n_dev. stats may be NULL. */
+gm_code gm_synthesize_multi(gm_model* m, int32_t n_dev, const int32_t* devices, int32_t exchange,
+                            int32_t transport, gm_result** out, gm_multi_stats* stats, gm_status* st);
 
 /* Large device blocks (>= 64 MB, e.g. stored matrices) are kept for reuse after
  * release; this returns them to the driver. */

@@ -71,6 +71,22 @@ class Sizes(C.Structure):
     ]
 
 
+GM_XCHG_AUTO, GM_XCHG_HALO, GM_XCHG_ALLGATHER = 0, 1, 2
+GM_XPORT_NCCL, GM_XPORT_PEER = 0, 1
+
+
+class MultiStats(C.Structure):
+    _fields_ = [
+        ("build_ms", C.c_double),
+        ("sweep_ms", C.c_double),
+        ("halo_states", C.c_int64),
+        ("allgather_states", C.c_int64),
+        ("exchange_used", C.c_int32),
+        ("transport_used", C.c_int32),
+        ("n_devices", C.c_int32),
+    ]
+
+
 # exported symbols and their (restype, argtypes); the CPU test suite checks
 # that every function declared in include/gridmdp_b200.h is exported.
 _VP = C.c_void_p
@@ -136,6 +152,10 @@ SIGNATURES = {
     "gm_sim_copy": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _PS]),
     "gm_sim_write_csv": (C.c_int, [_VP, C.c_char_p, _PS]),
     "gm_sim_free": (None, [_VP]),
+    "gm_model_clone": (C.c_int, [_VP, C.POINTER(_VP), _PS]),
+    "gm_model_last_times": (C.c_int, [_VP, _D, _D, _PS]),
+    "gm_synthesize_multi": (C.c_int, [_VP, C.c_int32, _VP, C.c_int32, C.c_int32, C.POINTER(_VP),
+                                      C.POINTER(MultiStats), _PS]),
 }
 
 

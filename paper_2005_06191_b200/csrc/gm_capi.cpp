@@ -4,6 +4,7 @@
 #include "gridmdp_b200.h"
 
 #include "gm_host.hpp"
+#include "gm_internal.hpp"
 #include "gm_jit.hpp"
 #include "gm_kernels.cuh"
 
@@ -14,6 +15,7 @@
 #include <climits>
 #include <cstring>
 #include <exception>
+#include <functional>
 #include <fstream>
 #include <map>
 #include <memory>
@@ -277,6 +279,8 @@ struct gm_model {
     bool jit_used = false;
     double jit_compile_s = 0.0;
     std::string jit_why;
+    // device time of the last gm_synthesize* (stage i / stage ii), ms
+    double last_build_ms = 0.0, last_sweep_ms = 0.0;
 };
 
 // Row kernels with the dynamics compiled for this model, or nullptr (interpreter).
@@ -400,6 +404,13 @@ void refresh_device(gm_model* m) {
     ensure_device(m);
     if (m->M.R > INT_MAX) throw MemoryErr("row width exceeds the device limit");
     m->D = m->M.device_descriptor();
+    {
+        // slab offsets (line table, element tables, V gathers) are 32-bit relative to
+        // the row's 64-bit origin: the slab's flat span must fit
+        long long span = 0;
+        for (int d = 0; d < m->D.n; ++d) span += static_cast<long long>(m->D.W[d] - 1) * m->D.xstride[d];
+        if (span > INT_MAX) throw MemoryErr("slab span exceeds the device's 32-bit offset range");
+    }
     m->D.prog = m->d_prog.p;
     m->D.lits = m->d_lits.p;
     const std::vector<int> lines = line_offsets(m->D);
@@ -605,7 +616,28 @@ void ensure_t0x(gm_model* m, gm_matrix* tm) {
 // tables are sized by a helper thread while the device builds and sweeps, and
 // each column goes to the host (aux stream) as soon as its step is done, under
 // the next step's kernels: the result is ready shortly after the last step.
-gm_result* run_backward(gm_model* m, gm_matrix* tm) {
+// CUDA events bracketing stage (i) / stage (ii) of one synthesis on the model's stream.
+struct PhaseTimer {
+    gm_model* m;
+    cudaEvent_t e[3] = {};
+    explicit PhaseTimer(gm_model* mm) : m(mm) {
+        for (cudaEvent_t& x : e) ck(cudaEventCreate(&x), "phase events");
+    }
+    ~PhaseTimer() {
+        for (cudaEvent_t x : e) cudaEventDestroy(x);
+    }
+    void mark(int i) { ck(cudaEventRecord(e[i], m->stream), "phase event"); }
+    void finish() {
+        float a = 0.f, b = 0.f;
+        ck(cudaEventSynchronize(e[2]), "phase event");
+        ck(cudaEventElapsedTime(&a, e[0], e[1]), "phase time");
+        ck(cudaEventElapsedTime(&b, e[1], e[2]), "phase time");
+        m->last_build_ms = a;
+        m->last_sweep_ms = b;
+    }
+};
+
+gm_result* run_backward(gm_model* m, gm_matrix* tm, PhaseTimer* pt = nullptr) {
     const int64_t n_x = m->M.n_x();
     const int T = m->M.spec.horizon;
     const bool reach = m->M.spec.reach();
@@ -665,6 +697,7 @@ gm_result* run_backward(gm_model* m, gm_matrix* tm) {
         ck(cudaMemcpyAsync(r->worst.data() + nx * k, wst.p + nx * k, nx * 4, cudaMemcpyDeviceToHost, m->aux), "worst");
         ck(cudaStreamSynchronize(m->aux), "column copy");
     };
+    if (pt) pt->mark(1);
     for (int k = T - 1; k >= 0; --k) {
         step_states(m, tm, 0, n_x, vals.p + nx * (k + 1), vals.p + nx * k, pol.p + nx * k, wst.p + nx * k, m->stream);
         ck(cudaEventRecord(done[k & 1], m->stream), "step event");
@@ -675,8 +708,10 @@ gm_result* run_backward(gm_model* m, gm_matrix* tm) {
             copy_column(k + 1, done[(k + 1) & 1]); // step k runs meanwhile
         }
     }
+    if (pt) pt->mark(2);
     ck(cudaStreamSynchronize(m->stream), "bellman sweep");
     raise_device_error(m);
+    if (pt) pt->finish();
     if (T > 0) copy_column(0, done[0]);
     join_sizer();
     if (reach) {
@@ -1372,12 +1407,16 @@ gm_code gm_synthesize(gm_model* m, gm_result** out, gm_status* st) {
                    << " are free; use ofa mode";
                 throw MemoryErr(os.str());
             }
+            PhaseTimer pt(m);
+            pt.mark(0);
             gm_matrix tm;
             build_rows(m, 0, m->M.rows(), &tm, m->M.spec.reach());
-            *out = run_backward(m, &tm);
+            *out = run_backward(m, &tm, &pt);
         } else {
             prepare(m);
-            *out = run_backward(m, nullptr);
+            PhaseTimer pt(m);
+            pt.mark(0);
+            *out = run_backward(m, nullptr, &pt);
         }
     });
 }
@@ -1460,6 +1499,21 @@ gm_code gm_result_from_tables(const gm_model* m, const double* values, const uin
     });
 }
 
+gm_code gm_model_last_times(const gm_model* m, double* build_ms, double* sweep_ms, gm_status* st) {
+    return guarded(st, [&] {
+        if (build_ms) *build_ms = m->last_build_ms;
+        if (sweep_ms) *sweep_ms = m->last_sweep_ms;
+    });
+}
+
+gm_code gm_model_clone(const gm_model* m, gm_model** out, gm_status* st) {
+    return guarded(st, [&] {
+        auto* c = new gm_model;
+        c->M = m->M; // host description only: device state is created on first use
+        *out = c;
+    });
+}
+
 gm_code gm_result_write(const gm_result* r, const char* path, gm_status* st) {
     return guarded(st, [&] {
         // write_results, io.cpp:142-179
@@ -1496,7 +1550,6 @@ gm_code gm_result_write(const gm_result* r, const char* path, gm_status* st) {
             os.write(buf.data(), static_cast<std::streamsize>(buf.size()));
             buf.clear();
         };
-        std::ostringstream tmp;
         for (size_t i = 0; i < nx; ++i)
             for (int k = 0; k <= T; ++k) {
                 uint64_t u;
@@ -1527,6 +1580,45 @@ void gm_result_free(gm_result* r) { delete r; }
 void gm_release_cached_memory(void) { flush_cache(); }
 
 } // extern "C"
+
+// ---------------------------------------------------------------- internal hooks (gm_internal.hpp)
+
+gm_result* gmi_result_new(const gm_model* m, int mode, const uint8_t* absorbing) {
+    std::unique_ptr<gm_result> r(new gm_result);
+    r->meta = m->M;
+    r->mode = mode;
+    r->n_x = m->M.n_x();
+    r->T = m->M.spec.horizon;
+    const size_t nx = static_cast<size_t>(r->n_x);
+    r->values.resize(nx * (r->T + 1));
+    r->policy.resize(nx * r->T);
+    r->worst.resize(nx * r->T);
+    const bool reach = m->M.spec.reach();
+    std::fill(r->values.begin() + static_cast<std::ptrdiff_t>(nx) * r->T, r->values.end(), reach ? 0.0 : 1.0);
+    if (reach) r->absorbing.assign(absorbing, absorbing + nx);
+    return r.release();
+}
+
+void gmi_result_tables(gm_result* r, double** values, uint32_t** policy, uint32_t** worst) {
+    *values = r->values.data();
+    *policy = r->policy.data();
+    *worst = r->worst.data();
+}
+
+gm_code gmi_guarded(gm_status* st, const std::function<void()>& f) { return guarded(st, f); }
+
+[[noreturn]] void gmi_throw(int code, const std::string& msg) {
+    switch (code) {
+        case GM_ERR_CONFIG: throw ConfigErr(msg);
+        case GM_ERR_MEMORY: throw MemoryErr(msg);
+        case GM_ERR_DOMAIN: throw DomainErr(msg);
+        case GM_ERR_IO: throw IoErr(msg);
+        case GM_ERR_RANGE: throw std::out_of_range(msg);
+        case GM_ERR_CUDA: throw CudaErr(msg);
+        default: throw std::runtime_error(msg);
+    }
+}
+
 
 // ===========================================================================
 // results reader (read_results, io.cpp:181-230) and the closed-loop simulator

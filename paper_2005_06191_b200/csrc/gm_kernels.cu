@@ -1362,8 +1362,14 @@ void build(const GmDev& D, long long row0, long long nrows, long long* origin_ou
     static const char* bw = std::getenv("GM_BUILD_WS"); // 0: single-role k_build
     if (!(bw && bw[0] == '0')) {
         // three-role pipelined build: layout of k_build_ws in doubles
+        // GM_BUILD_OPTS=16: per-role cycle totals (printf). The store-suppressing timing
+        // bits 32 / 64 write wrong rows and exist only in GM_DIAG builds.
         static const char* bo2 = std::getenv("GM_BUILD_OPTS");
         const int wopts = bo2 ? std::atoi(bo2) : 0;
+#ifndef GM_DIAG
+        if (wopts & 96)
+            throw std::runtime_error("build: GM_BUILD_OPTS bits 32/64 are timing diagnostics of GM_DIAG builds only");
+#endif
         const bool qs = build_uses_qs(D);
         const size_t fixed_d = D.n_ins + D.n_lits + 3 + (qs ? (D.pitch + 1) / 2 + (kThreads / 32) * (D.n_lines + 1) : 0);
         // two table buffers + two prologue buffers (pro_doubles: <= (5n + 2) rb + 2 for both)

@@ -664,11 +664,13 @@ __global__ void __launch_bounds__(kThreads, MINB) k_build_ws(GmDev D, long long 
                 const double* Pr = P + r * D.P_size;
                 double* out = probs + row * D.pitch;
                 const int pitch = static_cast<int>(D.pitch); // rows end in zero padding up to the pitch
-                if (opts & 96) { // diagnostics: 32 = constant stores only, 64 = no stores
+#ifdef GM_DIAG
+                if (opts & 96) { // timing diagnostics (GM_DIAG builds only): 32 = constant stores, 64 = no stores
                     if (opts & 32)
                         for (int t = lane; t < pitch; t += 32) __stcs(out + t, 0.0);
                     continue;
                 }
+#endif
                 if (QS) {
                     for (int L = lane; L < nl; L += 32) {
                         const int a = D.div_Wm.div(L), j = L - a * D.Wm;

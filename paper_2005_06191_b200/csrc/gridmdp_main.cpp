@@ -1,6 +1,7 @@
 // `gridmdp` CLI of the B200 engine: the reference's verbs, flags, key: value
 // report lines and exit codes (tools/gridmdp_main.cpp:16-227), driving the
-// C ABI of libgridmdp_b200.so. New options are CLI-only (`--device`), so the
+// C ABI of libgridmdp_b200.so. New options are CLI-only (`--device`, `--gpus`,
+// `--devices`, `--exchange`, `--transport`), so the
 // shared .cfg files stay valid for the reference parser (config.cpp:165-167).
 #include "gridmdp_b200.h"
 
@@ -20,7 +21,17 @@ struct Args {
     std::string verb, config, mode, output, dump, results, x0, dist_mode = "random", traj;
     long long threads = -1, mem_budget = -1, seed = -1, runs = -1, time_steps = -1;
     int device = 0;
+    // multi-GPU synthesis (CLI only): --gpus N (devices 0..N-1) or --devices a,b,..
+    std::vector<int> devices;
+    int exchange = GM_XCHG_AUTO, transport = GM_XPORT_NCCL;
 };
+
+// HBM bandwidth the roofline_frac line divides by: the measured copy bandwidth of a
+// B200 (MEASURED_PEAKS.json hbm_gbs), GM_HBM_PEAK_GBS overrides it.
+double hbm_peak_gbs() {
+    const char* e = std::getenv("GM_HBM_PEAK_GBS");
+    return e ? std::atof(e) : 6545.0;
+}
 
 double since(std::chrono::steady_clock::time_point t0) {
     return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -130,8 +141,40 @@ int cmd_synthesize(const Args& a) {
     if (a.device != 0 && gm_set_device(a.device, &st) != GM_OK) return fail(st);
     const auto t0 = std::chrono::steady_clock::now();
     gm_result* r = nullptr;
-    if (gm_synthesize(m, &r, &st) != GM_OK) return fail(st);
-    std::cout << "time_synthesize_s: " << since(t0) << "\n";
+    double build_ms = 0.0, sweep_ms = 0.0;
+    int gpus = 1;
+    if (!a.devices.empty()) { // one process, one host thread + stream per device
+        gm_multi_stats ms;
+        gpus = static_cast<int>(a.devices.size());
+        if (gm_synthesize_multi(m, gpus, a.devices.data(), a.exchange, a.transport, &r, &ms, &st) != GM_OK)
+            return fail(st);
+        build_ms = ms.build_ms;
+        sweep_ms = ms.sweep_ms;
+        std::cout << "time_synthesize_s: " << since(t0) << "\n";
+        if (gpus > 1)
+            std::cout << "v_exchange: " << (ms.exchange_used == GM_XCHG_HALO ? "halo" : "allgather") << " "
+                      << (ms.transport_used == GM_XPORT_NCCL ? "nccl" : "peer") << " ("
+                      << (ms.exchange_used == GM_XCHG_HALO ? ms.halo_states : ms.allgather_states)
+                      << " states per step)\n";
+    } else {
+        if (gm_synthesize(m, &r, &st) != GM_OK) return fail(st);
+        std::cout << "time_synthesize_s: " << since(t0) << "\n";
+        gm_model_last_times(m, &build_ms, &sweep_ms, &st);
+    }
+    // engine report lines (device time, CUDA events): stage (i), stage (ii), and the
+    // sweep against the HBM roofline (8 bytes per term T*V: the bytes matrix mode
+    // streams, the HBM-equivalent in OFA mode; SURVEY.md 8 d)
+    const double terms = static_cast<double>(sz.rows) * static_cast<double>(sz.row_width) * sz.horizon;
+    std::cout << "gpus: " << gpus << "\n";
+    std::cout << "time_build_s: " << build_ms / 1e3 << "\n";
+    std::cout << "time_sweep_s: " << sweep_ms / 1e3 << "\n";
+    if (sweep_ms > 0) {
+        std::cout << "sweep_terms_per_s: " << terms / (sweep_ms / 1e3) << "\n";
+        std::cout << "roofline_frac: " << terms * 8 / (sweep_ms / 1e3) / 1e9 / (hbm_peak_gbs() * gpus) << "\n";
+    }
+    if (build_ms > 0)
+        std::cout << "probs_per_s: " << static_cast<double>(sz.rows) * static_cast<double>(sz.row_width) / (build_ms / 1e3)
+                  << "\n";
     // output path: exec.output / -o, default results.bin (gridmdp_main.cpp:113)
     std::string out = gm_model_output_path(m);
     if (out.empty()) out = "results.bin";
@@ -245,7 +288,9 @@ void usage() {
                  "usage: gridmdp {estimate-mem|abstract|synthesize|simulate|export-prism} -c CFG [options]\n"
                  "  --threads N --mem-budget B --seed S --runs R --time-steps T -o PATH\n"
                  "  abstract: --dump-matrix PATH     synthesize: --mode matrix|ofa\n"
-                 "  GPU (CLI only): --device N\n";
+                 "  GPU (CLI only): --device N\n"
+                 "  synthesize on several GPUs: --gpus N | --devices a,b,.. [--exchange auto|halo|allgather]\n"
+                 "                              [--transport nccl|peer]\n";
 }
 
 } // namespace
@@ -307,6 +352,49 @@ int main(int argc, char** argv) {
             long long d = 0;
             num(d);
             a.device = static_cast<int>(d);
+        } else if (k == "--gpus" && a.verb == "synthesize") {
+            long long n = 0;
+            num(n);
+            if (n < 1) {
+                std::cerr << "--gpus: " << n << " not >= 1\n";
+                return 105;
+            }
+            a.devices.clear();
+            for (int d = 0; d < n; ++d) a.devices.push_back(d);
+        } else if (k == "--devices" && a.verb == "synthesize") {
+            const std::string s = val();
+            a.devices.clear();
+            size_t pos = 0;
+            while (pos <= s.size()) {
+                const size_t c = s.find(',', pos);
+                const std::string item = s.substr(pos, c == std::string::npos ? std::string::npos : c - pos);
+                char* end = nullptr;
+                const long d = std::strtol(item.c_str(), &end, 10);
+                if (item.empty() || *end || d < 0) {
+                    std::cerr << "Could not convert: --devices = " << s << "\n";
+                    return 105;
+                }
+                a.devices.push_back(static_cast<int>(d));
+                if (c == std::string::npos) break;
+                pos = c + 1;
+            }
+        } else if (k == "--exchange" && a.verb == "synthesize") {
+            const std::string e = val();
+            if (e == "auto") a.exchange = GM_XCHG_AUTO;
+            else if (e == "halo") a.exchange = GM_XCHG_HALO;
+            else if (e == "allgather") a.exchange = GM_XCHG_ALLGATHER;
+            else {
+                std::cerr << "--exchange: " << e << " not in {auto,halo,allgather}\n";
+                return 105;
+            }
+        } else if (k == "--transport" && a.verb == "synthesize") {
+            const std::string t = val();
+            if (t == "nccl") a.transport = GM_XPORT_NCCL;
+            else if (t == "peer") a.transport = GM_XPORT_PEER;
+            else {
+                std::cerr << "--transport: " << t << " not in {nccl,peer}\n";
+                return 105;
+            }
         } else if (k == "--dump-matrix" && a.verb == "abstract") a.dump = val();
         else if (k == "--mode" && a.verb == "synthesize") {
             a.mode = val();

@@ -583,6 +583,41 @@ def synthesize(m: SystemModel, spec: Optional[Spec] = None, opts: Optional[Synth
     return _result_from_handle(m, spec, h)
 
 
+def synthesize_multi(m: SystemModel, devices, spec: Optional[Spec] = None, opts: Optional[SynthesisOptions] = None,
+                     exchange: str = "auto", transport: str = "nccl"):
+    """synthesize over several GPUs of this process (gm_synthesize_multi): state shards,
+    one host thread + stream per device, V exchanged per step by `exchange`
+    ("auto" | "halo" | "allgather") over `transport` ("nccl" | "peer"; "peer" accepts a
+    device listed several times). Returns (SynthesisResult, stats dict)."""
+    spec = spec or m.spec
+    opts = opts or m.options
+    m.use_spec(spec)
+    m.use_options(opts)
+    dev = (C.c_int32 * len(devices))(*devices)
+    xchg = {"auto": _capi.GM_XCHG_AUTO, "halo": _capi.GM_XCHG_HALO, "allgather": _capi.GM_XCHG_ALLGATHER}[exchange]
+    xport = {"nccl": _capi.GM_XPORT_NCCL, "peer": _capi.GM_XPORT_PEER}[transport]
+    h = C.c_void_p()
+    ms = _capi.MultiStats()
+    call("gm_synthesize_multi", m.handle, C.c_int32(len(devices)), C.cast(dev, C.c_void_p), C.c_int32(xchg),
+         C.c_int32(xport), C.byref(h), C.byref(ms))
+    stats = {k: getattr(ms, k) for k, _ in _capi.MultiStats._fields_}
+    stats["exchange_used"] = {0: "none", 1: "halo", 2: "allgather"}[ms.exchange_used]
+    stats["transport_used"] = transport
+    return _result_from_handle(m, spec, h), stats
+
+
+def release_cached_memory() -> None:
+    """Returns the engine's cached large device blocks (released matrices) to the driver."""
+    lib.gm_release_cached_memory()
+
+
+def last_times(m: SystemModel) -> tuple[float, float]:
+    """(build_ms, sweep_ms) device time of the model's last synthesize (CUDA events)."""
+    b, w = C.c_double(), C.c_double()
+    call("gm_model_last_times", m.handle, C.byref(b), C.byref(w))
+    return b.value, w.value
+
+
 def synthesize_with_matrix(m: SystemModel, tm: TransitionMatrix, t0x: Optional[np.ndarray], spec: Spec,
                            opts: Optional[SynthesisOptions] = None) -> SynthesisResult:
     m.use_spec(spec)

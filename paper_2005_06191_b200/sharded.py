@@ -19,6 +19,7 @@ orchestration with the gloo process group.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 from dataclasses import dataclass
 from typing import Optional
@@ -163,6 +164,17 @@ def _exchange_halo(hp: HaloPlan, v: torch.Tensor, group=None) -> None:
 
 def synthesize_sharded(backend, n_x: int, horizon: int, reach: bool, matrix: bool, device,
                        group=None, timer=None, exchange: str = "auto"):
+    """run_backward (synthesis.cpp:165-195) over a sharded state space (see
+    `_synthesize_sharded`). Every torch op, collectives included, is issued on the
+    backend's stream, so the V exchange and the error check are ordered after the
+    backend's kernels whatever the caller's current stream is."""
+    bstream = getattr(backend, "stream", None) if torch.device(device).type == "cuda" else None
+    with torch.cuda.stream(bstream) if bstream is not None else contextlib.nullcontext():
+        return _synthesize_sharded(backend, n_x, horizon, reach, matrix, device, group, timer, exchange)
+
+
+def _synthesize_sharded(backend, n_x: int, horizon: int, reach: bool, matrix: bool, device,
+                        group=None, timer=None, exchange: str = "auto"):
     """run_backward (synthesis.cpp:165-195) over a sharded state space.
 
     Returns (values (T+1, n_x) on every rank, policy (T, n_x) and worst (T, n_x)
@@ -198,7 +210,8 @@ def synthesize_sharded(backend, n_x: int, horizon: int, reach: bool, matrix: boo
                 dist.all_gather_into_tensor(vals[k], vals[k, lo:lo + per].clone() if vals.device.type == "cpu"
                                             else vals[k, lo:lo + per], group=group)
             if k == T - 1 and hasattr(backend, "check"):
-                torch.cuda.current_stream().synchronize() if vals.is_cuda else None
+                if vals.is_cuda:
+                    torch.cuda.current_stream().synchronize()
                 backend.check()
     finally:
         if matrix and hasattr(backend, "free"):

@@ -116,3 +116,34 @@ def policy_ok(q_gpu, pol_gpu, pol_ref, rel=1e-9, abs_=1e-15):
     b = q_gpu[diff, pol_ref[diff]]
     ok = np.abs(a - b) <= rel * np.abs(a) + abs_
     return bool(ok.all()), int(diff.size)
+
+
+# ---------------------------------------------------------------- full-size goldens
+LARGE = GOLDEN / "large"
+
+
+def large_manifest() -> dict:
+    return json.loads((LARGE / "manifest.json").read_text())
+
+
+def large_results(name: str) -> dict:
+    return read_results(gzip.decompress((LARGE / large_manifest()[name]["results"]).read_bytes()))
+
+
+def large_cfg(name: str) -> Path:
+    return LARGE / large_manifest()[name]["config"]
+
+
+def large_array(name: str, dtype) -> np.ndarray:
+    return np.frombuffer(gzip.decompress((LARGE / f"{name}.gz").read_bytes()), dtype)
+
+
+def hashed_v(n: int) -> np.ndarray:
+    """The v_next of the C2b step golden (make_golden_large.hashed_v): splitmix64 of
+    the state index, top 53 bits, in [0, 1)."""
+    z = np.arange(n, dtype=np.uint64) + np.uint64(0x9E3779B97F4A7C15)
+    with np.errstate(over="ignore"):
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    return (z >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
