@@ -97,6 +97,72 @@ gm_code gm_model_parse(const char* text, const char* name, const gm_overrides* o
                        gm_status* st);
 void gm_model_free(gm_model* m);
 
+/* ---- the reference's in-memory types (for adapters that already hold a
+ * SystemModel / Spec / SynthesisOptions, e.g. INTEGRATION.md's drop-in of
+ * synthesize(const SystemModel&, const Spec&, const SynthesisOptions&)) ---- */
+
+/* Expr::Node (expr.hpp:36-52); op numbers follow Expr::Op (expr.hpp:38-45):
+ * add sub mul div pow lt le gt ge eq ne neg sin cos tan asin acos atan exp ln
+ * sqrt abs min max ite literal variable = 0..26; var_class 0 x / 1 u / 2 w. */
+typedef struct gm_expr_node {
+    int32_t op;
+    int32_t var_class;
+    int32_t var_index;
+    int32_t kid[3];
+    double value;
+} gm_expr_node;
+/* One Expr: its flat node pool (children before parents) and root (expr.hpp:48-49). */
+typedef struct gm_expr_desc {
+    const gm_expr_node* nodes;
+    int32_t n_nodes;
+    int32_t root;
+} gm_expr_desc;
+/* UniformGrid (grid.hpp:16-46) as made by make_grid(lb, ub, eta); dim 0 = the one-point grid. */
+typedef struct gm_grid_desc {
+    int32_t dim;
+    const double* lb;
+    const double* ub;
+    const double* eta;
+} gm_grid_desc;
+/* NoiseFamily (noise.hpp:12). */
+typedef enum gm_noise_family {
+    GM_NOISE_NORMAL = 0, GM_NOISE_UNIFORM = 1, GM_NOISE_EXPONENTIAL = 2, GM_NOISE_BETA = 3, GM_NOISE_CUSTOM = 4
+} gm_noise_family;
+/* SystemModel (model.hpp:15-33) + Spec (spec.hpp:14-20) + SynthesisOptions (synthesis.hpp:14-18). */
+typedef struct gm_model_desc {
+    gm_grid_desc state, input, disturbance;
+    const gm_expr_desc* dynamics;   /* one per state dimension */
+    int32_t n_dynamics;
+    /* NoiseSpec (noise.hpp:24-66): family, mode (0 additive, 1 multiplicative), gamma,
+     * param1 (sigma / a / rate / alpha) and param2 (b / beta; NULL otherwise), noise_dim
+     * entries each. Custom densities: the joint pdf as an expression over x0..x{n-1}
+     * (the noise coordinates) and its support box in param1 / param2. */
+    int32_t noise_family;
+    int32_t noise_mode;
+    double gamma;
+    int32_t noise_dim;
+    const double* param1;
+    const double* param2;
+    gm_expr_desc custom_pdf;
+    /* Spec: kind (gm_spec_kind), horizon, target / avoid boxes (NULL = empty). */
+    int32_t spec_kind;
+    int32_t horizon;
+    const double* target_lo;
+    const double* target_hi;
+    const double* avoid_lo;
+    const double* avoid_hi;
+    /* SynthesisOptions: mode (gm_mode), threads (host side only), memory budget. */
+    int32_t mode;
+    int32_t threads;
+    uint64_t mem_budget;
+} gm_model_desc;
+
+/* make_model (model.cpp:15-29) + validate_spec from the reference's in-memory types:
+ * the grids, the dynamics' node pools, the noise and the spec are copied. */
+gm_code gm_model_create(const gm_model_desc* desc, gm_model** out, gm_status* st);
+/* save_config (config.hpp:59-60, config.cpp:270-310) of a model made from configuration text. */
+gm_code gm_model_save_config(const gm_model* m, const char* path, gm_status* st);
+
 /* Replaces the model's Spec (make_safety/make_reachability/make_reach_avoid, spec.hpp:24-26).
  * target/avoid are n_dim-long [lo, hi] vectors, or NULL for an absent box. */
 gm_code gm_model_set_spec(gm_model* m, int32_t kind, int32_t horizon, const double* target_lo,
@@ -180,6 +246,16 @@ gm_code gm_matrix_write(const gm_matrix* tm, const gm_model* m, const char* path
  * from the device-resident matrix (the nonzero count is reduced on the device). */
 gm_code gm_matrix_write_prism(const gm_matrix* tm, const gm_model* m, const char* path, gm_status* st);
 void gm_matrix_free(gm_matrix* tm);
+/* read_matrix (io.hpp:18, io.cpp:258-283): a `gridmdp-matrix 1` container onto the
+ * current device (rows padded to the device pitch), e.g. for gm_synthesize_with_matrix.
+ * The container's grid / input / disturbance counts / window are checked against the
+ * model when the matrix is used with it. */
+gm_code gm_matrix_read(const char* path, gm_matrix** out, gm_status* st);
+/* A host TransitionMatrix (abstraction.hpp:22-65: origins int64[rows], row-major
+ * probs f64[rows x R]) onto the current device for the model's rows [row_begin,
+ * row_begin + rows); R must equal the model's row width. */
+gm_code gm_matrix_upload(const gm_model* m, int64_t row_begin, int64_t rows, const int64_t* origins,
+                         const double* probs, gm_matrix** out, gm_status* st);
 
 /* ------------------------------------------------------------ stage (ii) */
 
@@ -259,6 +335,11 @@ void gm_result_free(gm_result* r);
 
 /* read_results (io.hpp:14, io.cpp:181-230): a `gridmdp-results 1` container. */
 gm_code gm_result_read(const char* path, gm_result** out, gm_status* st);
+/* query_policy (synthesis.hpp:66, synthesis.cpp:230-239): the input vector prescribed
+ * at continuous state x (n = state dim) and step k (1 <= k <= horizon) into u_out
+ * (input dim doubles); GM_ERR_RANGE outside the quantized region or the horizon. */
+gm_code gm_query_policy(const gm_result* r, const double* x, int32_t n, int32_t k, double* u_out,
+                        gm_status* st);
 /* values(point_to_index(state_grid, x), k) (gridmdp_main.cpp:133-134 value_at_x0). */
 gm_code gm_result_value_at(const gm_result* r, const double* x, int32_t n, int32_t k, double* v, gm_status* st);
 

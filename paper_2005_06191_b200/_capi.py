@@ -153,6 +153,11 @@ SIGNATURES = {
     "gm_sim_write_csv": (C.c_int, [_VP, C.c_char_p, _PS]),
     "gm_sim_free": (None, [_VP]),
     "gm_model_clone": (C.c_int, [_VP, C.POINTER(_VP), _PS]),
+    "gm_model_create": (C.c_int, [_VP, C.POINTER(_VP), _PS]),
+    "gm_model_save_config": (C.c_int, [_VP, C.c_char_p, _PS]),
+    "gm_matrix_read": (C.c_int, [C.c_char_p, C.POINTER(_VP), _PS]),
+    "gm_matrix_upload": (C.c_int, [_VP, _I64, _I64, _VP, _VP, C.POINTER(_VP), _PS]),
+    "gm_query_policy": (C.c_int, [_VP, _VP, C.c_int32, C.c_int32, _D, _PS]),
     "gm_model_last_times": (C.c_int, [_VP, _D, _D, _PS]),
     "gm_synthesize_multi": (C.c_int, [_VP, C.c_int32, _VP, C.c_int32, C.c_int32, C.POINTER(_VP),
                                       C.POINTER(MultiStats), _PS]),

@@ -315,6 +315,11 @@ struct gm_matrix {
     DevBuf<double> t0x; // optional (shard builds for reach specs)
     bool has_t0x = false;
     bool masked = false;
+    // read_matrix containers carry their own shape (io.cpp:262-276), checked against a model
+    bool has_meta = false;
+    Grid X;
+    int64_t n_u = 0, n_w = 0;
+    std::vector<int64_t> extents;
 };
 
 // Host tables that are filled by copies: resize() leaves the elements
@@ -353,6 +358,55 @@ struct gm_result {
 };
 
 namespace {
+
+struct ManifestR { // io.cpp:72-121
+    std::map<std::string, std::string> kv;
+    ManifestR(std::istream& is, const char* magic) {
+        std::string line;
+        if (!std::getline(is, line)) throw IoErr("empty container");
+        std::istringstream head(line);
+        std::string mg;
+        int version = 0;
+        head >> mg >> version;
+        if (mg != magic) throw IoErr("bad magic line '" + line + "'");
+        if (version != 1) throw IoErr("unsupported container version " + std::to_string(version));
+        while (std::getline(is, line)) {
+            if (line == "payload") return;
+            const auto eq = line.find('=');
+            if (eq == std::string::npos || line.empty() || line.back() != ';')
+                throw IoErr("malformed manifest line '" + line + "'");
+            auto trim = [](std::string s) {
+                const auto b = s.find_first_not_of(" \t");
+                const auto e = s.find_last_not_of(" \t");
+                return b == std::string::npos ? std::string{} : s.substr(b, e - b + 1);
+            };
+            kv[trim(line.substr(0, eq))] = trim(line.substr(eq + 1, line.size() - eq - 2));
+        }
+        throw IoErr("missing payload marker");
+    }
+    bool has(const std::string& k) const { return kv.count(k) != 0; }
+    const std::string& str(const std::string& k) const {
+        auto it = kv.find(k);
+        if (it == kv.end()) throw IoErr("manifest key '" + k + "' missing");
+        return it->second;
+    }
+    int64_t integer(const std::string& k) const { return std::stoll(str(k)); }
+    double number(const std::string& k) const { return std::stod(str(k)); }
+    std::vector<double> vec(const std::string& k) const {
+        const std::string& s = str(k);
+        if (s.size() < 2 || s.front() != '{' || s.back() != '}')
+            throw IoErr("manifest key '" + k + "' is not a vector");
+        std::vector<double> out;
+        std::istringstream iss(s.substr(1, s.size() - 2));
+        std::string item;
+        while (std::getline(iss, item, ',')) out.push_back(std::stod(item));
+        return out;
+    }
+    Grid grid(const std::string& prefix) const {
+        if (integer(prefix + ".dim") == 0) return grid_from({}, {}, {});
+        return grid_from(vec(prefix + ".lb"), vec(prefix + ".ub"), vec(prefix + ".eta"));
+    }
+};
 
 std::vector<int> line_offsets(const GmDev& D) {
     // relative flat offset of every slab line (all axes but the last, row-major)
@@ -501,6 +555,16 @@ void pipeline(gm_model* m, int64_t n, int64_t chunk, cudaStream_t s, Produce&& p
     ck(cudaStreamWaitEvent(s, m->ev_join, 0), "join");
 }
 
+// A matrix used with a model must have its row shape (and, when read from a
+// container, its grid, input / disturbance counts and window).
+void check_matrix_model(const gm_matrix* tm, const gm_model* m) {
+    bool ok = tm->R == m->M.R && tm->row_end <= m->M.rows();
+    if (ok && tm->has_meta)
+        ok = tm->X.lb == m->M.X.lb && tm->X.ub == m->M.X.ub && tm->X.eta == m->M.X.eta && tm->n_u == m->M.n_u() &&
+             tm->n_w == m->M.n_w() && tm->extents == m->M.extents;
+    if (!ok) throw ConfigErr("the transition matrix does not match the model (grid, counts or window)");
+}
+
 // Stage (i) for rows [r0, r1): origins + probabilities (+ T0x for reach shards)
 void build_rows(gm_model* m, int64_t r0, int64_t r1, gm_matrix* tm, bool want_t0x) {
     const int64_t n = r1 - r0;
@@ -542,6 +606,7 @@ void step_states(gm_model* m, gm_matrix* tm, int64_t x0, int64_t x1, const doubl
     const int64_t n = r1 - r0;
     m->d_vin.ensure(static_cast<size_t>(std::max<int64_t>(n, 1)), "v_in workspace");
     if (tm) {
+        check_matrix_model(tm, m);
         if (tm->row_begin > r0 || tm->row_end < r1)
             throw ConfigErr("bellman step: the matrix does not cover the requested states");
         Launch L(gmk::KF_EXPECT_MATRIX, s);
@@ -782,6 +847,73 @@ static gm_code make_model(const Cfg& c0, const gm_overrides* ov, gm_model** out,
             throw;
         }
         *out = m;
+    });
+}
+
+gm_code gm_model_create(const gm_model_desc* d, gm_model** out, gm_status* st) {
+    return guarded(st, [&] {
+        auto grid = [](const gm_grid_desc& g) {
+            if (g.dim < 0 || g.dim > GM_MAX_DIMS) throw ConfigErr("model_create: grid dimension out of range");
+            if (g.dim == 0) return grid_from({}, {}, {});
+            return grid_from(std::vector<double>(g.lb, g.lb + g.dim), std::vector<double>(g.ub, g.ub + g.dim),
+                             std::vector<double>(g.eta, g.eta + g.dim));
+        };
+        const Grid X = grid(d->state), U = grid(d->input), W = grid(d->disturbance);
+        const int n = X.dim(), mm = U.dim(), p = W.dim();
+        auto expr = [&](const gm_expr_desc& e, int nn, int m2, int p2, const std::string& what) {
+            if (e.n_nodes <= 0 || !e.nodes) throw ConfigErr(what + ": empty expression");
+            std::vector<XNode> nodes(static_cast<size_t>(e.n_nodes));
+            for (int32_t i = 0; i < e.n_nodes; ++i) {
+                const gm_expr_node& s = e.nodes[i];
+                XNode& x = nodes[static_cast<size_t>(i)];
+                if (s.op < 0 || s.op > static_cast<int>(XOp::variable))
+                    throw ConfigErr(what + ": node " + std::to_string(i) + " has an unknown operator");
+                x.op = static_cast<XOp>(s.op);
+                x.value = s.value;
+                x.vclass = static_cast<uint8_t>(s.var_class);
+                x.vindex = s.var_index;
+                for (int k = 0; k < 3; ++k) x.kid[k] = s.kid[k];
+            }
+            return expr_from_nodes(std::move(nodes), e.root, nn, m2, p2, what);
+        };
+        std::vector<Expr> dyn;
+        for (int32_t i = 0; i < d->n_dynamics; ++i)
+            dyn.push_back(expr(d->dynamics[i], n, mm, p, "dynamics.x" + std::to_string(i)));
+        const int nd = d->noise_dim;
+        if (nd < 0 || nd > GM_MAX_DIMS) throw ConfigErr("model_create: noise dimension out of range");
+        std::vector<double> p1(d->param1, d->param1 + (d->param1 ? nd : 0));
+        std::vector<double> p2(d->param2, d->param2 + (d->param2 ? nd : 0));
+        Expr pdf;
+        if (d->noise_family == GM_NOISE_CUSTOM) pdf = expr(d->custom_pdf, n, 0, 0, "noise.pdf");
+        SpecV spec;
+        if (d->spec_kind < GM_SAFETY || d->spec_kind > GM_REACH_AVOID) throw ConfigErr("model_create: unknown spec kind");
+        spec.kind = d->spec_kind;
+        spec.horizon = d->horizon;
+        if (d->target_lo && d->target_hi)
+            spec.target = BoxV{std::vector<double>(d->target_lo, d->target_lo + n),
+                               std::vector<double>(d->target_hi, d->target_hi + n)};
+        if (d->avoid_lo && d->avoid_hi)
+            spec.avoid = BoxV{std::vector<double>(d->avoid_lo, d->avoid_lo + n),
+                              std::vector<double>(d->avoid_hi, d->avoid_hi + n)};
+        auto* m = new gm_model;
+        try {
+            m->M = build_model_from_parts(X, U, W, std::move(dyn), d->noise_family, d->noise_mode ? 1 : 0, d->gamma, p1,
+                                          p2, std::move(pdf), spec, d->mode == GM_MODE_OFA ? GM_MODE_OFA_ : GM_MODE_MATRIX_,
+                                          d->threads, d->mem_budget);
+        } catch (...) {
+            delete m;
+            throw;
+        }
+        *out = m;
+    });
+}
+
+gm_code gm_model_save_config(const gm_model* m, const char* path, gm_status* st) {
+    return guarded(st, [&] {
+        std::ofstream os(path);
+        if (!os) throw IoErr(std::string("cannot open '") + path + "' for writing");
+        os << save_config_text(m->M.cfg);
+        if (!os) throw IoErr(std::string("failed while writing '") + path + "'");
     });
 }
 
@@ -1313,6 +1445,88 @@ void gm_matrix_free(gm_matrix* tm) {
     delete tm;
 }
 
+gm_code gm_matrix_read(const char* path, gm_matrix** out, gm_status* st) {
+    return guarded(st, [&] {
+        // read_matrix, io.cpp:258-283
+        std::ifstream is(path, std::ios::binary);
+        if (!is) throw IoErr(std::string("cannot open '") + path + "'");
+        ManifestR mf(is, "gridmdp-matrix");
+        auto tm = std::make_unique<gm_matrix>();
+        tm->has_meta = true;
+        tm->X = mf.grid("states");
+        tm->n_u = mf.integer("n_inputs");
+        tm->n_w = mf.integer("n_disturbances");
+        int64_t R = 1;
+        for (double w : mf.vec("window")) {
+            tm->extents.push_back(static_cast<int64_t>(w));
+            R *= tm->extents.back();
+        }
+        const int64_t rows = tm->X.total * tm->n_u * tm->n_w;
+        int count = 0;
+        if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+            cudaGetLastError();
+            throw CudaErr("no CUDA device available: the B200 engine has no CPU fallback");
+        }
+        ck(cudaGetDevice(&tm->device), "cudaGetDevice");
+        tm->row_begin = 0;
+        tm->row_end = rows;
+        tm->R = R;
+        tm->pitch = row_pitch(R);
+        tm->probs.ensure(mul_checked(static_cast<uint64_t>(rows), static_cast<uint64_t>(tm->pitch), "matrix size"),
+                         "matrix payload");
+        tm->origins.ensure(static_cast<size_t>(std::max<int64_t>(rows, 1)), "matrix origins");
+        if (tm->pitch != R) ck(cudaMemset(tm->probs.p, 0, static_cast<size_t>(rows * tm->pitch) * 8), "padding");
+        // little-endian payloads (io.cpp:30-70) on a little-endian host: bulk reads
+        std::vector<long long> org(static_cast<size_t>(rows));
+        is.read(reinterpret_cast<char*>(org.data()), static_cast<std::streamsize>(org.size() * 8));
+        if (!is) throw IoErr("truncated payload");
+        if (rows) ck(cudaMemcpy(tm->origins.p, org.data(), org.size() * 8, cudaMemcpyHostToDevice), "origins");
+        const int64_t blk = std::max<int64_t>(1, (64LL << 20) / 8 / std::max<int64_t>(R, 1));
+        std::vector<double> buf;
+        for (int64_t r = 0; r < rows; r += blk) {
+            const int64_t n = std::min(blk, rows - r);
+            buf.resize(static_cast<size_t>(n * R));
+            is.read(reinterpret_cast<char*>(buf.data()), static_cast<std::streamsize>(buf.size() * 8));
+            if (!is) throw IoErr("truncated payload");
+            ck(cudaMemcpy2D(tm->probs.p + r * tm->pitch, static_cast<size_t>(tm->pitch) * 8, buf.data(),
+                            static_cast<size_t>(R) * 8, static_cast<size_t>(R) * 8, static_cast<size_t>(n),
+                            cudaMemcpyHostToDevice),
+               "probs");
+        }
+        char extra;
+        if (is.get(extra)) throw IoErr("trailing bytes after the declared payload");
+        *out = tm.release();
+    });
+}
+
+gm_code gm_matrix_upload(const gm_model* mc, int64_t row_begin, int64_t rows, const int64_t* origins,
+                         const double* probs, gm_matrix** out, gm_status* st) {
+    return guarded(st, [&] {
+        gm_model* m = const_cast<gm_model*>(mc); // device residency only
+        if (row_begin < 0 || rows < 0 || row_begin + rows > m->M.rows())
+            throw std::out_of_range("matrix_upload: row range outside the model");
+        prepare(m);
+        auto tm = std::make_unique<gm_matrix>();
+        tm->device = m->device;
+        tm->row_begin = row_begin;
+        tm->row_end = row_begin + rows;
+        tm->R = m->M.R;
+        tm->pitch = m->D.pitch;
+        const int64_t R = tm->R;
+        tm->probs.ensure(mul_checked(static_cast<uint64_t>(rows), static_cast<uint64_t>(tm->pitch), "matrix size"),
+                         "matrix payload");
+        tm->origins.ensure(static_cast<size_t>(std::max<int64_t>(rows, 1)), "matrix origins");
+        if (tm->pitch != R) ck(cudaMemset(tm->probs.p, 0, static_cast<size_t>(rows * tm->pitch) * 8), "padding");
+        if (rows) {
+            ck(cudaMemcpy(tm->origins.p, origins, static_cast<size_t>(rows) * 8, cudaMemcpyHostToDevice), "origins");
+            ck(cudaMemcpy2D(tm->probs.p, static_cast<size_t>(tm->pitch) * 8, probs, static_cast<size_t>(R) * 8,
+                            static_cast<size_t>(R) * 8, static_cast<size_t>(rows), cudaMemcpyHostToDevice),
+               "probs");
+        }
+        *out = tm.release();
+    });
+}
+
 // ---------------------------------------------------------------- stage (ii)
 
 gm_code gm_bellman_step(gm_model* m, gm_matrix* tm, const double* t0x, const double* v_next, double* v_out,
@@ -1636,54 +1850,6 @@ struct gm_sim {
 
 namespace {
 
-struct ManifestR { // io.cpp:72-121
-    std::map<std::string, std::string> kv;
-    ManifestR(std::istream& is, const char* magic) {
-        std::string line;
-        if (!std::getline(is, line)) throw IoErr("empty container");
-        std::istringstream head(line);
-        std::string mg;
-        int version = 0;
-        head >> mg >> version;
-        if (mg != magic) throw IoErr("bad magic line '" + line + "'");
-        if (version != 1) throw IoErr("unsupported container version " + std::to_string(version));
-        while (std::getline(is, line)) {
-            if (line == "payload") return;
-            const auto eq = line.find('=');
-            if (eq == std::string::npos || line.empty() || line.back() != ';')
-                throw IoErr("malformed manifest line '" + line + "'");
-            auto trim = [](std::string s) {
-                const auto b = s.find_first_not_of(" \t");
-                const auto e = s.find_last_not_of(" \t");
-                return b == std::string::npos ? std::string{} : s.substr(b, e - b + 1);
-            };
-            kv[trim(line.substr(0, eq))] = trim(line.substr(eq + 1, line.size() - eq - 2));
-        }
-        throw IoErr("missing payload marker");
-    }
-    bool has(const std::string& k) const { return kv.count(k) != 0; }
-    const std::string& str(const std::string& k) const {
-        auto it = kv.find(k);
-        if (it == kv.end()) throw IoErr("manifest key '" + k + "' missing");
-        return it->second;
-    }
-    int64_t integer(const std::string& k) const { return std::stoll(str(k)); }
-    double number(const std::string& k) const { return std::stod(str(k)); }
-    std::vector<double> vec(const std::string& k) const {
-        const std::string& s = str(k);
-        if (s.size() < 2 || s.front() != '{' || s.back() != '}')
-            throw IoErr("manifest key '" + k + "' is not a vector");
-        std::vector<double> out;
-        std::istringstream iss(s.substr(1, s.size() - 2));
-        std::string item;
-        while (std::getline(iss, item, ',')) out.push_back(std::stod(item));
-        return out;
-    }
-    Grid grid(const std::string& prefix) const {
-        if (integer(prefix + ".dim") == 0) return grid_from({}, {}, {});
-        return grid_from(vec(prefix + ".lb"), vec(prefix + ".ub"), vec(prefix + ".eta"));
-    }
-};
 
 // contains(grid, x), grid.cpp:67-75
 bool grid_contains(const Grid& g, const std::vector<double>& x) {
@@ -1767,6 +1933,21 @@ gm_code gm_result_read(const char* path, gm_result** out, gm_status* st) {
         char extra;
         if (is.get(extra)) throw IoErr("trailing bytes after the declared payload");
         *out = r.release();
+    });
+}
+
+gm_code gm_query_policy(const gm_result* r, const double* x, int32_t n, int32_t k, double* u_out, gm_status* st) {
+    return guarded(st, [&] {
+        // query_policy, synthesis.cpp:230-239
+        if (k < 1 || k > r->T) {
+            std::ostringstream os;
+            os << "query_policy: step " << k << " outside [1, " << r->T << "]";
+            throw std::out_of_range(os.str());
+        }
+        const int64_t ix = grid_index(r->meta.X, std::vector<double>(x, x + n)); // point_to_index
+        const uint32_t iu = r->policy[static_cast<size_t>(k - 1) * static_cast<size_t>(r->n_x) + static_cast<size_t>(ix)];
+        const std::vector<double> u = grid_point(r->meta.U, static_cast<int64_t>(iu)); // index_to_point
+        std::copy(u.begin(), u.end(), u_out);
     });
 }
 

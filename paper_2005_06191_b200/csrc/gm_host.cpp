@@ -1113,7 +1113,17 @@ Model build_model_from_cfg(const Cfg& c) {
         }
     } else M.noise = make_noise(GM_BETA, c.alpha, c.beta, g, c.noise_mult);
 
-    // make_model checks (model.cpp:15-29)
+    M.spec = spec_from_cfg(c);
+    M.mode = c.mode == "ofa" ? GM_MODE_OFA_ : GM_MODE_MATRIX_;
+    M.threads = c.threads;
+    M.mem_budget = c.mem_budget;
+    finish_model(M);
+    return M;
+}
+
+// make_model checks (model.cpp:15-29), then sizes and the dynamics program
+void finish_model(Model& M) {
+    const int n = M.X.dim(), m = M.U.dim(), p = M.W.dim();
     if (n == 0) throw ConfigErr("model: the state grid must have at least one dimension");
     if (static_cast<int>(M.dyn.size()) != n) {
         std::ostringstream os;
@@ -1124,12 +1134,135 @@ Model build_model_from_cfg(const Cfg& c) {
     if (n > GMD_MAXD || m > GMD_MAXD || p > GMD_MAXD)
         throw ConfigErr("model: more than " + std::to_string(GMD_MAXD) +
                         " dimensions per grid exceeds the device limit");
-    M.spec = spec_from_cfg(c);
-    M.mode = c.mode == "ofa" ? GM_MODE_OFA_ : GM_MODE_MATRIX_;
-    M.threads = c.threads;
-    M.mem_budget = c.mem_budget;
     M.refresh();
+}
+
+Expr expr_from_nodes(std::vector<XNode> nodes, int32_t root, int n, int m, int p, const std::string& what) {
+    // a node pool as the reference's parser / ExprBuilder lays it out (expr.hpp:36-60):
+    // children precede their parent, so the tree is acyclic by construction
+    const int32_t N = static_cast<int32_t>(nodes.size());
+    auto bad = [&](int32_t i, const std::string& why) -> ConfigErr {
+        return ConfigErr(what + ": node " + std::to_string(i) + " " + why);
+    };
+    if (root < 0 || root >= N) throw ConfigErr(what + ": root outside the node pool");
+    for (int32_t i = 0; i < N; ++i) {
+        const XNode& x = nodes[static_cast<size_t>(i)];
+        const int op = static_cast<int>(x.op);
+        if (op < 0 || op > static_cast<int>(XOp::variable)) throw bad(i, "has an unknown operator");
+        const int arity = x.op == XOp::literal || x.op == XOp::variable ? 0
+                          : x.op == XOp::ite                            ? 3
+                          : (x.op == XOp::neg || (x.op >= XOp::sin && x.op <= XOp::abs)) ? 1
+                                                                                         : 2;
+        for (int k = 0; k < 3; ++k) {
+            const int32_t c = x.kid[k];
+            if (k < arity && (c < 0 || c >= i)) throw bad(i, "has a child outside the preceding nodes");
+        }
+        if (x.op == XOp::variable) {
+            const int lim = x.vclass == 0 ? n : x.vclass == 1 ? m : x.vclass == 2 ? p : -1;
+            if (lim < 0 || x.vindex < 0 || x.vindex >= lim) throw bad(i, "names a variable outside the declared dimensions");
+        }
+    }
+    Expr e;
+    e.nodes = std::move(nodes);
+    e.root = root;
+    e.n = n;
+    e.m = m;
+    e.p = p;
+    return e;
+}
+
+Model build_model_from_parts(const Grid& X, const Grid& U, const Grid& W, std::vector<Expr> dyn, int family,
+                             int mult, double gamma, const std::vector<double>& p1, const std::vector<double>& p2,
+                             Expr pdf, const SpecV& spec, int mode, int threads, uint64_t mem_budget) {
+    Model M;
+    M.X = X;
+    M.U = U;
+    M.W = W;
+    M.dyn = std::move(dyn);
+    if (family < GM_NORMAL || family > GM_CUSTOM) throw ConfigErr("noise: unknown family");
+    M.noise = make_noise(family, p1, p2, gamma, mult);
+    if (family == GM_CUSTOM) M.noise.pdf = std::move(pdf);
+    M.spec = spec;
+    M.mode = mode == GM_MODE_OFA_ ? GM_MODE_OFA_ : GM_MODE_MATRIX_;
+    M.threads = threads;
+    M.mem_budget = mem_budget;
+    finish_model(M);
+    // the Config a save_config of this model writes (config.cpp:270-310): expressions
+    // rendered back to text (constants were substituted when the reference parsed them)
+    Cfg& c = M.cfg;
+    c.states = GridCfg{X.dim(), X.lb, X.ub, X.eta};
+    c.inputs = GridCfg{U.dim(), U.lb, U.ub, U.eta};
+    if (W.dim() > 0) c.dist = GridCfg{W.dim(), W.lb, W.ub, W.eta};
+    for (const Expr& e : M.dyn) c.dynamics.push_back(expr_to_string(e, e.root));
+    static const char* names[] = {"normal", "uniform", "exponential", "beta", "custom"};
+    c.noise_type = names[family];
+    c.noise_mult = mult;
+    c.gamma = gamma;
+    switch (family) {
+        case GM_NORMAL: c.sigma = p1; break;
+        case GM_UNIFORM: c.a = p1; c.b = p2; break;
+        case GM_EXPONENTIAL: c.rate = p1; break;
+        case GM_BETA: c.alpha = p1; c.beta = p2; break;
+        default:
+            c.support_lb = p1;
+            c.support_ub = p2;
+            c.pdf = expr_to_string(M.noise.pdf, M.noise.pdf.root);
+    }
+    c.spec_type = spec.kind == GM_SPEC_SAFETY ? "safety" : spec.kind == GM_SPEC_REACH ? "reachability" : "reach-avoid";
+    c.time_steps = spec.horizon;
+    if (spec.target.dim()) c.target = BoxCfg{spec.target.lo, spec.target.hi};
+    if (spec.avoid.dim()) c.avoid = BoxCfg{spec.avoid.lo, spec.avoid.hi};
+    c.mode = M.mode == GM_MODE_OFA_ ? "ofa" : "matrix";
+    c.threads = threads;
+    c.mem_budget = mem_budget;
     return M;
+}
+
+// save_config, config.cpp:270-310 (same key order and number formatting)
+std::string save_config_text(const Cfg& c) {
+    std::ostringstream os;
+    auto grid = [&](const char* prefix, const GridCfg& g) {
+        os << prefix << ".dim = " << g.dim << ";\n";
+        os << prefix << ".lb = " << fmt_vec(g.lb) << ";\n";
+        os << prefix << ".ub = " << fmt_vec(g.ub) << ";\n";
+        os << prefix << ".eta = " << fmt_vec(g.eta) << ";\n";
+    };
+    grid("states", c.states);
+    grid("inputs", c.inputs);
+    if (c.dist) grid("disturbances", *c.dist);
+    for (size_t i = 0; i < c.dynamics.size(); ++i) os << "dynamics.x" << i << " = " << c.dynamics[i] << ";\n";
+    for (const auto& [k, v] : c.constants) os << "constants." << k << " = " << fmt_shortest(v) << ";\n";
+    os << "noise.type = " << c.noise_type << ";\n";
+    os << "noise.mode = " << (c.noise_mult ? "multiplicative" : "additive") << ";\n";
+    os << "noise.cutting_probability = " << fmt_shortest(c.gamma) << ";\n";
+    if (!c.sigma.empty()) os << "noise.sigma = " << fmt_vec(c.sigma) << ";\n";
+    if (!c.a.empty()) os << "noise.a = " << fmt_vec(c.a) << ";\n";
+    if (!c.b.empty()) os << "noise.b = " << fmt_vec(c.b) << ";\n";
+    if (!c.rate.empty()) os << "noise.rate = " << fmt_vec(c.rate) << ";\n";
+    if (!c.alpha.empty()) os << "noise.alpha = " << fmt_vec(c.alpha) << ";\n";
+    if (!c.beta.empty()) os << "noise.beta = " << fmt_vec(c.beta) << ";\n";
+    if (c.noise_type == "custom") { // engine extension keys (noise.type = custom)
+        os << "noise.pdf = " << c.pdf << ";\n";
+        os << "noise.support.lb = " << fmt_vec(c.support_lb) << ";\n";
+        os << "noise.support.ub = " << fmt_vec(c.support_ub) << ";\n";
+    }
+    os << "spec.type = " << c.spec_type << ";\n";
+    os << "spec.time_steps = " << c.time_steps << ";\n";
+    if (c.target) {
+        os << "target.lb = " << fmt_vec(c.target->lb) << ";\n";
+        os << "target.ub = " << fmt_vec(c.target->ub) << ";\n";
+    }
+    if (c.avoid) {
+        os << "avoid.lb = " << fmt_vec(c.avoid->lb) << ";\n";
+        os << "avoid.ub = " << fmt_vec(c.avoid->ub) << ";\n";
+    }
+    os << "exec.threads = " << c.threads << ";\n";
+    os << "exec.mode = " << c.mode << ";\n";
+    os << "exec.mem_budget = " << c.mem_budget << ";\n";
+    os << "exec.seed = " << c.seed << ";\n";
+    os << "exec.runs = " << c.runs << ";\n";
+    if (!c.output.empty()) os << "exec.output = " << c.output << ";\n";
+    return os.str();
 }
 
 namespace {

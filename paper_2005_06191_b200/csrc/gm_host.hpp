@@ -150,6 +150,16 @@ struct Model {
 };
 
 Model build_model_from_cfg(const Cfg& cfg);
+// make_model (model.cpp:15-29) from already-built parts, e.g. the reference's own
+// SystemModel / Spec / SynthesisOptions handed over the C ABI (gm_model_create)
+Model build_model_from_parts(const Grid& X, const Grid& U, const Grid& W, std::vector<Expr> dyn, int family,
+                             int mult, double gamma, const std::vector<double>& p1, const std::vector<double>& p2,
+                             Expr pdf, const SpecV& spec, int mode, int threads, uint64_t mem_budget);
+// An expression from a reference node pool (Expr::Node, expr.hpp:36-52), validated.
+Expr expr_from_nodes(std::vector<XNode> nodes, int32_t root, int n, int m, int p, const std::string& what);
+void finish_model(Model& M);
+// save_config (config.cpp:270-310)
+std::string save_config_text(const Cfg& c);
 SpecV spec_from_cfg(const Cfg& cfg);
 int tpr_for_width(int64_t R);
 int64_t row_pitch(int64_t R); // row stride of stored matrices (doubles)

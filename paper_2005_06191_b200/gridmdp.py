@@ -469,6 +469,28 @@ def build_matrix(m: SystemModel, threads: int = 0, rows: Optional[tuple] = None)
     return TransitionMatrix(m, h)
 
 
+def read_matrix(path: str, model: SystemModel) -> TransitionMatrix:
+    """read_matrix (io.hpp:18, io.cpp:258-283) onto the device; the container's shape is
+    checked against `model` when the matrix is used with it."""
+    h = C.c_void_p()
+    call("gm_matrix_read", str(path).encode(), C.byref(h))
+    return TransitionMatrix(model, h)
+
+
+def upload_matrix(m: SystemModel, origins: np.ndarray, probs: np.ndarray, row_begin: int = 0) -> TransitionMatrix:
+    """A host TransitionMatrix (origins int64[rows], probs f64[rows, R]) onto the device."""
+    o = np.ascontiguousarray(origins, dtype=np.int64)
+    p = np.ascontiguousarray(probs, dtype=np.float64)
+    h = C.c_void_p()
+    call("gm_matrix_upload", m.handle, C.c_int64(row_begin), C.c_int64(o.size), ptr(o), ptr(p), C.byref(h))
+    return TransitionMatrix(m, h)
+
+
+def save_config(m: SystemModel, path: str) -> None:
+    """save_config (config.hpp:59-60, config.cpp:270-310)."""
+    call("gm_model_save_config", m.handle, str(path).encode())
+
+
 def build_target_hit(m: SystemModel, spec: Spec, threads: int = 0) -> np.ndarray:
     m.use_spec(spec)
     n = m.n_rows()
@@ -664,6 +686,12 @@ def q_values(m: SystemModel) -> np.ndarray:
 
 def query_policy(res: SynthesisResult, input_grid: Grid, state_grid: Grid, x, k: int) -> np.ndarray:
     """Input prescribed at continuous state x and step k (synthesis.cpp:230-239)."""
+    h = res._handle()
+    if h:  # gm_query_policy over the engine result's own grids
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        u = np.empty(input_grid.dim, dtype=np.float64)
+        call("gm_query_policy", h, ptr(x), C.c_int32(x.size), C.c_int32(k), u.ctypes.data_as(C.POINTER(C.c_double)))
+        return u
     T = res.spec.horizon
     if k < 1 or k > T:
         raise IndexError(f"query_policy: step {k} outside [1, {T}]")

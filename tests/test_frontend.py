@@ -166,3 +166,126 @@ def test_dynamics_compile_for_sm100a(case):
     secs = ctypes.c_double()
     _capi.call("gm_model_jit_compile", m.handle, ctypes.c_int32(0), ctypes.byref(secs))
     assert secs.value > 0
+
+
+# ------------------------------------------- the reference's in-memory types (no GPU)
+
+def _sizes_tuple(m):
+    s = m.sizes()
+    return (int(s.n_states), int(s.rows), int(s.row_width), int(s.memory_estimate),
+            [int(s.extents[d]) for d in range(s.n_dim)], int(s.spec_kind), int(s.horizon), int(s.mode))
+
+
+@pytest.mark.parametrize("name", ["robot_reachavoid", "bmw7", "vehicle3", "room5", "traffic5"])
+def test_save_config_round_trip(name, tmp_path):
+    """save_config (config.cpp:270-310) re-parses to the same model (parse(save(c)) == c)."""
+    cfg = tmp_path / "a.cfg"
+    cfg.write_text(MAN["estimate"][name]["config"])
+    m = g.load_config(str(cfg))
+    out = tmp_path / "saved.cfg"
+    g.save_config(m, str(out))
+    m2 = g.load_config(str(out))
+    assert _sizes_tuple(m) == _sizes_tuple(m2)
+    out2 = tmp_path / "saved2.cfg"
+    g.save_config(m2, str(out2))
+    assert out.read_text() == out2.read_text()
+
+
+class ExprNode(ctypes.Structure):
+    _fields_ = [("op", ctypes.c_int32), ("var_class", ctypes.c_int32), ("var_index", ctypes.c_int32),
+                ("kid", ctypes.c_int32 * 3), ("value", ctypes.c_double)]
+
+
+class ExprDesc(ctypes.Structure):
+    _fields_ = [("nodes", ctypes.POINTER(ExprNode)), ("n_nodes", ctypes.c_int32), ("root", ctypes.c_int32)]
+
+
+class GridDesc(ctypes.Structure):
+    _fields_ = [("dim", ctypes.c_int32), ("lb", ctypes.POINTER(ctypes.c_double)),
+                ("ub", ctypes.POINTER(ctypes.c_double)), ("eta", ctypes.POINTER(ctypes.c_double))]
+
+
+class ModelDesc(ctypes.Structure):
+    _fields_ = [("state", GridDesc), ("input", GridDesc), ("disturbance", GridDesc),
+                ("dynamics", ctypes.POINTER(ExprDesc)), ("n_dynamics", ctypes.c_int32),
+                ("noise_family", ctypes.c_int32), ("noise_mode", ctypes.c_int32), ("gamma", ctypes.c_double),
+                ("noise_dim", ctypes.c_int32), ("param1", ctypes.POINTER(ctypes.c_double)),
+                ("param2", ctypes.POINTER(ctypes.c_double)), ("custom_pdf", ExprDesc),
+                ("spec_kind", ctypes.c_int32), ("horizon", ctypes.c_int32),
+                ("target_lo", ctypes.POINTER(ctypes.c_double)), ("target_hi", ctypes.POINTER(ctypes.c_double)),
+                ("avoid_lo", ctypes.POINTER(ctypes.c_double)), ("avoid_hi", ctypes.POINTER(ctypes.c_double)),
+                ("mode", ctypes.c_int32), ("threads", ctypes.c_int32), ("mem_budget", ctypes.c_uint64)]
+
+
+def _dv(*v):
+    return (ctypes.c_double * len(v))(*v)
+
+
+# Expr::Op numbering (expr.hpp:38-45)
+OP = {n: i for i, n in enumerate("add sub mul div pow lt le gt ge eq ne neg sin cos tan asin acos atan exp ln "
+                                 "sqrt abs min max ite literal variable".split())}
+
+
+def _tiny_desc(nodes, root, keep):
+    """tiny.cfg (test_cli.cpp:33-50) as the reference holds it in memory: grids,
+    x0' = 0.7*x0 + 0.4*u0 as a node pool, normal noise, safety T = 3."""
+    arr = (ExprNode * len(nodes))(*nodes)
+    dyn = (ExprDesc * 1)(ExprDesc(arr, len(nodes), root))
+    vals = [_dv(-1.0), _dv(1.0), _dv(0.25), _dv(-0.5), _dv(0.5), _dv(0.5), _dv(0.3)]
+    keep += [arr, dyn, vals]
+    d = ModelDesc()
+    d.state = GridDesc(1, vals[0], vals[1], vals[2])
+    d.input = GridDesc(1, vals[3], vals[4], vals[5])
+    d.disturbance = GridDesc(0, None, None, None)
+    d.dynamics, d.n_dynamics = dyn, 1
+    d.noise_family, d.noise_mode, d.gamma, d.noise_dim = 0, 0, 0.001, 1
+    d.param1, d.param2 = vals[6], None
+    d.spec_kind, d.horizon, d.mode = 0, 3, 0
+    return d
+
+
+def _node(op, value=0.0, vc=0, vi=0, kids=(-1, -1, -1)):
+    return ExprNode(OP[op], vc, vi, (ctypes.c_int32 * 3)(*kids), value)
+
+
+TINY_NODES = [_node("literal", 0.7), _node("variable", vc=0, vi=0), _node("mul", kids=(0, 1, -1)),
+              _node("literal", 0.4), _node("variable", vc=1, vi=0), _node("mul", kids=(3, 4, -1)),
+              _node("add", kids=(2, 5, -1))]
+
+
+def test_model_create_from_reference_types_matches_config(tmp_path):
+    """gm_model_create (the reference's SystemModel / Spec / SynthesisOptions over the
+    C ABI) gives the model the configuration text gives: sizes, windows, and a
+    save_config that re-parses to the same model."""
+    keep = []
+    d = _tiny_desc(TINY_NODES, 6, keep)
+    h = ctypes.c_void_p()
+    _capi.call("gm_model_create", ctypes.byref(d), ctypes.byref(h))
+    ref = g.load_config(str(G.case_cfg("tiny")))
+    s1, s2 = _capi.Sizes(), _capi.Sizes()
+    _capi.call("gm_model_sizes", h, ctypes.byref(s1))
+    _capi.call("gm_model_sizes", ref.handle, ctypes.byref(s2))
+    for f, _ in _capi.Sizes._fields_:
+        a, b = getattr(s1, f), getattr(s2, f)
+        assert (list(a) if hasattr(a, "__len__") else a) == (list(b) if hasattr(b, "__len__") else b), f
+    out = tmp_path / "tiny_saved.cfg"
+    _capi.call("gm_model_save_config", h, str(out).encode())
+    text = out.read_text()
+    assert "dynamics.x0 = 0.7*x0 + 0.4*u0;" in text
+    m2 = g.load_config(str(out))
+    assert _sizes_tuple(m2)[:5] == _sizes_tuple(ref)[:5]
+    _capi.lib.gm_model_free(h)
+
+
+@pytest.mark.parametrize("nodes,root,needle", [
+    (TINY_NODES, 7, "root outside"),
+    ([_node("add", kids=(1, 2, -1)), _node("literal", 1.0), _node("literal", 2.0)], 0, "child outside"),
+    ([_node("variable", vc=1, vi=3)], 0, "variable outside"),
+    ([ExprNode(99, 0, 0, (ctypes.c_int32 * 3)(-1, -1, -1), 0.0)], 0, "unknown operator"),
+])
+def test_model_create_rejects_malformed_expressions(nodes, root, needle):
+    keep = []
+    d = _tiny_desc(nodes, root, keep)
+    h = ctypes.c_void_p()
+    with pytest.raises(_capi.ConfigError, match=needle):
+        _capi.call("gm_model_create", ctypes.byref(d), ctypes.byref(h))
