@@ -299,7 +299,11 @@ static const gmj::Kernels* jit_kernels(gm_model* m, int want, int64_t rows) {
         m->jit_why = "not used: fewer than 2^21 rows in the launch (GM_JIT=1 forces it)";
         return nullptr;
     }
-    const gmj::Kernels* k = gmj::kernels_for(m->M.prog, m->M.X.dim(), want, &why);
+    // the build kernel is specialised to the row shape when it qualifies (GM_JIT_SHAPE=0: off)
+    static const char* js = std::getenv("GM_JIT_SHAPE");
+    const std::string shape =
+        (want & gmj::WANT_BUILD_QS) && !(js && js[0] == '0') ? gmj::shape_defines(m->D) : std::string();
+    const gmj::Kernels* k = gmj::kernels_for(m->M.prog, m->M.X.dim(), want, &why, shape);
     m->jit_used = k != nullptr;
     m->jit_why = k ? std::string() : why;
     m->jit_compile_s = k ? k->compile_s : 0.0;
@@ -558,7 +562,7 @@ void pipeline(gm_model* m, int64_t n, int64_t chunk, cudaStream_t s, Produce&& p
 // A matrix used with a model must have its row shape (and, when read from a
 // container, its grid, input / disturbance counts and window).
 void check_matrix_model(const gm_matrix* tm, const gm_model* m) {
-    bool ok = tm->R == m->M.R && tm->row_end <= m->M.rows();
+    bool ok = tm->R == m->M.R && tm->pitch == m->D.pitch && tm->row_end <= m->M.rows();
     if (ok && tm->has_meta)
         ok = tm->X.lb == m->M.X.lb && tm->X.ub == m->M.X.ub && tm->X.eta == m->M.X.eta && tm->n_u == m->M.n_u() &&
              tm->n_w == m->M.n_w() && tm->extents == m->M.extents;
@@ -607,6 +611,8 @@ void step_states(gm_model* m, gm_matrix* tm, int64_t x0, int64_t x1, const doubl
     m->d_vin.ensure(static_cast<size_t>(std::max<int64_t>(n, 1)), "v_in workspace");
     if (tm) {
         check_matrix_model(tm, m);
+        if (m->M.spec.reach() && !tm->has_t0x)
+            throw ConfigErr("bellman step: a reach specification needs the matrix's target-hit vector");
         if (tm->row_begin > r0 || tm->row_end < r1)
             throw ConfigErr("bellman step: the matrix does not cover the requested states");
         Launch L(gmk::KF_EXPECT_MATRIX, s);
@@ -1031,7 +1037,11 @@ int64_t gm_model_program_size(const gm_model* m) { return static_cast<int64_t>(m
 
 gm_code gm_model_jit_compile(const gm_model* m, int32_t kind, double* seconds, gm_status* st) {
     return guarded(st, [&] {
-        const std::string err = gmj::compile_only(m->M.prog, m->M.X.dim(), kind, seconds);
+        // kind 2 with the model's row-shape specialisation, as the launcher compiles it
+        const char* js = std::getenv("GM_JIT_SHAPE");
+        const std::string shape =
+            kind == 2 && !(js && js[0] == '0') ? gmj::shape_defines(m->M.device_descriptor()) : std::string();
+        const std::string err = gmj::compile_only(m->M.prog, m->M.X.dim(), kind, seconds, shape);
         if (!err.empty()) throw std::runtime_error(err);
     });
 }
@@ -1075,6 +1085,8 @@ double gm_kernel_ms_total(int32_t family) {
     if (family < 0 || family >= gmk::KF_COUNT) return 0.0;
     return g_total_ms[family];
 }
+
+const char* gm_last_kernel_variant(int32_t family) { return gmk::last_variant(family); }
 
 int64_t gm_kernel_launches(int32_t family) {
     if (family < 0 || family >= gmk::KF_COUNT) return 0;
@@ -1641,6 +1653,7 @@ gm_code gm_synthesize_with_matrix(gm_model* m, gm_matrix* tm, const double* t0x,
         prepare(m);
         if (tm->row_begin != 0 || tm->row_end != m->M.rows())
             throw ConfigErr("synthesize_with_matrix: the matrix must cover every row");
+        check_matrix_model(tm, m);
         if (m->M.spec.reach()) {
             gm_status s2;
             if (gm_mask_absorbing(m, tm, &s2) != GM_OK) throw CudaErr(s2.msg);
@@ -1651,6 +1664,7 @@ gm_code gm_synthesize_with_matrix(gm_model* m, gm_matrix* tm, const double* t0x,
                    "t0x");
                 tm->has_t0x = true;
             }
+            ensure_t0x(m, tm); // t0x NULL: built on demand (synthesis.hpp:49-50)
         }
         *out = run_backward(m, tm);
     });

@@ -20,10 +20,35 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 
 namespace gmk {
+
+namespace {
+std::mutex g_var_mu;
+char g_variant[KF_COUNT][96] = {};
+void note_variant(int fam, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+void note_variant(int fam, const char* fmt, ...) {
+    char buf[96];
+    va_list ap;
+    va_start(ap, fmt);
+    std::vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    std::lock_guard<std::mutex> lk(g_var_mu);
+    std::memcpy(g_variant[fam], buf, sizeof buf);
+}
+} // namespace
+
+const char* last_variant(int family) {
+    if (family < 0 || family >= KF_COUNT) return "";
+    return g_variant[family];
+}
+
 
 namespace {
 
@@ -1409,6 +1434,8 @@ void build(const GmDev& D, long long row0, long long nrows, long long* origin_ou
                 int opts_i = wopts;
                 void* args[] = {&Dv,    &row0,       &nrows,    &rb_i,      &npw_i, &ncw_i,
                                 &opts_i, &origin_out, &t0x_out, &probs_out, &d_err};
+                note_variant(KF_BUILD, "k_build_ws<%d,%d>%s", qs ? 1 : 0, ctas,
+                             (jit_ws && jit_ws[qs ? 1 : 0]) ? " (NVRTC)" : "");
                 const cudaError_t e = cudaLaunchKernel(k, dim3(static_cast<unsigned>(std::max<long long>(grid, 1))),
                                                        dim3(kThreads), args, smem, s);
                 if (e != cudaSuccess) throw std::runtime_error(std::string("build: ") + cudaGetErrorString(e));
@@ -1441,6 +1468,7 @@ void build(const GmDev& D, long long row0, long long nrows, long long* origin_ou
     const size_t smem = fixed + (tab == TAB_Q ? q_row : p_row) * static_cast<size_t>(rb);
     const long long batches = (nrows + rb - 1) / rb;
     const GmFastDiv drb = gm_fastdiv(static_cast<uint32_t>(rb));
+    note_variant(KF_BUILD, "k_build<%s>", tab == TAB_Q ? "Q" : "P");
     if (tab == TAB_Q) {
         allow_smem(k_build<TAB_Q>, smem);
         k_build<TAB_Q><<<resident_grid(k_build<TAB_Q>, smem, batches), kThreads, smem, s>>>(
@@ -1481,6 +1509,9 @@ static void launch_ofa(const GmDev& D, const BatchPlan& b, long long nrows, cons
             : up == 7 ? k_expect_ofa_pk<TAB, LS, 7>
                       : k_expect_ofa_pk<TAB, LS, 8>;
     }
+    const bool pk = up && !ou && (pk_mode == 1 || (pk_mode == -1 && per_lane >= 64));
+    note_variant(KF_EXPECT_OFA, "%s<%s,%d,%d>", pk ? "k_expect_ofa_pk" : "k_expect_ofa", TAB == TAB_Q ? "Q" : "P", LS,
+                 pk ? up : u);
     allow_smem(k, b.smem);
     k<<<resident_grid(k, b.smem, batches), kThreads, b.smem, s>>>(D, nrows, b.rb, gm_fastdiv(b.rb), mass, origin,
                                                                  t0x, rowflag, V, v_in);
@@ -1532,6 +1563,7 @@ void expect_matrix(const GmDev& D, long long row0, long long r_lo, long long r_h
 #define GM_ET1(T, UU, MB)                                                                                   \
     {                                                                                                       \
         auto k = k_expect_matrix_et<T, UU, MB>;                                                             \
+        note_variant(KF_EXPECT_MATRIX, "k_expect_matrix_et<%d,%d,%d>", T, UU, MB);                           \
         allow_smem(k, et_smem);                                                                             \
         k<<<resident_grid(k, et_smem, blocks_needed), kThreads, et_smem, s>>>(D, row0, r_lo, r_hi, dn, flags, \
                                                                              probs, origins, t0x, V, v_in); \
@@ -1550,6 +1582,7 @@ void expect_matrix(const GmDev& D, long long row0, long long r_lo, long long r_h
         // (et2 at (14, 6) 17.3 ms, (12, 7) 17.2, (8, 8) 17.1 vs (12, 6) 16.8)
         if (D.tpr == 32 && var == 0) {
             auto k = k_expect_matrix_et2<12, 6>;
+            note_variant(KF_EXPECT_MATRIX, "k_expect_matrix_et2<12,6>");
             allow_smem(k, et_smem);
             const long long pairs = (r_hi - r_lo + 1) / 2;
             k<<<resident_grid(k, et_smem, (pairs + kThreads / 32 - 1) / (kThreads / 32)), kThreads, et_smem, s>>>(
@@ -1565,6 +1598,7 @@ void expect_matrix(const GmDev& D, long long row0, long long r_lo, long long r_h
 #undef GM_ET1
     }
     const size_t smem = (kThreads / 32) * sizeof(double) + (in_smem ? table : 0);
+    note_variant(KF_EXPECT_MATRIX, "k_expect_matrix<%d>", in_smem ? 1 : 0);
     if (in_smem) {
         k_expect_matrix<true><<<resident_grid(k_expect_matrix<true>, smem, blocks_needed), kThreads, smem, s>>>(
             D, row0, r_lo, r_hi, probs, origins, t0x, V, v_in);

@@ -26,6 +26,10 @@ struct BatchPlan {
 };
 BatchPlan plan_batches(const GmDev& D, bool ofa);
 
+// Name of the kernel variant the last launch of a family used (e.g.
+// "k_expect_ofa_pk<P,2,5>"), "" if none: tests check which path really ran.
+const char* last_variant(int family);
+
 void absorb_flags(const GmDev& D, uint8_t* d_flags, cudaStream_t s);
 void zero_absorbing(const GmDev& D, double* d_v, cudaStream_t s);
 

@@ -563,6 +563,33 @@ __device__ __forceinline__ void build_prologue(const GmDev& D, const GmIns* spro
 // HBM writes for this row pattern (scripts/store_probe.cu).
 // QS = per-warp Q scratch + element table (n_lines and W_last small enough);
 // otherwise rows are expanded by the incremental slab walk, q = P[a]*mm[j] per term.
+#ifdef GM_FILL_WL
+// ld.shared.f64 at a register address plus an immediate offset (one LDS, no address math)
+template <int OFF>
+__device__ __forceinline__ double lds_imm(unsigned addr) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(addr), "n"(OFF));
+    return v;
+}
+// The lane's elements t = lane + 32 i of one row, i = 0 .. pitch/32 - 1, unrolled at
+// compile time: element i = s + PER*b is Q[L(s) + DL*b] * ml[k(s)], one LDS, one DMUL,
+// one evict-first STG with immediate offsets; elements past R (row padding) store +0.0.
+template <int I>
+struct FillRow {
+    static __device__ __forceinline__ void run(const unsigned* fq, const double* mv, double* o, int lane) {
+        constexpr int PER = GM_FILL_PER, S = I % PER, B = I / PER;
+        constexpr int OFF = 8 * (32 * PER / GM_FILL_WL) * B;
+        if constexpr (32 * I + 31 < GM_FILL_R) {
+            __stcs(o + 32 * I, lds_imm<OFF>(fq[S]) * mv[S]);
+        } else {
+            const double q = lane + 32 * I < GM_FILL_R ? lds_imm<OFF>(fq[S]) : 0.0;
+            __stcs(o + 32 * I, q * mv[S]);
+        }
+        if constexpr (I + 1 < GM_FILL_PITCH / 32) FillRow<I + 1>::run(fq, mv, o, lane);
+    }
+};
+#endif
+
 #if !defined(__CUDACC_RTC__) || defined(GM_JIT_BUILD)
 template <bool QS, int MINB = 3>
 __global__ void __launch_bounds__(kThreads, MINB) k_build_ws(GmDev D, long long row0, long long nrows, int rb,
@@ -592,6 +619,22 @@ __global__ void __launch_bounds__(kThreads, MINB) k_build_ws(GmDev D, long long 
         if (threadIdx.x < kThreads / 32) g_sm[offQs + threadIdx.x * (nl + 1) + nl] = 0.0;
     }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef GM_FILL_WL
+    // Row shape fixed at run-time compilation (NVRTC, gm_jit.cpp shape_defines): the
+    // lane -> element map does not depend on the row, so each lane's Q-scratch index
+    // and last-axis cell of its first PER elements are kernel-lifetime registers;
+    // element i = s + PER*b of the lane reads Q[fq[s] + DL*b] * ml[fm[s]]
+    // (32*PER is a multiple of Wl, so the cell repeats with period PER).
+    constexpr int F_WL = GM_FILL_WL, F_WM = GM_FILL_WM, F_NL = GM_FILL_NL, F_PER = GM_FILL_PER;
+    constexpr int F_R = GM_FILL_R, F_NIT = GM_FILL_PITCH / 32, F_DL = 32 * F_PER / F_WL, F_NQ = (F_NL + 31) / 32;
+    unsigned fq[F_PER]; // shared-window byte addresses of Q[L(s)] in this warp's scratch
+    {
+        const unsigned sm0 = static_cast<unsigned>(__cvta_generic_to_shared(g_sm));
+#pragma unroll
+        for (int s = 0; s < F_PER; ++s)
+            fq[s] = sm0 + 8u * static_cast<unsigned>(offQs + warp * (F_NL + 1) + (lane + 32 * s) / F_WL);
+    }
+#endif
     const int np = npw * 32, nc = ncw * 32;
     const int role = warp < npw ? 0 : (warp < npw + ncw ? 1 : 2); // producer, consumer, filler
     const int ct = threadIdx.x - np;
@@ -672,6 +715,20 @@ __global__ void __launch_bounds__(kThreads, MINB) k_build_ws(GmDev D, long long 
                 }
 #endif
                 if (QS) {
+#ifdef GM_FILL_WL
+                    // line prefixes Q[L] = P[a] * mm[j] (abstraction.cpp:150-159 association)
+#pragma unroll
+                    for (int c = 0; c < F_NQ; ++c) {
+                        const int L = lane + 32 * c; // constant divisors: multiply-shift
+                        if (F_NL % 32 == 0 || L < F_NL) Qs[L] = Pr[L / F_WM] * m[D.mm_off + L % F_WM];
+                    }
+                    __syncwarp();
+                    double mv[F_PER];
+#pragma unroll
+                    for (int s2 = 0; s2 < F_PER; ++s2) mv[s2] = m[D.ml_off + (lane + 32 * s2) % F_WL];
+                    FillRow<0>::run(fq, mv, out + lane, lane);
+                    __syncwarp();
+#else
                     for (int L = lane; L < nl; L += 32) {
                         const int a = D.div_Wm.div(L), j = L - a * D.Wm;
                         Qs[L] = Pr[a] * m[D.mm_off + j];
@@ -689,6 +746,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_build_ws(GmDev D, long long 
                                       *reinterpret_cast<const double*>(mb + (ev >> 16)));
                     }
                     __syncwarp();
+#endif
                 } else {
                     Walk wk = wk0;
 #pragma unroll 4

@@ -172,7 +172,7 @@ int cmd_synthesize(const Args& a) {
         std::cout << "sweep_terms_per_s: " << terms / (sweep_ms / 1e3) << "\n";
         std::cout << "roofline_frac: " << terms * 8 / (sweep_ms / 1e3) / 1e9 / (hbm_peak_gbs() * gpus) << "\n";
     }
-    if (build_ms > 0)
+    if (sz.mode == GM_MODE_MATRIX && build_ms > 0)
         std::cout << "probs_per_s: " << static_cast<double>(sz.rows) * static_cast<double>(sz.row_width) / (build_ms / 1e3)
                   << "\n";
     // output path: exec.output / -o, default results.bin (gridmdp_main.cpp:113)

@@ -168,6 +168,19 @@ def test_dynamics_compile_for_sm100a(case):
     assert secs.value > 0
 
 
+@pytest.mark.parametrize("workload", ["C2b", "C1", "C3u"])
+def test_shape_specialised_build_compiles(workload):
+    """The stage (i) build kernel specialised to the row shape (gm_jit.cpp shape_defines,
+    gm_rowdev.cuh GM_FILL_*) compiles for sm_100a with NVRTC (no GPU needed)."""
+    from paper_2005_06191_b200 import _capi
+    from paper_2005_06191_b200 import gridmdp as g
+    from paper_2005_06191_b200 import workloads as W
+    m = g.parse_config(W.WORKLOADS[workload](), workload)
+    secs = ctypes.c_double()
+    _capi.call("gm_model_jit_compile", m.handle, ctypes.c_int32(2), ctypes.byref(secs))
+    assert secs.value > 0
+
+
 # ------------------------------------------- the reference's in-memory types (no GPU)
 
 def _sizes_tuple(m):

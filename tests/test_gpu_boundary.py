@@ -76,7 +76,7 @@ def test_upload_host_matrix_bellman_step(case):
 
 def test_matrix_of_another_model_is_rejected(tmp_path):
     m = _model("fixture2d_ra")
-    tm = g.read_matrix(str(_dump("fixture2d_safety", "matrix", tmp_path)), m)
+    tm = g.read_matrix(str(_dump("tiny", "matrix", tmp_path)), m)
     with pytest.raises(g.ConfigError, match="does not match the model"):
         g.synthesize_with_matrix(m, tm, None, m.spec)
 

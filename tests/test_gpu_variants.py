@@ -23,6 +23,8 @@ sys.path.insert(0, {repo!r}); sys.path.insert(0, {tests!r})
 import numpy as np
 import golden_io as G
 from paper_2005_06191_b200 import gridmdp as g
+from paper_2005_06191_b200 import _capi
+ofa = lambda: _capi.lib.gm_last_kernel_variant(_capi.KF_EXPECT_OFA).decode()
 for case in {cases!r}:
     e = G.manifest()["cases"][case]
     h = hashlib.sha256()
@@ -33,7 +35,7 @@ for case in {cases!r}:
         r = g.synthesize(m, m.spec, g.SynthesisOptions(mode=mode))
         h.update(np.ascontiguousarray(r.values).tobytes()); h.update(np.ascontiguousarray(r.policy).tobytes())
         h.update(np.ascontiguousarray(r.worst_dist).tobytes())
-    print(case, h.hexdigest())
+    print(case, h.hexdigest(), ofa())
 # R = 729 rows (a warp per row in the stored-matrix sweep): vehicle3 at eta/4 on a
 # 2 x 2 x 3 m corner of its grid
 from paper_2005_06191_b200 import workloads as W
@@ -50,7 +52,9 @@ assert m.sizes().row_width == 729
 h = hashlib.sha256()
 r = g.synthesize(m)
 h.update(np.ascontiguousarray(r.values).tobytes()); h.update(np.ascontiguousarray(r.policy).tobytes())
-print("vehicle_r729", h.hexdigest())
+r = g.synthesize(m, m.spec, g.SynthesisOptions(mode="ofa"))
+h.update(np.ascontiguousarray(r.values).tobytes())
+print("vehicle_r729", h.hexdigest(), ofa())
 """
 
 SETTINGS = [
@@ -72,7 +76,17 @@ def digests(env_extra):
     env = dict(os.environ, **env_extra)
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
-    return dict(line.split() for line in out.stdout.strip().splitlines())
+    return {c: (d, v) for c, d, v in (line.split() for line in out.stdout.strip().splitlines())}
+
+
+def _digest(rows):
+    return {c: d for c, (d, _) in rows.items()}
+
+
+# the hoisted last-axis cell needs an unroll U in [4, 8] that is a multiple of the
+# lane's cell period (launch_ofa): fixture2d_ra and ref_vehicle3_desk have one;
+# exp_dist (period 13) and vehicle_r729 (period 9) keep the plain kernel
+PK_CASES = {"fixture2d_ra", "ref_vehicle3_desk"}
 
 
 @pytest.fixture(scope="module")
@@ -83,10 +97,16 @@ def default():
 @pytest.mark.parametrize("knob", SETTINGS, ids=lambda d: ",".join(f"{k}={v}" for k, v in d.items()))
 def test_variant_bit_identical_to_default(default, knob):
     env = {"GM_JIT": "0", **knob}
-    assert digests(env) == default
+    got = digests(env)
+    assert _digest(got) == _digest(default)
+    if knob.get("GM_OFA_PK") == "1":  # the forced kernel really ran where it applies
+        for c, (_, v) in got.items():
+            assert v.startswith("k_expect_ofa_pk<") == (c in PK_CASES), (c, v)
+    if "GM_OFA_TABLE" in knob:
+        assert all(",P," in v or "<P," in v for _, v in got.values()), got
 
 
 def test_row_pitch_does_not_change_results(default):
     """Rows padded to another granule (GM_PITCH_GRANULE) change the layout only."""
     got = digests({"GM_JIT": "0", "GM_PITCH_GRANULE": "1"})
-    assert got == default
+    assert _digest(got) == _digest(default)
