@@ -768,6 +768,10 @@ gm_result* run_backward(gm_model* m, gm_matrix* tm, PhaseTimer* pt = nullptr) {
         ck(cudaMemcpyAsync(r->worst.data() + nx * k, wst.p + nx * k, nx * 4, cudaMemcpyDeviceToHost, m->aux), "worst");
         ck(cudaStreamSynchronize(m->aux), "column copy");
     };
+    // small tables (<= 64 MB) stay on the device until the sweep ends: the T steps are
+    // enqueued back to back with no host synchronisation between them (launch-bound
+    // configurations); larger ones stream each column out under the next step
+    const bool defer = (nx * (T + 1) * 8 + 2 * nx * T * 4) <= (size_t(64) << 20);
     if (pt) pt->mark(1);
     for (int k = T - 1; k >= 0; --k) {
         step_states(m, tm, 0, n_x, vals.p + nx * (k + 1), vals.p + nx * k, pol.p + nx * k, wst.p + nx * k, m->stream);
@@ -775,7 +779,7 @@ gm_result* run_backward(gm_model* m, gm_matrix* tm, PhaseTimer* pt = nullptr) {
         if (k == T - 1) {
             ck(cudaStreamSynchronize(m->stream), "bellman step");
             raise_device_error(m);
-        } else {
+        } else if (!defer) {
             copy_column(k + 1, done[(k + 1) & 1]); // step k runs meanwhile
         }
     }
@@ -783,7 +787,14 @@ gm_result* run_backward(gm_model* m, gm_matrix* tm, PhaseTimer* pt = nullptr) {
     ck(cudaStreamSynchronize(m->stream), "bellman sweep");
     raise_device_error(m);
     if (pt) pt->finish();
-    if (T > 0) copy_column(0, done[0]);
+    if (defer && T > 0) {
+        join_sizer();
+        ck(cudaMemcpy(r->values.data(), vals.p, nx * T * 8, cudaMemcpyDeviceToHost), "values");
+        ck(cudaMemcpy(r->policy.data(), pol.p, nx * T * 4, cudaMemcpyDeviceToHost), "policy");
+        ck(cudaMemcpy(r->worst.data(), wst.p, nx * T * 4, cudaMemcpyDeviceToHost), "worst");
+    } else if (T > 0) {
+        copy_column(0, done[0]);
+    }
     join_sizer();
     if (reach) {
         r->absorbing.resize(nx);
@@ -1651,9 +1662,9 @@ gm_code gm_synthesize_with_matrix(gm_model* m, gm_matrix* tm, const double* t0x,
     return guarded(st, [&] {
         check_spec(m->M.spec, m->M.X);
         prepare(m);
+        check_matrix_model(tm, m);
         if (tm->row_begin != 0 || tm->row_end != m->M.rows())
             throw ConfigErr("synthesize_with_matrix: the matrix must cover every row");
-        check_matrix_model(tm, m);
         if (m->M.spec.reach()) {
             gm_status s2;
             if (gm_mask_absorbing(m, tm, &s2) != GM_OK) throw CudaErr(s2.msg);

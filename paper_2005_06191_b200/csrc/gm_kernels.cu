@@ -799,23 +799,23 @@ __global__ void __launch_bounds__(kThreads) k_maxmin(GmDev D, long long x0, long
     const bool reach = D.spec_kind != GM_SPEC_SAFETY;
     const bool absorbed = valid && reach && D.absorb != nullptr && D.absorb[ix];
     double best = -INFINITY;
-    long long bu = 0, bw = 0;
+    uint32_t bu = 0, bw = 0; // policy / worst_dist are uint32 tables (synthesis.hpp:21)
     if (valid && !absorbed) {
         const double* base = v_in + xi * D.n_u * D.n_w;
         for (long long iu = lane; iu < D.n_u; iu += L) {
             double mn = INFINITY;
-            long long mw = 0;
+            uint32_t mw = 0;
             const double* q = base + iu * D.n_w;
             for (long long iw = 0; iw < D.n_w; ++iw) {
                 const double v = q[iw];
                 if (v < mn) {
                     mn = v;
-                    mw = iw;
+                    mw = static_cast<uint32_t>(iw);
                 }
             }
             if (mn > best) {
                 best = mn;
-                bu = iu;
+                bu = static_cast<uint32_t>(iu);
                 bw = mw;
             }
         }
@@ -823,8 +823,8 @@ __global__ void __launch_bounds__(kThreads) k_maxmin(GmDev D, long long x0, long
     if (L > 1) {
         for (int off = L >> 1; off >= 1; off >>= 1) {
             const double ob = __shfl_xor_sync(0xffffffffu, best, off);
-            const long long ou = __shfl_xor_sync(0xffffffffu, bu, off);
-            const long long ow = __shfl_xor_sync(0xffffffffu, bw, off);
+            const uint32_t ou = __shfl_xor_sync(0xffffffffu, bu, off);
+            const uint32_t ow = __shfl_xor_sync(0xffffffffu, bw, off);
             if (ob > best || (ob == best && ou < bu)) {
                 best = ob;
                 bu = ou;
@@ -1636,11 +1636,20 @@ unsigned long long count_positive(const double* p, long long n, unsigned long lo
 void maxmin(const GmDev& D, long long x0, long long nx, const double* v_in, double* v_out,
             uint32_t* pol, uint32_t* wst, cudaStream_t s) {
     if (nx <= 0) return;
+    // L lanes per state, each scanning about three inputs (lane-strided, increasing u),
+    // then a lowest-index-on-ties butterfly: C2b (n_u = 25) 8 lanes
     const long long nuw = D.n_u * D.n_w;
-    if (nuw <= 8) {
-        k_maxmin<1><<<grid_for(nx, kThreads), kThreads, 0, s>>>(D, x0, nx, v_in, v_out, pol, wst);
-    } else {
-        k_maxmin<32><<<grid_for(nx * 32, kThreads), kThreads, 0, s>>>(D, x0, nx, v_in, v_out, pol, wst);
+    int L = 1;
+    while (L < 32 && 2 * L <= D.n_u / 3) L *= 2;
+    if (nuw <= 8) L = 1;
+    note_variant(KF_MAXMIN, "k_maxmin<%d>", L);
+    switch (L) {
+#define GM_MM(LL)                                                                                   \
+    case LL:                                                                                        \
+        k_maxmin<LL><<<grid_for(nx * LL, kThreads), kThreads, 0, s>>>(D, x0, nx, v_in, v_out, pol, wst); \
+        break;
+        GM_MM(1) GM_MM(2) GM_MM(4) GM_MM(8) GM_MM(16) GM_MM(32)
+#undef GM_MM
     }
     check_launch("maxmin");
 }
