@@ -51,6 +51,16 @@ def peaks():
     return 6650.0, "fallback"
 
 
+def ncu_l1tex(workload: str):
+    """L1/TEX utilisation of the OFA consumer kernel from the newest committed ncu capture
+    (profiles/*/ncu_l1tex.json, scripts/ncu_summary.py --l1tex), else None."""
+    for f in sorted(REPO.glob("profiles/*/ncu_l1tex.json"), reverse=True):
+        for k, e in json.loads(f.read_text()).items():
+            if e.get("workload") == workload:
+                return dict(e, kernel=k, source=str(f.relative_to(REPO)))
+    return None
+
+
 def ncu_traffic(kernel: str, workload: str):
     """DRAM bytes per launch of `kernel` from the newest committed ncu --set full capture
     (profiles/*/ncu_traffic.json, written by scripts/ncu_summary.py --traffic), else None."""
@@ -510,7 +520,11 @@ def main():
                             "v_exchange": ("none" if world == 1 else
                                            f"halo p2p ({xp.halo_states} of {xp.allgather_states} states)"
                                            if xp is not None else "all-gather per step"),
-                            "rows": int(st.rows), "row_width": int(st.row_width), "horizon": int(st.horizon)}
+                            "rows": int(st.rows), "row_width": int(st.row_width), "horizon": int(st.horizon),
+                            # OFA reads (almost) nothing from DRAM: its ceiling is the L1/TEX pipe that
+                            # serves the V gathers and the shared-memory tables (ncu, committed profile)
+                            "roofline_l1tex": ncu_l1tex(wname),
+                            "kernel_variant": _capi.lib.gm_last_kernel_variant(_capi.KF_EXPECT_OFA).decode()}
             bet.release()
         line["extra"] = extra
 

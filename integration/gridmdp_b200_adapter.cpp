@@ -23,6 +23,7 @@
 
 #include "gridmdp_b200.h"
 
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -198,11 +199,38 @@ TargetHitVector build_target_hit(const SystemModel& m, const Spec& spec, int thr
     return t0x;
 }
 
+// Devices of this process for synthesize: GRIDMDP_B200_DEVICES="0,1,2,3" (the reference's
+// SynthesisOptions has no device field; the variable keeps its signature unchanged).
+std::vector<int32_t> adapter_devices() {
+    std::vector<int32_t> out;
+    const char* e = std::getenv("GRIDMDP_B200_DEVICES");
+    if (!e || !*e) return out;
+    std::string s(e);
+    size_t pos = 0;
+    while (pos <= s.size()) {
+        const size_t c = s.find(',', pos);
+        out.push_back(static_cast<int32_t>(std::stoi(s.substr(pos, c == std::string::npos ? std::string::npos : c - pos))));
+        if (c == std::string::npos) break;
+        pos = c + 1;
+    }
+    return out;
+}
+
 SynthesisResult synthesize(const SystemModel& m, const Spec& spec, const SynthesisOptions& opts) {
     const ModelHandle mh(m, spec, opts);
     ResultHandle r;
     gm_status st;
-    ok(gm_synthesize(mh.h, &r.h, &st), st); // budget check, build, mask, T0x, backward
+    const std::vector<int32_t> dev = adapter_devices();
+    if (dev.size() > 1) { // state shards over the listed GPUs, V exchanged by NCCL (parallel.hpp:23-51's role)
+        const char* tp = std::getenv("GRIDMDP_B200_TRANSPORT");
+        const int32_t transport = tp && std::string(tp) == "peer" ? GM_XPORT_PEER : GM_XPORT_NCCL;
+        ok(gm_synthesize_multi(mh.h, static_cast<int32_t>(dev.size()), dev.data(), GM_XCHG_AUTO, transport, &r.h,
+                               nullptr, &st),
+           st);
+    } else {
+        if (dev.size() == 1) ok(gm_set_device(dev[0], &st), st);
+        ok(gm_synthesize(mh.h, &r.h, &st), st); // budget check, build, mask, T0x, backward
+    }
     return to_result(m, spec, r.h);
 }
 

@@ -303,7 +303,7 @@ static const gmj::Kernels* jit_kernels(gm_model* m, int want, int64_t rows) {
     static const char* js = std::getenv("GM_JIT_SHAPE");
     const std::string shape =
         (want & gmj::WANT_BUILD_QS) && !(js && js[0] == '0') ? gmj::shape_defines(m->D) : std::string();
-    const gmj::Kernels* k = gmj::kernels_for(m->M.prog, m->M.X.dim(), want, &why, shape);
+    const gmj::Kernels* k = gmj::kernels_for(m->M.prog, m->M.X.dim(), m->M.U.dim(), m->M.W.dim(), want, &why, shape);
     m->jit_used = k != nullptr;
     m->jit_why = k ? std::string() : why;
     m->jit_compile_s = k ? k->compile_s : 0.0;
@@ -1052,7 +1052,7 @@ gm_code gm_model_jit_compile(const gm_model* m, int32_t kind, double* seconds, g
         const char* js = std::getenv("GM_JIT_SHAPE");
         const std::string shape =
             kind == 2 && !(js && js[0] == '0') ? gmj::shape_defines(m->M.device_descriptor()) : std::string();
-        const std::string err = gmj::compile_only(m->M.prog, m->M.X.dim(), kind, seconds, shape);
+        const std::string err = gmj::compile_only(m->M.prog, m->M.X.dim(), m->M.U.dim(), m->M.W.dim(), kind, seconds, shape);
         if (!err.empty()) throw std::runtime_error(err);
     });
 }

@@ -32,7 +32,7 @@ enum Want { WANT_PROLOGUE = 1, WANT_BUILD_NOQS = 2, WANT_BUILD_QS = 4 };
 // is its own NVRTC program, compiled on first use: ~2 s k_prologue, ~5 s
 // k_build_ws), or nullptr with the reason in *why (NVRTC missing, compile or
 // load failure, GM_JIT=0).
-const Kernels* kernels_for(const gmh::Program& P, int n, int want, std::string* why,
+const Kernels* kernels_for(const gmh::Program& P, int n, int m, int p, int want, std::string* why,
                            const std::string& shape = "");
 
 // #defines that specialise the per-warp-Q build kernel (k_build_ws<true>) to one row
@@ -42,6 +42,7 @@ std::string shape_defines(const GmDev& D);
 // NVRTC compile of one kernel kind (0 k_prologue, 1 k_build_ws<false>, 2
 // k_build_ws<true>) without loading it: "" on success, else the compiler log.
 // Needs no GPU (tests run it on the build host).
-std::string compile_only(const gmh::Program& P, int n, int kind, double* seconds, const std::string& shape = "");
+std::string compile_only(const gmh::Program& P, int n, int m, int p, int kind, double* seconds,
+                         const std::string& shape = "");
 
 } // namespace gmj

@@ -23,6 +23,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -1303,6 +1304,25 @@ void prologue(const GmDev& D, long long row0, long long nrows, int flags, long l
     check_launch("prologue");
 }
 
+// Resident CTAs per SM of a kernel at a dynamic shared-memory size, cached: the
+// occupancy query is a driver call that costs microseconds per launch (small,
+// launch-bound sweeps launch two kernels per step).
+static int occupancy(const void* kernel, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, size_t>, int> cache;
+    const auto key = std::make_pair(kernel, smem); // every device of the node is a B200
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) return it->second;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
+    std::lock_guard<std::mutex> lk(mu);
+    cache[key] = per_sm;
+    return per_sm;
+}
+
 static int num_sms() {
     static int sms = 0;
     if (!sms) {
@@ -1317,8 +1337,7 @@ static int num_sms() {
 // persistent grids: resident CTAs per SM x SMs, capped by the work
 template <class K>
 static int resident_grid(K kernel, size_t smem, long long batches, int reserve = 0) {
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
+    int per_sm = occupancy(reinterpret_cast<const void*>(kernel), smem);
     per_sm -= reserve; // slots left for the row prologue running concurrently on the aux stream
     if (per_sm < 1) per_sm = 1;
     long long g = static_cast<long long>(per_sm) * num_sms();
@@ -1387,13 +1406,13 @@ void build(const GmDev& D, long long row0, long long nrows, long long* origin_ou
     static const char* bw = std::getenv("GM_BUILD_WS"); // 0: single-role k_build
     if (!(bw && bw[0] == '0')) {
         // three-role pipelined build: layout of k_build_ws in doubles
-        // GM_BUILD_OPTS=16: per-role cycle totals (printf). The store-suppressing timing
-        // bits 32 / 64 write wrong rows and exist only in GM_DIAG builds.
+        // GM_BUILD_OPTS (GM_DIAG builds only): 16 = per-role cycle totals (printf),
+        // 32 / 64 = constant / no stores (timing only, wrong rows).
         static const char* bo2 = std::getenv("GM_BUILD_OPTS");
         const int wopts = bo2 ? std::atoi(bo2) : 0;
 #ifndef GM_DIAG
-        if (wopts & 96)
-            throw std::runtime_error("build: GM_BUILD_OPTS bits 32/64 are timing diagnostics of GM_DIAG builds only");
+        if (wopts & 112)
+            throw std::runtime_error("build: GM_BUILD_OPTS (16 / 32 / 64) are diagnostics of GM_DIAG builds only");
 #endif
         const bool qs = build_uses_qs(D);
         const size_t fixed_d = D.n_ins + D.n_lits + 3 + (qs ? (D.pitch + 1) / 2 + (kThreads / 32) * (D.n_lines + 1) : 0);
@@ -1425,8 +1444,7 @@ void build(const GmDev& D, long long row0, long long nrows, long long* origin_ou
                                           : (qs ? reinterpret_cast<const void*>(&k_build_ws<true, 3>)
                                                 : reinterpret_cast<const void*>(&k_build_ws<false, 3>)));
                 if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                int per_sm = 0;
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, smem);
+                const int per_sm = occupancy(k, smem);
                 const long long grid = std::min<long long>(batches, static_cast<long long>(std::max(per_sm, 1)) *
                                                                         num_sms());
                 GmDev Dv = D;
@@ -1513,6 +1531,10 @@ static void launch_ofa(const GmDev& D, const BatchPlan& b, long long nrows, cons
     note_variant(KF_EXPECT_OFA, "%s<%s,%d,%d>", pk ? "k_expect_ofa_pk" : "k_expect_ofa", TAB == TAB_Q ? "Q" : "P", LS,
                  pk ? up : u);
     allow_smem(k, b.smem);
+    // GM_OFA_CARVEOUT (tuning): shared-memory share of the unified L1/shared storage, in
+    // percent; more CTAs per SM against fewer L1 hits for the V gathers
+    static const char* oc = std::getenv("GM_OFA_CARVEOUT");
+    if (oc) cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(oc));
     k<<<resident_grid(k, b.smem, batches), kThreads, b.smem, s>>>(D, nrows, b.rb, gm_fastdiv(b.rb), mass, origin,
                                                                  t0x, rowflag, V, v_in);
 }

@@ -13,6 +13,19 @@ enum : int { PF_SKIP_ABSORBED = 1, PF_T0X = 2, PF_MASSES = 4 };
 #endif
 
 constexpr int kThreads = 256;
+
+// Grid dimensions of the row code: compile-time constants in the kernels compiled at
+// run time for one model (gm_jit.cpp: loops unroll, the per-row x / u / w / mu
+// arrays live in registers instead of local memory), the descriptor's otherwise.
+#ifdef GM_JIT_NDIM
+#define GM_DN(D) GM_JIT_NDIM
+#define GM_DM(D) GM_JIT_MDIM
+#define GM_DP(D) GM_JIT_PDIM
+#else
+#define GM_DN(D) ((D).n)
+#define GM_DM(D) ((D).m)
+#define GM_DP(D) ((D).p)
+#endif
 constexpr double kIdxTol = 1e-9; // abstraction.cpp:10
 
 // x86-64 cvttsd2si semantics of static_cast<int64_t>(double) in the reference:
@@ -34,19 +47,19 @@ __device__ void decode_row(const GmDev& D, long long row, long long& ix, double*
         const int x32 = D.div_nu.div(pr), iu = pr - x32 * static_cast<int>(D.n_u);
         ix = x32;
         int rem = x32;
-        for (int d = 0; d < D.n; ++d) {
+        for (int d = 0; d < GM_DN(D); ++d) {
             const int j = D.div_xs[d].div(rem);
             rem -= j * static_cast<int>(D.xstride[d]);
             x[d] = D.xlb[d] + static_cast<double>(j) * D.xeta[d];
         }
         rem = iu;
-        for (int d = 0; d < D.m; ++d) {
+        for (int d = 0; d < GM_DM(D); ++d) {
             const int j = D.div_us[d].div(rem);
             rem -= j * static_cast<int>(D.ustride[d]);
             u[d] = D.ulb[d] + static_cast<double>(j) * D.ueta[d];
         }
         rem = iw;
-        for (int d = 0; d < D.p; ++d) {
+        for (int d = 0; d < GM_DP(D); ++d) {
             const int j = D.div_ws[d].div(rem);
             rem -= j * static_cast<int>(D.wstride[d]);
             w[d] = D.wlb[d] + static_cast<double>(j) * D.weta[d];
@@ -58,19 +71,19 @@ __device__ void decode_row(const GmDev& D, long long row, long long& ix, double*
     const long long iu = pr % D.n_u;
     ix = pr / D.n_u;
     long long rem = ix;
-    for (int d = 0; d < D.n; ++d) {
+    for (int d = 0; d < GM_DN(D); ++d) {
         const long long j = rem / D.xstride[d];
         rem -= j * D.xstride[d];
         x[d] = D.xlb[d] + static_cast<double>(j) * D.xeta[d];
     }
     rem = iu;
-    for (int d = 0; d < D.m; ++d) {
+    for (int d = 0; d < GM_DM(D); ++d) {
         const long long j = rem / D.ustride[d];
         rem -= j * D.ustride[d];
         u[d] = D.ulb[d] + static_cast<double>(j) * D.ueta[d];
     }
     rem = iw;
-    for (int d = 0; d < D.p; ++d) {
+    for (int d = 0; d < GM_DP(D); ++d) {
         const long long j = rem / D.wstride[d];
         rem -= j * D.wstride[d];
         w[d] = D.wlb[d] + static_cast<double>(j) * D.weta[d];
@@ -334,9 +347,9 @@ __device__ __forceinline__ long long slab_origin(const GmDev& D, int d, double m
 
 __device__ __forceinline__ bool in_box(const GmDev& D, const double* p, const double* lo,
                                        const double* hi) {
-    for (int d = 0; d < D.n; ++d)
+    for (int d = 0; d < GM_DN(D); ++d)
         if (!(p[d] >= lo[d])) return false;
-    for (int d = 0; d < D.n; ++d)
+    for (int d = 0; d < GM_DN(D); ++d)
         if (!(p[d] <= hi[d])) return false;
     return true;
 }
@@ -397,14 +410,14 @@ __global__ void __launch_bounds__(kThreads) k_prologue(GmDev D, long long row0, 
     }
     long long org[GMD_MAXD];
     long long flat = 0;
-    for (int d = 0; d < D.n; ++d) {
+    for (int d = 0; d < GM_DN(D); ++d) {
         org[d] = slab_origin(D, d, mu[d]);
         flat += org[d] * D.xstride[d];
     }
     if (origin_out) origin_out[i] = flat;
     bool ok = true;
     if (flags & PF_MASSES) { // per-cell form: keeps this kernel at 64 registers (axis_masses: 80)
-        for (int d = 0; d < D.n; ++d) {
+        for (int d = 0; d < GM_DN(D); ++d) {
             const double scale = D.mult ? x[d] : 1.0;
             const double half = 0.5 * D.xeta[d];
             double* md = mass_out + static_cast<long long>(D.mass_off[d]) * nrows + i;
@@ -418,7 +431,7 @@ __global__ void __launch_bounds__(kThreads) k_prologue(GmDev D, long long row0, 
         double p = 0.0;
         if (!absorbed) { // cell_probability_impl (noise.cpp:251-257) over the target box
             p = 1.0;
-            for (int d = 0; d < D.n; ++d) {
+            for (int d = 0; d < GM_DN(D); ++d) {
                 const double scale = D.mult ? x[d] : 1.0;
                 p *= tmass(D, d, D.tlo[d], D.thi[d], mu[d], scale, ok);
                 if (p == 0.0) break;
@@ -521,7 +534,7 @@ __device__ __forceinline__ void build_prologue(const GmDev& D, const GmIns* spro
             if (run_dynamics(D, sprog, slits, x, u, w, mu)) {
                 ok = 1.0;
                 long long flat = 0;
-                for (int d = 0; d < D.n; ++d) {
+                for (int d = 0; d < GM_DN(D); ++d) {
                     const long long o = slab_origin(D, d, mu[d]);
                     pb.org[i * pb.n + d] = static_cast<int>(o);
                     flat += o * D.xstride[d];
@@ -535,7 +548,7 @@ __device__ __forceinline__ void build_prologue(const GmDev& D, const GmIns* spro
                     bool bok = true;
                     if (!absorbed) {
                         p = 1.0;
-                        for (int d = 0; d < D.n; ++d) {
+                        for (int d = 0; d < GM_DN(D); ++d) {
                             p *= tmass(D, d, D.tlo[d], D.thi[d], mu[d], D.mult ? x[d] : 1.0, bok);
                             if (p == 0.0) break;
                         }
@@ -641,7 +654,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_build_ws(GmDev D, long long 
     Walk wk0;
     wk0.init(D, lane, 32);
     auto first_row = [&](long long j) { return (static_cast<long long>(blockIdx.x) + j * gridDim.x) * rb; };
-    // opts bit 4: cycle totals of one thread per role (CTA 0; diagnostics only)
+#ifdef GM_DIAG
+    // opts bit 4: cycle totals of one thread per role (CTA 0; GM_DIAG builds only: the
+    // counters cost registers in the shipped kernel)
     const bool prof = (opts & 16) && blockIdx.x == 0 && (threadIdx.x == 0 || threadIdx.x == np ||
                                                          threadIdx.x == np + nc);
     long long tp[3] = {0, 0, 0}, tl = clock64();
@@ -651,6 +666,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_build_ws(GmDev D, long long 
         tp[k] += n_ - tl;                 \
         tl = n_;                          \
     }
+#else
+#define GM_TP(k)
+#endif
     __syncthreads();
     if (role == 0 && first_row(0) < nrows)
         build_prologue(D, sprog, slits, row0, nrows, first_row(0), rb, threadIdx.x, np, pro_buf(offPro, rb, D.n),
@@ -763,8 +781,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_build_ws(GmDev D, long long 
         GM_TP(2)
     }
 #undef GM_TP
+#ifdef GM_DIAG
     if (prof)
         printf("k_build_ws %s: rb %d npw %d ncw %d cycles: own work %lld, fill %lld, barrier %lld\n",
                role == 0 ? "producer" : (role == 1 ? "consumer" : "filler"), rb, npw, ncw, tp[0], tp[1], tp[2]);
+#endif
 }
 #endif

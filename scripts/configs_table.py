@@ -73,43 +73,32 @@ def fp64_peak():
 
 
 def gpu_run(name, text, stream, dev):
-    import torch
-
+    """One synthesis through the engine's C++ entry (gm_synthesize: build, then the T
+    steps enqueued back to back), device time from the model's own CUDA events
+    (gm_model_last_times), after a warm-up run; a third run with per-launch timing
+    gives the kernel-family split."""
     from paper_2005_06191_b200 import _capi
     from paper_2005_06191_b200 import gridmdp as g
-    from paper_2005_06191_b200 import sharded as S
 
     lib = _capi.lib
     m = g.parse_config(text, name)
     s = m.sizes()
-    be = S.DeviceBackend(m, stream)
-    # warm-up: JIT, the model's device buffers and matrix allocation (a few ms of one-time
-    # setup that dominates the small configs); the 7-step traffic OFA cases warm at T = 1
     big = int(s.rows) * int(s.row_width) * int(s.horizon) > 2e12
-    mw = g.parse_config(with_horizon(text, 1), name) if big else m
-    bw = S.DeviceBackend(mw, stream) if big else be
-    S.synthesize_sharded(bw, int(s.n_states), int(mw.sizes().horizon), m.spec.is_reach(),
-                         m.options.mode == "matrix", dev)
-    if big:
-        bw.release()
-    ev = {}
-
-    def mark(k):
-        e = torch.cuda.Event(enable_timing=True)
-        e.record(stream)
-        ev[k] = e
-
-    lib.gm_reset_kernel_stats()
-    lib.gm_enable_kernel_timing(1)
-    S.synthesize_sharded(be, int(s.n_states), int(s.horizon), m.spec.is_reach(), m.options.mode == "matrix", dev,
-                         timer=mark)
-    torch.cuda.synchronize()
-    lib.gm_enable_kernel_timing(0)
-    be.release()
-    build_s = ev["build_start"].elapsed_time(ev["build_end"]) / 1e3
-    sweep_s = ev["build_end"].elapsed_time(ev["sweep_end"]) / 1e3
-    fam = {n: lib.gm_kernel_ms_total(i) for i, n in enumerate(_capi.KF_NAMES) if lib.gm_kernel_ms_total(i)}
-    return s, build_s, sweep_s, fam
+    if big:  # the 7-step traffic OFA cases warm at T = 1
+        g.synthesize(g.parse_config(with_horizon(text, 1), name))
+    else:
+        g.synthesize(m)
+    g.synthesize(m)
+    build_ms, sweep_ms = g.last_times(m)
+    fam = {}
+    if not big:
+        lib.gm_reset_kernel_stats()
+        lib.gm_enable_kernel_timing(1)
+        g.synthesize(m)
+        lib.gm_enable_kernel_timing(0)
+        fam = {n: lib.gm_kernel_ms_total(i) for i, n in enumerate(_capi.KF_NAMES) if lib.gm_kernel_ms_total(i)}
+    g.release_cached_memory()
+    return s, build_ms / 1e3, sweep_ms / 1e3, fam
 
 
 def main():
@@ -181,7 +170,7 @@ def main():
         Path(a.out).write_text(
             "# SURVEY §8.0 workloads on one B200 vs the reference on the host CPU\n\n"
             f"`python scripts/configs_table.py --out {a.out}`. HBM = {hbm} GB/s ({peak_kind}); FP64 DFMA peak "
-            f"{f64:.2f} TFLOP/s measured by scripts/fp64_peak.cu on the same box. GPU: one full synthesis after a "
+            f"{f64:.2f} TFLOP/s measured by scripts/fp64_peak.cu on the same box. GPU: one full synthesis (gm_synthesize) after a "
             "warm-up run of the same model (T = 1 for C4/C4p), CUDA events on the engine's stream (build = stage i of matrix mode; sweep = the T "
             "Bellman steps; OFA has no build). G terms/s = rows·R·T / sweep; HBM-equiv = 8 B per term of the "
             "rows the sweep reads (absorbed states' rows excluded) against HBM (the bytes matrix mode streams); "

@@ -36,6 +36,32 @@ def record_traffic(rep, out, kernel, workload):
     json.dump(d, open(out, "w"), indent=1)
 
 
+def l1tex_util(rep):
+    """L1/TEX cache throughput (% of peak) and hit rate of the first captured launch: the
+    ceiling of the OFA kernels, whose V gathers and table reads all go through L1/shared."""
+    rows = list(csv.reader(io.StringIO(run([rep, "--page", "details", "--csv"]))))
+    h = rows[0]
+    out = {}
+    for r in rows[1:]:
+        d = dict(zip(h, r))
+        if d["Metric Name"] in ("L1/TEX Cache Throughput", "L1/TEX Hit Rate", "Duration", "Issue Slots Busy",
+                                "Achieved Occupancy"):
+            out.setdefault(d["Metric Name"], float(d["Metric Value"].replace(",", "")))
+    return out
+
+
+def record_l1tex(rep, out, kernel, workload):
+    """Merges {kernel: {workload, l1tex_pct_of_peak, ...}} into `out` (read by bench.py)."""
+    import json
+    import os
+    d = json.load(open(out)) if os.path.exists(out) else {}
+    u = l1tex_util(rep)
+    d[kernel] = {"workload": workload, "l1tex_pct_of_peak": u.get("L1/TEX Cache Throughput"),
+                 "l1tex_hit_rate_pct": u.get("L1/TEX Hit Rate"), "issue_slots_busy_pct": u.get("Issue Slots Busy"),
+                 "achieved_occupancy_pct": u.get("Achieved Occupancy"), "report": os.path.basename(rep)}
+    json.dump(d, open(out, "w"), indent=1)
+
+
 def main(rep, top=25):
     rows = list(csv.reader(io.StringIO(run([rep, "--page", "details", "--csv"]))))
     h = rows[0]
@@ -65,5 +91,7 @@ if __name__ == "__main__":
     # ncu_summary.py REPORT [TOP]  |  ncu_summary.py --traffic OUT.json KERNEL WORKLOAD REPORT
     if sys.argv[1] == "--traffic":
         record_traffic(sys.argv[5], sys.argv[2], sys.argv[3], sys.argv[4])
+    elif sys.argv[1] == "--l1tex":
+        record_l1tex(sys.argv[5], sys.argv[2], sys.argv[3], sys.argv[4])
     else:
         main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 25)

@@ -95,3 +95,18 @@ def test_reference_bellman_step_on_engine(case, mode, tmp_path):
     assert r.returncode == 0, r.stderr
     got = np.fromfile(f"{pre}.v", "<f8")
     assert G.tol_ok(got, v).all(), np.abs(got - v).max()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["ref_vehicle3_desk", "fixture2d_ra"])
+def test_reference_synthesize_on_several_devices(case, tmp_path):
+    """GRIDMDP_B200_DEVICES routes the reference's synthesize to gm_synthesize_multi
+    (one GPU here: the device repeated, peer transport); same container bytes."""
+    import os
+    a, b = tmp_path / "one.bin", tmp_path / "multi.bin"
+    assert run("synthesize", "-c", G.case_cfg(case), "-o", a).returncode == 0
+    env = dict(os.environ, GRIDMDP_B200_DEVICES="0,0,0", GRIDMDP_B200_TRANSPORT="peer")
+    r = subprocess.run([str(BIN), "synthesize", "-c", str(G.case_cfg(case)), "-o", str(b)], capture_output=True,
+                       text=True, env=env)
+    assert r.returncode == 0, r.stderr
+    assert a.read_bytes() == b.read_bytes()
