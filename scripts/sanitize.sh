@@ -7,7 +7,7 @@ CS=/usr/local/cuda/bin/compute-sanitizer
 run() { # tool scenario env...
   local tool=$1 sc=$2; shift 2
   local tag=${tool}_${sc}${*:+_$(echo "$*" | tr ' =' '__')}
-  env "$@" timeout 1800 $CS --tool $tool --error-exitcode 99 --print-limit 20 \
+  env "$@" timeout 600 $CS --tool $tool --error-exitcode 99 --print-limit 20 \
       python scripts/sanitize_cases.py $sc > $O/$tag.log 2>&1
   echo "$tag rc=$? $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY|scenario .* ok' $O/$tag.log | tr '\n' ' ')"
 }
