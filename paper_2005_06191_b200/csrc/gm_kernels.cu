@@ -1415,9 +1415,11 @@ void build(const GmDev& D, long long row0, long long nrows, long long* origin_ou
             throw std::runtime_error("build: GM_BUILD_OPTS (16 / 32 / 64) are diagnostics of GM_DIAG builds only");
 #endif
         const bool qs = build_uses_qs(D);
-        const size_t fixed_d = D.n_ins + D.n_lits + 3 + (qs ? (D.pitch + 1) / 2 + (kThreads / 32) * (D.n_lines + 1) : 0);
+        // + 8 ints of consumer leader counts
+        const size_t fixed_d = D.n_ins + D.n_lits + 3 + 4 + (qs ? (D.pitch + 1) / 2 + (kThreads / 32) * (D.n_lines + 1) : 0);
         // two table buffers + two prologue buffers (pro_doubles: <= (5n + 2) rb + 2 for both)
-        const size_t per_d = 2 * (mw + D.P_size) + 5 * static_cast<size_t>(D.n) + 2;
+        // + the consumers' leader / compaction ints (2 n per row)
+        const size_t per_d = 2 * (mw + D.P_size) + 6 * static_cast<size_t>(D.n) + 2;
         static const char* bc = std::getenv("GM_BUILD_CTAS"); // resident CTAs per SM (tuning; AOT kernels)
         const int ctas = bc ? std::max(2, std::min(6, std::atoi(bc))) : 3; // C2b: 3 beats 4 by 2-4 %, 2 is 19 % slower
         const size_t budget_d = (216 / ctas) * 1024 / sizeof(double);

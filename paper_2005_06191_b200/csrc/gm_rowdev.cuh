@@ -620,6 +620,11 @@ __global__ void __launch_bounds__(kThreads, MINB) k_build_ws(GmDev D, long long 
     double* slits = g_sm + offProg + D.n_ins;
     int* claim = reinterpret_cast<int*>(slits + D.n_lits); // fill-row counters by batch parity
     int* ET = claim + 2;
+    // consumer scratch: leader row of each (row, axis) item, compacted leader items,
+    // per-consumer-warp leader counts
+    int* dlead = ET + (QS ? static_cast<int>(D.pitch) : 0);
+    int* dlist = dlead + rb * D.n;
+    int* dcnt = dlist + rb * D.n;
     for (int c = threadIdx.x; c < D.n_ins; c += blockDim.x) sprog[c] = D.prog[c];
     for (int c = threadIdx.x; c < D.n_lits; c += blockDim.x) slits[c] = D.lits[c];
     if (threadIdx.x < 2) claim[threadIdx.x] = 0;
@@ -686,16 +691,56 @@ __global__ void __launch_bounds__(kThreads, MINB) k_build_ws(GmDev D, long long 
             if (bn < nrows) {
                 const ProBuf cur = pro_buf(offPro + static_cast<int>((i + 1) & 1) * psz, rb, D.n);
                 double* tb = g_sm + offT + static_cast<int>((i + 1) & 1) * tsz;
-                // fill_axis_masses (abstraction.cpp:130-146): thread per (row, axis)
-                for (int c = ct; c < rb * D.n; c += nc) {
-                    const int d = c / rb, r = c - d * rb;
-                    if (cur.ok[r] != 0.0) {
+                // fill_axis_masses (abstraction.cpp:130-146), one (row, axis) item per thread.
+                // An axis' masses are a pure function of (origin, mu, scale) on that axis, and
+                // separable dynamics repeat them across the rows of a batch (C2b: mu_2 =
+                // x2 + tau*u1 is shared by every u0): only the first row with a given key
+                // (its leader) evaluates the CDFs, compacted over the consumer warps so the
+                // erf work shrinks with the repeats; the others copy the leader's bits.
+                const int items = rb * D.n, cw = ct >> 5;
+                for (int base = 0; base < items; base += nc) {
+                    const int c = base + ct;
+                    const bool is_item = c < items;
+                    const int d = is_item ? c / rb : 0, r = is_item ? c - d * rb : 0;
+                    const bool ok_r = is_item && cur.ok[r] != 0.0;
+                    int lead = r;
+                    if (ok_r) {
+                        const int o = cur.org[r * cur.n + d];
+                        const double mu = cur.mu[r * cur.n + d], xs = cur.x[r * cur.n + d];
+                        for (int r2 = 0; r2 < r; ++r2)
+                            if (cur.ok[r2] != 0.0 && cur.org[r2 * cur.n + d] == o && same_bits(cur.mu[r2 * cur.n + d], mu) &&
+                                (!D.mult || same_bits(cur.x[r2 * cur.n + d], xs))) {
+                                lead = r2;
+                                break;
+                            }
+                    }
+                    const bool leader = ok_r && lead == r;
+                    const unsigned bal = __ballot_sync(0xffffffffu, leader);
+                    if (lane == 0) dcnt[cw] = __popc(bal);
+                    if (is_item) dlead[c] = lead;
+                    named_sync(1, nc);
+                    int before = 0, total = 0;
+                    for (int w2 = 0; w2 < ncw; ++w2) {
+                        const int k = dcnt[w2];
+                        before += w2 < cw ? k : 0;
+                        total += k;
+                    }
+                    if (leader) dlist[before + __popc(bal & ((1u << lane) - 1u))] = c;
+                    named_sync(1, nc);
+                    for (int k = ct; k < total; k += nc) {
+                        const int c2 = dlist[k], d2 = c2 / rb, r2 = c2 - d2 * rb;
                         bool ok = true;
-                        axis_masses(D, d, cur.org[r * cur.n + d], cur.mu[r * cur.n + d],
-                                    D.mult ? cur.x[r * cur.n + d] : 1.0, tb + r * mw + D.mass_off[d], 1, ok);
-                        if (!ok) record_error(err, row0 + bn + r);
-                    } else {
+                        axis_masses(D, d2, cur.org[r2 * cur.n + d2], cur.mu[r2 * cur.n + d2],
+                                    D.mult ? cur.x[r2 * cur.n + d2] : 1.0, tb + r2 * mw + D.mass_off[d2], 1, ok);
+                        if (!ok) record_error(err, row0 + bn + r2);
+                    }
+                    named_sync(1, nc);
+                    if (is_item && !ok_r) {
                         for (int t = 0; t < D.W[d]; ++t) tb[r * mw + D.mass_off[d] + t] = 1.0;
+                    } else if (is_item && lead != r) {
+                        const double* src = tb + lead * mw + D.mass_off[d];
+                        double* dst = tb + r * mw + D.mass_off[d];
+                        for (int t = 0; t < D.W[d]; ++t) dst[t] = src[t];
                     }
                 }
                 for (int r = ct; r < rb; r += nc) tb[r * mw + D.sumW] = 1.0; // virtual-axis slot
