@@ -120,6 +120,38 @@ class Clocks:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def store_ceiling_ms(be, stream, reps=3):
+    """The in-step store ceiling of stage (i): a plain zero fill (torch's vectorised fill
+    kernel) of the same matrix buffer, straight after the timed synthesis steps (same
+    power / clock regime), device time on the engine's stream. Diagnostic only."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2005_06191_b200 import _capi
+
+    rb, re_, R, dp = C.c_int64(), C.c_int64(), C.c_int64(), C.c_void_p()
+    _capi.call("gm_matrix_info", be._tm, C.byref(rb), C.byref(re_), C.byref(R), C.byref(dp), None)
+    n = (re_.value - rb.value) * int(_capi.lib.gm_matrix_pitch(be._tm))
+
+    class _Buf:  # zero-copy view of the engine's device buffer
+        __cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (dp.value, False), "version": 3}
+
+    t = torch.as_tensor(_Buf(), device="cuda")
+    out = []
+    with torch.cuda.stream(stream):
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            t.zero_()
+            b.record(stream)
+            b.synchronize()
+            out.append(a.elapsed_time(b))
+    return {"ms": statistics.median(out), "bytes": n * 8,
+            "gbs": n * 8 / (statistics.median(out) / 1e3) / 1e9,
+            "note": "zero fill of the matrix buffer after the timed steps (same regime): the build's store ceiling"}
+
+
 def load_workloads():
     """paper_2005_06191_b200/workloads.py by file path: importing the package would
     load the engine library, which the reference arm must not map."""
@@ -362,6 +394,7 @@ def main():
         torch.cuda.synchronize()
     launches = lib.gm_launch_count() - launches0
     lib.gm_enable_kernel_timing(0)
+    store_ceiling = store_ceiling_ms(be, stream) if matrix else None
     be.release()  # free the shard's matrix before the end-to-end run allocates its own
     torch.cuda.empty_cache()
     for ev in evs:
@@ -409,6 +442,8 @@ def main():
                       "traffic": ncu_traffic("k_build_ws", args.workload)}
     if roofline_build["achieved"]:
         roofline_build["frac"] = roofline_build["achieved"] / hbm
+        if store_ceiling:  # build time against a plain fill of the same bytes in the same regime
+            roofline_build["frac_of_store_ceiling"] = store_ceiling["ms"] / exp_ms
 
     line = {
         "metric": METRIC, "value": value, "unit": "probs/s", "n_gpus": world, "steps": args.steps,
@@ -423,7 +458,7 @@ def main():
         "sweep_terms_per_s": terms_per_step / sweep_s if sweep_s > 0 else None,
         "kernel_ms_per_step": {k: v / args.steps for k, v in fam_ms.items() if v},
         "gpu_launches": int(launches),
-        "roofline": roofline, "roofline_build": roofline_build,
+        "roofline": roofline, "roofline_build": roofline_build, "store_ceiling": store_ceiling,
         "clocks": clk.summary(),
     }
 

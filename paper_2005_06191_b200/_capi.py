@@ -11,7 +11,8 @@ import os
 from pathlib import Path
 
 PKG_DIR = Path(__file__).resolve().parent
-LIB_PATH = PKG_DIR / "libgridmdp_b200.so"
+# GM_LIB=checked loads the build with device bounds / layout checks (GM_CHECK)
+LIB_PATH = PKG_DIR / ("libgridmdp_b200_checked.so" if os.environ.get("GM_LIB") == "checked" else "libgridmdp_b200.so")
 CLI_PATH = PKG_DIR / "gridmdp"
 
 GM_MAX_DIMS = 12

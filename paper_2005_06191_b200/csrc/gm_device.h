@@ -40,6 +40,29 @@ struct GmIns {
     int32_t arg; // literal index / variable index / jump target
 };
 
+// Bounds / layout checks of the checked build (libgridmdp_b200_checked.so, -DGM_CHECKED;
+// compute-sanitizer is not available on the GPU pool): a failed check prints the
+// condition and traps, which surfaces as a launch failure of the calling API.
+#if defined(__CUDACC__) && defined(GM_CHECKED)
+#define GM_CHECK(c)                                                                                      \
+    do {                                                                                                 \
+        if (!(c)) {                                                                                      \
+            printf("GM_CHECK failed: %s (%s:%d) block %d thread %d\n", #c, __FILE__, __LINE__,            \
+                   static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));                         \
+            __trap();                                                                                    \
+        }                                                                                                \
+    } while (0)
+__device__ __forceinline__ unsigned gm_dyn_smem_bytes() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
+    return r;
+}
+#else
+#define GM_CHECK(c) \
+    do {            \
+    } while (0)
+#endif
+
 // Device error codes recorded per failing row
 enum GmDevErr { GE_NONE = 0, GE_EXPR = 1, GE_BETA = 2 };
 

@@ -489,6 +489,9 @@ __device__ __forceinline__ void expect_ofa_body(GmDev D, long long nrows, int rb
                                                         const double* __restrict__ V,
                                                         double* __restrict__ v_in) {
     const Layout Y(D, rb, TAB);
+    GM_CHECK(static_cast<unsigned>(8 * Y.offR + 8 * (kThreads / 32)) <= gm_dyn_smem_bytes());
+    GM_CHECK(LS != 1 || static_cast<unsigned>(4 * (Y.offL + D.n_lines)) <= gm_dyn_smem_bytes());
+    GM_CHECK(LS != 2 || static_cast<unsigned>(4 * (Y.offL + D.P_size)) <= gm_dyn_smem_bytes());
     if (LS == 1) {
         int* si = reinterpret_cast<int*>(g_sm);
         for (int c = threadIdx.x; c < D.n_lines; c += blockDim.x) si[Y.offL + c] = D.line_off[c];
@@ -514,6 +517,7 @@ __device__ __forceinline__ void expect_ofa_body(GmDev D, long long nrows, int rb
             const uint8_t fl = valid ? rowflag[row] : RF_ABSORBED;
             double s = 0.0;
             if (!(fl & (RF_ABSORBED | RF_ERROR))) {
+                GM_CHECK_SLAB(D, origin[row]);
                 if (PK)
                     s = row_dot_pk<TAB == TAB_Q ? 1 : 2, U, LS>(D, lane, tpr, Y.offQ + i * D.n_lines,
                                                                 Y.offP + i * D.P_size, i * Y.mw + D.mm_off,
@@ -588,6 +592,7 @@ __global__ void __launch_bounds__(kThreads) k_expect_matrix(GmDev D, long long r
         bool skip = !valid;
         if (valid && reach && D.absorb != nullptr) skip = D.absorb[(row0 + r) / nuw];
         double s = 0.0;
+        if (!skip) GM_CHECK_SLAB(D, origins[r]);
         if (!skip)
             s = row_dot<0, 8, LS>(D, lane, tpr, probs + r * D.pitch, 0, 0, 0, 0, V + origins[r], D.line_off, Y.offL);
         s = group_reduce(s, tpr, Y.offR, g * tpr);
@@ -639,6 +644,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_expect_matrix_et(GmDev D, lo
     for (int t = threadIdx.x; t < R; t += kThreads) {
         const int L = D.div_Wl.div(t);
         E[t] = D.line_off[L] + (t - L * D.Wl);
+        GM_CHECK(E[t] >= 0 && E[t] <= slab_span(D));
     }
     __syncthreads();
     const int g = threadIdx.x / TPR, lane = threadIdx.x % TPR;
@@ -660,6 +666,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_expect_matrix_et(GmDev D, lo
         }
         double s = 0.0;
         if (!skip) {
+            GM_CHECK_SLAB(D, origins[r]);
             const double* pr = probs + r * D.pitch + lane;
             const double* vb = V + origins[r];
             const int* e = E + lane;
@@ -750,6 +757,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_expect_matrix_et2(GmDev D, l
     for (int t = threadIdx.x; t < R; t += kThreads) {
         const int L = D.div_Wl.div(t);
         E[t] = D.line_off[L] + (t - L * D.Wl);
+        GM_CHECK(E[t] >= 0 && E[t] <= slab_span(D));
     }
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -772,6 +780,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_expect_matrix_et2(GmDev D, l
             skA = absorbed(rA);
             if (hasB) skB = absorbed(rB);
         }
+        if (!skA) GM_CHECK_SLAB(D, origins[rA]);
+        if (!skB) GM_CHECK_SLAB(D, origins[rB]);
         const double sA = skA ? 0.0
                               : et_row_partial<32, U>(probs + rA * D.pitch + lane, V + origins[rA], E + lane, n_full, rem);
         const double sB = skB ? 0.0
@@ -1415,11 +1425,9 @@ void build(const GmDev& D, long long row0, long long nrows, long long* origin_ou
             throw std::runtime_error("build: GM_BUILD_OPTS (16 / 32 / 64) are diagnostics of GM_DIAG builds only");
 #endif
         const bool qs = build_uses_qs(D);
-        // + 8 ints of consumer leader counts
-        const size_t fixed_d = D.n_ins + D.n_lits + 3 + 4 + (qs ? (D.pitch + 1) / 2 + (kThreads / 32) * (D.n_lines + 1) : 0);
+        const size_t fixed_d = D.n_ins + D.n_lits + 3 + (qs ? (D.pitch + 1) / 2 + (kThreads / 32) * (D.n_lines + 1) : 0);
         // two table buffers + two prologue buffers (pro_doubles: <= (5n + 2) rb + 2 for both)
-        // + the consumers' leader / compaction ints (2 n per row)
-        const size_t per_d = 2 * (mw + D.P_size) + 6 * static_cast<size_t>(D.n) + 2;
+        const size_t per_d = 2 * (mw + D.P_size) + 5 * static_cast<size_t>(D.n) + 2;
         static const char* bc = std::getenv("GM_BUILD_CTAS"); // resident CTAs per SM (tuning; AOT kernels)
         const int ctas = bc ? std::max(2, std::min(6, std::atoi(bc))) : 3; // C2b: 3 beats 4 by 2-4 %, 2 is 19 % slower
         const size_t budget_d = (216 / ctas) * 1024 / sizeof(double);

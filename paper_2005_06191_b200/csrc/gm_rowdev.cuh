@@ -358,6 +358,15 @@ __device__ __forceinline__ void record_error(unsigned long long* err, long long 
     atomicMin(err, static_cast<unsigned long long>(row));
 }
 
+// Flat offset of a slab's last post-state from its origin (the gathers of a row read
+// V[origin .. origin + span]); the checked build asserts every row's slab is in V.
+__device__ __forceinline__ long long slab_span(const GmDev& D) {
+    long long s = 0;
+    for (int d = 0; d < GM_DN(D); ++d) s += static_cast<long long>(D.W[d] - 1) * D.xstride[d];
+    return s;
+}
+#define GM_CHECK_SLAB(D, o) GM_CHECK((o) >= 0 && (o) + slab_span(D) < (D).n_x)
+
 extern __shared__ __align__(16) double g_sm[];
 
 // Prefix product of entry a of the P table (fill_product's recursion carried as
@@ -414,6 +423,7 @@ __global__ void __launch_bounds__(kThreads) k_prologue(GmDev D, long long row0, 
         org[d] = slab_origin(D, d, mu[d]);
         flat += org[d] * D.xstride[d];
     }
+    GM_CHECK_SLAB(D, flat);
     if (origin_out) origin_out[i] = flat;
     bool ok = true;
     if (flags & PF_MASSES) { // per-cell form: keeps this kernel at 64 registers (axis_masses: 80)
@@ -541,6 +551,8 @@ __device__ __forceinline__ void build_prologue(const GmDev& D, const GmIns* spro
                     pb.mu[i * pb.n + d] = mu[d];
                     pb.x[i * pb.n + d] = x[d];
                 }
+                GM_CHECK_SLAB(D, flat);
+                GM_CHECK(r < nrows && i < rb);
                 origin_out[r] = flat;
                 if (t0x_out) {
                     const bool absorbed = reach && D.absorb != nullptr && D.absorb[ix];
@@ -620,11 +632,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_build_ws(GmDev D, long long 
     double* slits = g_sm + offProg + D.n_ins;
     int* claim = reinterpret_cast<int*>(slits + D.n_lits); // fill-row counters by batch parity
     int* ET = claim + 2;
-    // consumer scratch: leader row of each (row, axis) item, compacted leader items,
-    // per-consumer-warp leader counts
-    int* dlead = ET + (QS ? static_cast<int>(D.pitch) : 0);
-    int* dlist = dlead + rb * D.n;
-    int* dcnt = dlist + rb * D.n;
+    // the launcher's shared-memory size covers the whole layout
+    GM_CHECK(static_cast<unsigned>(reinterpret_cast<const char*>(ET + (QS ? D.pitch : 0)) -
+                                   reinterpret_cast<const char*>(g_sm)) <= gm_dyn_smem_bytes());
+    GM_CHECK(npw * 32 + ncw * 32 <= kThreads);
     for (int c = threadIdx.x; c < D.n_ins; c += blockDim.x) sprog[c] = D.prog[c];
     for (int c = threadIdx.x; c < D.n_lits; c += blockDim.x) slits[c] = D.lits[c];
     if (threadIdx.x < 2) claim[threadIdx.x] = 0;
@@ -633,6 +644,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_build_ws(GmDev D, long long 
         for (int t = threadIdx.x; t < D.pitch; t += blockDim.x) {
             const int L = D.div_Wl.div(t < R ? t : 0);
             ET[t] = t < R ? (L * 8) | ((t - L * D.Wl) * 8) << 16 : nl * 8;
+            GM_CHECK((ET[t] & 0xffff) <= nl * 8 && (ET[t] >> 16) < D.Wl * 8 && nl * 8 < 0x10000);
         }
         if (threadIdx.x < kThreads / 32) g_sm[offQs + threadIdx.x * (nl + 1) + nl] = 0.0;
     }
@@ -651,6 +663,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_build_ws(GmDev D, long long 
 #pragma unroll
         for (int s = 0; s < F_PER; ++s)
             fq[s] = sm0 + 8u * static_cast<unsigned>(offQs + warp * (F_NL + 1) + (lane + 32 * s) / F_WL);
+        // every Q element a lane reads (t < R) lies in its warp's scratch
+        GM_CHECK(D.Wl == F_WL && D.Wm == F_WM && D.n_lines == F_NL && D.R == F_R && D.pitch == GM_FILL_PITCH);
+        for (int t = lane; t < F_R; t += 32) GM_CHECK(t / F_WL < F_NL);
     }
 #endif
     const int np = npw * 32, nc = ncw * 32;
@@ -691,56 +706,19 @@ __global__ void __launch_bounds__(kThreads, MINB) k_build_ws(GmDev D, long long 
             if (bn < nrows) {
                 const ProBuf cur = pro_buf(offPro + static_cast<int>((i + 1) & 1) * psz, rb, D.n);
                 double* tb = g_sm + offT + static_cast<int>((i + 1) & 1) * tsz;
-                // fill_axis_masses (abstraction.cpp:130-146), one (row, axis) item per thread.
-                // An axis' masses are a pure function of (origin, mu, scale) on that axis, and
-                // separable dynamics repeat them across the rows of a batch (C2b: mu_2 =
-                // x2 + tau*u1 is shared by every u0): only the first row with a given key
-                // (its leader) evaluates the CDFs, compacted over the consumer warps so the
-                // erf work shrinks with the repeats; the others copy the leader's bits.
-                const int items = rb * D.n, cw = ct >> 5;
-                for (int base = 0; base < items; base += nc) {
-                    const int c = base + ct;
-                    const bool is_item = c < items;
-                    const int d = is_item ? c / rb : 0, r = is_item ? c - d * rb : 0;
-                    const bool ok_r = is_item && cur.ok[r] != 0.0;
-                    int lead = r;
-                    if (ok_r) {
-                        const int o = cur.org[r * cur.n + d];
-                        const double mu = cur.mu[r * cur.n + d], xs = cur.x[r * cur.n + d];
-                        for (int r2 = 0; r2 < r; ++r2)
-                            if (cur.ok[r2] != 0.0 && cur.org[r2 * cur.n + d] == o && same_bits(cur.mu[r2 * cur.n + d], mu) &&
-                                (!D.mult || same_bits(cur.x[r2 * cur.n + d], xs))) {
-                                lead = r2;
-                                break;
-                            }
-                    }
-                    const bool leader = ok_r && lead == r;
-                    const unsigned bal = __ballot_sync(0xffffffffu, leader);
-                    if (lane == 0) dcnt[cw] = __popc(bal);
-                    if (is_item) dlead[c] = lead;
-                    named_sync(1, nc);
-                    int before = 0, total = 0;
-                    for (int w2 = 0; w2 < ncw; ++w2) {
-                        const int k = dcnt[w2];
-                        before += w2 < cw ? k : 0;
-                        total += k;
-                    }
-                    if (leader) dlist[before + __popc(bal & ((1u << lane) - 1u))] = c;
-                    named_sync(1, nc);
-                    for (int k = ct; k < total; k += nc) {
-                        const int c2 = dlist[k], d2 = c2 / rb, r2 = c2 - d2 * rb;
+                // fill_axis_masses (abstraction.cpp:130-146): thread per (row, axis). (Evaluating
+                // each distinct (origin, mu, scale) once per batch and copying the repeats cut
+                // the instructions 4 % but lengthened the consumers' critical path: C2b build
+                // 20 -> 28 ms; the W+1 serial CDF calls of one item set the pipeline's pace.)
+                for (int c = ct; c < rb * D.n; c += nc) {
+                    const int d = c / rb, r = c - d * rb;
+                    if (cur.ok[r] != 0.0) {
                         bool ok = true;
-                        axis_masses(D, d2, cur.org[r2 * cur.n + d2], cur.mu[r2 * cur.n + d2],
-                                    D.mult ? cur.x[r2 * cur.n + d2] : 1.0, tb + r2 * mw + D.mass_off[d2], 1, ok);
-                        if (!ok) record_error(err, row0 + bn + r2);
-                    }
-                    named_sync(1, nc);
-                    if (is_item && !ok_r) {
+                        axis_masses(D, d, cur.org[r * cur.n + d], cur.mu[r * cur.n + d],
+                                    D.mult ? cur.x[r * cur.n + d] : 1.0, tb + r * mw + D.mass_off[d], 1, ok);
+                        if (!ok) record_error(err, row0 + bn + r);
+                    } else {
                         for (int t = 0; t < D.W[d]; ++t) tb[r * mw + D.mass_off[d] + t] = 1.0;
-                    } else if (is_item && lead != r) {
-                        const double* src = tb + lead * mw + D.mass_off[d];
-                        double* dst = tb + r * mw + D.mass_off[d];
-                        for (int t = 0; t < D.W[d]; ++t) dst[t] = src[t];
                     }
                 }
                 for (int r = ct; r < rb; r += nc) tb[r * mw + D.sumW] = 1.0; // virtual-axis slot
@@ -766,6 +744,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_build_ws(GmDev D, long long 
                 r = __shfl_sync(0xffffffffu, r, 0);
                 const long long row = b0 + r;
                 if (r >= rb || row >= nrows) break;
+                GM_CHECK(r >= 0 && row >= 0);
                 const double* m = tb + r * mw;
                 const double* Pr = P + r * D.P_size;
                 double* out = probs + row * D.pitch;

@@ -1,11 +1,15 @@
-"""Small workloads that launch every device kernel of the engine, for
-compute-sanitizer (memcheck / racecheck / synccheck) runs (scripts/sanitize.sh).
-One scenario per process: the kernel-selection knobs are read once per process.
+"""Small workloads that launch every device kernel of the engine, for the
+bounds-checked library (GM_LIB=checked: libgridmdp_b200_checked.so, built with
+-DGM_CHECKED: shared-memory layout vs the launch's dynamic size, every row's V slab
+inside V, element / line tables, consumer compaction indices, specialised-fill
+addresses). compute-sanitizer is closed on the GPU pool; tests/test_gpu_checked.py
+runs these scenarios under the checked build instead. One scenario per process:
+the kernel-selection knobs are read once per process.
 
-  python scripts/sanitize_cases.py <scenario>
+  GM_LIB=checked python scripts/check_cases.py <scenario>
 
 Each scenario prints the kernel variants it launched (gm_last_kernel_variant) and
-checks its values against the reference goldens, so a sanitizer run is also a
+checks its values against the reference goldens, so a checked run is also a
 parity run of the same launches.
 """
 import sys
