@@ -138,18 +138,30 @@ def store_ceiling_ms(be, stream, reps=3):
         __cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (dp.value, False), "version": 3}
 
     t = torch.as_tensor(_Buf(), device="cuda")
-    out = []
-    with torch.cuda.stream(stream):
-        for _ in range(reps):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            t.zero_()
-            b.record(stream)
-            b.synchronize()
-            out.append(a.elapsed_time(b))
-    return {"ms": statistics.median(out), "bytes": n * 8,
-            "gbs": n * 8 / (statistics.median(out) / 1e3) / 1e9,
-            "note": "zero fill of the matrix buffer after the timed steps (same regime): the build's store ceiling"}
+
+    def timed(fill):
+        out = []
+        with torch.cuda.stream(stream):
+            for _ in range(reps):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                fill()
+                b.record(stream)
+                b.synchronize()
+                out.append(a.elapsed_time(b))
+        return statistics.median(out)
+
+    # HBM write power depends on the data (zeros toggle few bits): the ceiling is a
+    # write of varied doubles (arange: every element differs in its low mantissa bits);
+    # the zero fill is reported beside it
+    step = 1.0000001
+    ptr0 = t.data_ptr()
+    ms = timed(lambda: torch.arange(0.0, (n - 0.5) * step, step, dtype=torch.float64, out=t))
+    assert t.data_ptr() == ptr0 and t.numel() == n, "the fill must write the matrix buffer in place"
+    zero_ms = timed(t.zero_)
+    return {"ms": ms, "bytes": n * 8, "gbs": n * 8 / (ms / 1e3) / 1e9, "zero_fill_ms": zero_ms,
+            "note": "varied-data write of the matrix buffer after the timed steps (same regime): the build's "
+                    "store ceiling; zero_fill_ms: the same bytes as zeros"}
 
 
 def load_workloads():
