@@ -152,12 +152,10 @@ def store_ceiling_ms(be, stream, reps=3):
         return statistics.median(out)
 
     # HBM write power depends on the data (zeros toggle few bits): the ceiling is a
-    # write of varied doubles (arange: every element differs in its low mantissa bits);
-    # the zero fill is reported beside it
-    step = 1.0000001
-    ptr0 = t.data_ptr()
-    ms = timed(lambda: torch.arange(0.0, (n - 0.5) * step, step, dtype=torch.float64, out=t))
-    assert t.data_ptr() == ptr0 and t.numel() == n, "the fill must write the matrix buffer in place"
+    # write of varied doubles (gm_store_probe: hashed mantissas, 16-byte evict-first
+    # stores); torch's zero fill is reported beside it
+    ms = timed(lambda: _capi.call("gm_store_probe", C.c_void_p(dp.value), C.c_int64(n), C.c_uint64(7),
+                                  C.c_void_p(stream.cuda_stream)))
     zero_ms = timed(t.zero_)
     return {"ms": ms, "bytes": n * 8, "gbs": n * 8 / (ms / 1e3) / 1e9, "zero_fill_ms": zero_ms,
             "note": "varied-data write of the matrix buffer after the timed steps (same regime): the build's "

@@ -300,6 +300,12 @@ gm_code gm_build_shard_host(gm_model* m, int64_t state_begin, int64_t state_end,
  * much smaller than the grid, otherwise the V shards are all-gathered. */
 gm_code gm_shard_reach(gm_model* m, int64_t x_begin, int64_t x_end, int64_t* lo, int64_t* hi,
                        gm_status* st);
+/* OFA steps through gm_step_device keep the row prologue results (per-axis cell
+ * masses, origins, T0x, row flags: Σ W_d + 3 values per row, never the R-wide rows)
+ * of the stepped rows on the device, so the following steps of a sweep only recompute
+ * the rows' products and dot them with V. This releases them (call at the start of a
+ * sweep of new data, or to return the memory; gm_synthesize manages its own). */
+gm_code gm_model_release_ofa_cache(gm_model* m, gm_status* st);
 /* Per-row expected values of the model's most recent step (the v_in workspace of
  * bellman_impl, synthesis.cpp:69-109), rows of the stepped states; n doubles. */
 gm_code gm_copy_row_values(gm_model* m, double* out, int64_t n, gm_status* st);
@@ -406,6 +412,10 @@ gm_code gm_model_clone(const gm_model* m, gm_model** out, gm_status* st);
  * Results are bit-identical to gm_synthesize for any n_dev. stats may be NULL. */
 gm_code gm_synthesize_multi(gm_model* m, int32_t n_dev, const int32_t* devices, int32_t exchange,
                             int32_t transport, gm_result** out, gm_multi_stats* stats, gm_status* st);
+
+/* Measurement only: writes n varied doubles (16-byte evict-first stores) to a device
+ * buffer on `stream` — the store-bandwidth ceiling stage (i) is compared with. */
+gm_code gm_store_probe(double* d_buf, int64_t n, uint64_t seed, void* stream, gm_status* st);
 
 /* Large device blocks (>= 64 MB, e.g. stored matrices) are kept for reuse after
  * release; this returns them to the driver. */

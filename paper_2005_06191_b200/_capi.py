@@ -154,6 +154,8 @@ SIGNATURES = {
     "gm_sim_write_csv": (C.c_int, [_VP, C.c_char_p, _PS]),
     "gm_sim_free": (None, [_VP]),
     "gm_model_clone": (C.c_int, [_VP, C.POINTER(_VP), _PS]),
+    "gm_model_release_ofa_cache": (C.c_int, [_VP, _PS]),
+    "gm_store_probe": (C.c_int, [_VP, _I64, C.c_uint64, _VP, _PS]),
     "gm_last_kernel_variant": (C.c_char_p, [C.c_int32]),
     "gm_model_create": (C.c_int, [_VP, C.POINTER(_VP), _PS]),
     "gm_model_save_config": (C.c_int, [_VP, C.c_char_p, _PS]),

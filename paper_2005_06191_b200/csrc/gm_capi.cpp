@@ -281,6 +281,17 @@ struct gm_model {
     std::string jit_why;
     // device time of the last gm_synthesize* (stage i / stage ii), ms
     double last_build_ms = 0.0, last_sweep_ms = 0.0;
+    // OFA row prologue results (per-axis cell masses, origins, T0x, row flags) of the
+    // rows [ofa_r0, ofa_r0 + ofa_n), kept across the steps of a sweep: a step depends
+    // on V only, so steps 2..T recompute every row's T(x'|x,u) from the cached 1-D
+    // masses (Σ W_d doubles per row, never the R-wide row) without re-running the
+    // dynamics and the CDFs. Invalidated when the spec changes (refresh_device).
+    DevBuf<double> ofa_mass, ofa_t0x;
+    DevBuf<long long> ofa_origin;
+    DevBuf<uint8_t> ofa_flag;
+    int64_t ofa_r0 = -1, ofa_n = 0, ofa_chunk = 0;
+    bool ofa_valid = false;
+    bool ofa_cache_steps = false; // set by the multi-step drivers (run_backward, gm_step_device)
 };
 
 // Row kernels with the dynamics compiled for this model, or nullptr (interpreter).
@@ -460,6 +471,7 @@ void ensure_device(gm_model* m) {
 // absorbing flags (absorbing_states, spec.cpp:51-60 -> k_absorb)
 void refresh_device(gm_model* m) {
     ensure_device(m);
+    m->ofa_valid = false; // T0x and the absorbed-row flags depend on the spec
     if (m->M.R > INT_MAX) throw MemoryErr("row width exceeds the device limit");
     m->D = m->M.device_descriptor();
     {
@@ -601,6 +613,70 @@ void build_rows(gm_model* m, int64_t r0, int64_t r1, gm_matrix* tm, bool want_t0
     raise_device_error(m);
 }
 
+// OFA step from cached row prologue results. The first step of rows [r0, r0+n) runs
+// the usual prologue / consumer pipeline with the prologue writing into the cache
+// (one slot per chunk); later steps launch only the consumers. Off when GM_OFA_CACHE=0,
+// for one-off steps (m->ofa_cache_steps unset) or when the cache would not leave a
+// quarter of the device free. Returns false when the caller must run the plain path.
+bool ofa_cached_step(gm_model* m, int64_t r0, int64_t n, const double* v_next, cudaStream_t s) {
+    static const char* env = std::getenv("GM_OFA_CACHE");
+    if ((env && env[0] == '0') || !m->ofa_cache_steps || m->M.noise.family == GM_CUSTOM) return false;
+    const int64_t chunk = std::min(chunk_rows(m), n);
+    const size_t sumW = static_cast<size_t>(std::max(m->D.sumW, 1));
+    const bool hit = m->ofa_valid && m->ofa_r0 == r0 && m->ofa_n == n && m->ofa_chunk == chunk;
+    if (!hit) {
+        const uint64_t need = static_cast<uint64_t>(n) * (sumW * 8 + 8 + 8 + 1);
+        size_t free_b = 0, total_b = 0;
+        ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+        free_b += cached_bytes();
+        if (need + total_b / 4 > free_b) return false;
+        m->ofa_valid = false;
+        m->ofa_mass.ensure(static_cast<size_t>(n) * sumW, "OFA mass cache");
+        m->ofa_origin.ensure(static_cast<size_t>(n), "OFA origin cache");
+        m->ofa_t0x.ensure(static_cast<size_t>(n), "OFA target-hit cache");
+        m->ofa_flag.ensure(static_cast<size_t>(n), "OFA row-flag cache");
+    }
+    const bool reach = m->M.spec.reach();
+    double* vin = m->d_vin.p;
+    if (hit) {
+        for (int64_t c0 = 0; c0 < n; c0 += chunk) {
+            const int64_t cn = std::min(chunk, n - c0);
+            Launch L(gmk::KF_EXPECT_OFA, s);
+            gmk::expect_ofa(m->D, cn, m->ofa_mass.p + c0 * sumW, m->ofa_origin.p + c0, m->ofa_t0x.p + c0,
+                            m->ofa_flag.p + c0, v_next, vin + c0, s);
+        }
+        return true;
+    }
+    // first step: the pipeline of the plain path, prologue results written to the cache
+    ensure_scratch(m, chunk); // the aux stream and events
+    const gmj::Kernels* J = jit_kernels(m, gmj::WANT_PROLOGUE, n);
+    ck(cudaEventRecord(m->ev_fork, s), "fork");
+    ck(cudaStreamWaitEvent(m->aux, m->ev_fork, 0), "fork");
+    int64_t c = 0;
+    for (int64_t c0 = 0; c0 < n; c0 += chunk, ++c) {
+        const int64_t cn = std::min(chunk, n - c0);
+        const int b = static_cast<int>(c & 1);
+        {
+            Launch L(gmk::KF_PROLOGUE, m->aux);
+            gmk::prologue(m->D, r0 + c0, cn, gmk::PF_SKIP_ABSORBED | gmk::PF_MASSES | (reach ? gmk::PF_T0X : 0),
+                          m->ofa_origin.p + c0, m->ofa_t0x.p + c0, m->ofa_flag.p + c0, m->ofa_mass.p + c0 * sumW,
+                          m->d_err.p, m->aux, J ? J->prologue : nullptr);
+        }
+        ck(cudaEventRecord(m->ev_ready[b], m->aux), "ready");
+        ck(cudaStreamWaitEvent(s, m->ev_ready[b], 0), "ready");
+        Launch L(gmk::KF_EXPECT_OFA, s);
+        gmk::expect_ofa(m->D, cn, m->ofa_mass.p + c0 * sumW, m->ofa_origin.p + c0, m->ofa_t0x.p + c0,
+                        m->ofa_flag.p + c0, v_next, vin + c0, s);
+    }
+    ck(cudaEventRecord(m->ev_join, m->aux), "join");
+    ck(cudaStreamWaitEvent(s, m->ev_join, 0), "join");
+    m->ofa_r0 = r0;
+    m->ofa_n = n;
+    m->ofa_chunk = chunk;
+    m->ofa_valid = true;
+    return true;
+}
+
 // One backward step over states [x0, x1) (bellman_impl, synthesis.cpp:61-143).
 // v_next: full device V (absorbing zeroed); outputs indexed from x0.
 void step_states(gm_model* m, gm_matrix* tm, int64_t x0, int64_t x1, const double* v_next,
@@ -637,6 +713,8 @@ void step_states(gm_model* m, gm_matrix* tm, int64_t x0, int64_t x1, const doubl
             gmk::expect_matrix(m->D, r0 + c0, 0, cn, m->d_chunk.p, m->d_origin[0].p, reach ? m->d_t0x[0].p : nullptr,
                                v_next, m->d_vin.p + c0, s);
         }
+    } else if (n > 0 && ofa_cached_step(m, r0, n, v_next, s)) {
+        // consumer only, from the prologue results cached by an earlier step of the sweep
     } else if (n > 0) {
         const int64_t chunk = std::min(chunk_rows(m), n);
         ensure_scratch(m, chunk);
@@ -710,6 +788,19 @@ struct PhaseTimer {
 
 gm_result* run_backward(gm_model* m, gm_matrix* tm, PhaseTimer* pt = nullptr) {
     const int64_t n_x = m->M.n_x();
+    // OFA prologue results cached across the T steps; released when the sweep ends
+    struct CacheScope {
+        gm_model* m;
+        explicit CacheScope(gm_model* mm) : m(mm) { m->ofa_cache_steps = true; }
+        ~CacheScope() {
+            m->ofa_cache_steps = false;
+            m->ofa_valid = false;
+            m->ofa_mass.release();
+            m->ofa_origin.release();
+            m->ofa_t0x.release();
+            m->ofa_flag.release();
+        }
+    } cache_scope(m);
     const int T = m->M.spec.horizon;
     const bool reach = m->M.spec.reach();
     const size_t nx = static_cast<size_t>(n_x);
@@ -1593,7 +1684,23 @@ gm_code gm_step_device(gm_model* m, gm_matrix* tm, int64_t x0, int64_t x1, const
         if (x0 < 0 || x1 > m->M.n_x() || x0 > x1) throw std::out_of_range("step_device: state range");
         prepare(m);
         if (tm) ensure_t0x(m, tm);
+        m->ofa_cache_steps = true; // sharded sweeps step the same rows T times (freed with the model)
         step_states(m, tm, x0, x1, d_v_next, d_v_out, d_pol, d_wst, static_cast<cudaStream_t>(stream));
+    });
+}
+
+gm_code gm_store_probe(double* d_buf, int64_t n, uint64_t seed, void* stream, gm_status* st) {
+    return guarded(st, [&] { gmk::store_probe(d_buf, n, seed, static_cast<cudaStream_t>(stream)); });
+}
+
+gm_code gm_model_release_ofa_cache(gm_model* m, gm_status* st) {
+    return guarded(st, [&] {
+        if (m->dev_ready) ck(cudaSetDevice(m->device), "cudaSetDevice");
+        m->ofa_valid = false;
+        m->ofa_mass.release();
+        m->ofa_origin.release();
+        m->ofa_t0x.release();
+        m->ofa_flag.release();
     });
 }
 

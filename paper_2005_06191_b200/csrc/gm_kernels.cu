@@ -1652,6 +1652,29 @@ __global__ void k_count_positive(const double* __restrict__ p, long long n, unsi
 }
 } // namespace
 
+namespace {
+// Store ceiling probe: varied doubles (hashed index, every mantissa bit toggles) with
+// 16-byte evict-first stores, grid-stride over the buffer.
+__global__ void __launch_bounds__(kThreads) k_store_probe(double2* __restrict__ p, long long n2, unsigned long long seed) {
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n2; i += stride) {
+        unsigned long long z = (static_cast<unsigned long long>(i) + seed) * 0x9E3779B97F4A7C15ULL;
+        z ^= z >> 29;
+        const double a = __longlong_as_double(static_cast<long long>((z >> 12) | 0x3FF0000000000000ULL));
+        const double b = __longlong_as_double(static_cast<long long>((z << 20 >> 12) | 0x3FF0000000000000ULL));
+        __stcs(p + i, make_double2(a, b));
+    }
+}
+} // namespace
+
+void store_probe(double* p, long long n, unsigned long long seed, cudaStream_t s) {
+    if (n < 2) return;
+    const long long n2 = n / 2;
+    const int blocks = std::max(1, std::min(grid_for(n2, kThreads), num_sms() * 8));
+    k_store_probe<<<blocks, kThreads, 0, s>>>(reinterpret_cast<double2*>(p), n2, seed);
+    check_launch("store_probe");
+}
+
 unsigned long long count_positive(const double* p, long long n, unsigned long long* d_count, cudaStream_t s) {
     cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), s);
     if (n > 0) {

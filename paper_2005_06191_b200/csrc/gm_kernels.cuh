@@ -31,6 +31,8 @@ BatchPlan plan_batches(const GmDev& D, bool ofa);
 const char* last_variant(int family);
 
 void absorb_flags(const GmDev& D, uint8_t* d_flags, cudaStream_t s);
+// Writes n (even) varied doubles (a store-bandwidth probe, not a result).
+void store_probe(double* p, long long n, unsigned long long seed, cudaStream_t s);
 void zero_absorbing(const GmDev& D, double* d_v, cudaStream_t s);
 
 // Row prologue (RowKernel::compute + fill_axis_masses + box_mass,

@@ -97,6 +97,11 @@ class DeviceBackend:
     def check(self) -> None:
         call("gm_check_device_errors", self.model.handle)
 
+    def begin_sweep(self) -> None:
+        """A new sweep: the OFA row prologue results of the previous one are dropped
+        (gm_step_device caches them across the steps of one sweep)."""
+        call("gm_model_release_ofa_cache", self.model.handle)
+
     def reach(self, x0: int, x1: int) -> tuple[int, int]:
         """Flat interval of V_{k+1} read by the step of states [x0, x1) (gm_shard_reach)."""
         lo, hi = C.c_int64(), C.c_int64()
@@ -193,6 +198,8 @@ def _synthesize_sharded(backend, n_x: int, horizon: int, reach: bool, matrix: bo
     wst = torch.zeros((T, per * world), dtype=torch.int32, device=device)
     vals[T, :n_x] = 0.0 if reach else 1.0
     tm = None
+    if hasattr(backend, "begin_sweep"):
+        backend.begin_sweep()
     if timer:
         timer("build_start")
     if matrix:
