@@ -187,7 +187,8 @@ int64_t gm_model_program_size(const gm_model* m);
  * why, e.g. NVRTC missing or GM_JIT=0). compile_s: NVRTC + load seconds. */
 int32_t gm_model_jit_status(const gm_model* m, double* compile_s, char* why, int64_t why_len);
 /* Compiles (does not load) one run-time kernel of this model with NVRTC: kind 0
- * k_prologue, 1 / 2 the build kernel without / with per-warp line prefixes.
+ * k_prologue, 1 / 2 the build kernel without / with per-warp line prefixes, 3 the
+ * OFA consumer specialised to the row shape (k_expect_ofa_shape).
  * Needs NVRTC but no GPU; GM_ERR_OTHER carries the compiler log on failure. */
 gm_code gm_model_jit_compile(const gm_model* m, int32_t kind, double* seconds, gm_status* st);
 

@@ -321,6 +321,20 @@ static const gmj::Kernels* jit_kernels(gm_model* m, int want, int64_t rows) {
     return k;
 }
 
+// The OFA consumer compiled for the model's row shape (gm_jit.cpp ofa_kernel), or
+// nullptr: same policy as jit_kernels (GM_JIT=1 forces, 0 disables, unset: launches
+// over >= 2^21 rows); GM_OFA_SHAPE=0 keeps the ahead-of-time consumers.
+static const void* ofa_jit(gm_model* m, int64_t rows) {
+    static const char* off = std::getenv("GM_OFA_SHAPE");
+    if (off && off[0] == '0') return nullptr;
+    const char* env = std::getenv("GM_JIT");
+    if ((env && env[0] == '0') || (!env && rows < (int64_t(1) << 21))) return nullptr;
+    if (m->M.noise.family == GM_CUSTOM) return nullptr;
+    std::string why;
+    double cs = 0.0;
+    return gmj::ofa_kernel(gmj::ofa_shape_defines(m->D), &cs, &why);
+}
+
 struct gm_matrix {
     int device = -1;
     int64_t row_begin = 0, row_end = 0, R = 0;
@@ -638,12 +652,13 @@ bool ofa_cached_step(gm_model* m, int64_t r0, int64_t n, const double* v_next, c
     }
     const bool reach = m->M.spec.reach();
     double* vin = m->d_vin.p;
+    const void* JO = ofa_jit(m, n);
     if (hit) {
         for (int64_t c0 = 0; c0 < n; c0 += chunk) {
             const int64_t cn = std::min(chunk, n - c0);
             Launch L(gmk::KF_EXPECT_OFA, s);
             gmk::expect_ofa(m->D, cn, m->ofa_mass.p + c0 * sumW, m->ofa_origin.p + c0, m->ofa_t0x.p + c0,
-                            m->ofa_flag.p + c0, v_next, vin + c0, s);
+                            m->ofa_flag.p + c0, v_next, vin + c0, s, JO);
         }
         return true;
     }
@@ -666,7 +681,7 @@ bool ofa_cached_step(gm_model* m, int64_t r0, int64_t n, const double* v_next, c
         ck(cudaStreamWaitEvent(s, m->ev_ready[b], 0), "ready");
         Launch L(gmk::KF_EXPECT_OFA, s);
         gmk::expect_ofa(m->D, cn, m->ofa_mass.p + c0 * sumW, m->ofa_origin.p + c0, m->ofa_t0x.p + c0,
-                        m->ofa_flag.p + c0, v_next, vin + c0, s);
+                        m->ofa_flag.p + c0, v_next, vin + c0, s, JO);
     }
     ck(cudaEventRecord(m->ev_join, m->aux), "join");
     ck(cudaStreamWaitEvent(s, m->ev_join, 0), "join");
@@ -720,6 +735,7 @@ void step_states(gm_model* m, gm_matrix* tm, int64_t x0, int64_t x1, const doubl
         ensure_scratch(m, chunk);
         const bool reach = m->M.spec.reach();
         const gmj::Kernels* J = jit_kernels(m, gmj::WANT_PROLOGUE, n);
+        const void* JO = ofa_jit(m, n);
         pipeline(
             m, n, chunk, s,
             [&](int64_t c0, int64_t cn, int b) {
@@ -731,7 +747,7 @@ void step_states(gm_model* m, gm_matrix* tm, int64_t x0, int64_t x1, const doubl
             [&](int64_t c0, int64_t cn, int b) {
                 Launch L(gmk::KF_EXPECT_OFA, s);
                 gmk::expect_ofa(m->D, cn, m->d_mass[b].p, m->d_origin[b].p, m->d_t0x[b].p, m->d_rowflag[b].p,
-                                v_next, m->d_vin.p + c0, s);
+                                v_next, m->d_vin.p + c0, s, JO);
             });
     }
     Launch L(gmk::KF_MAXMIN, s);
@@ -1141,8 +1157,10 @@ gm_code gm_model_jit_compile(const gm_model* m, int32_t kind, double* seconds, g
     return guarded(st, [&] {
         // kind 2 with the model's row-shape specialisation, as the launcher compiles it
         const char* js = std::getenv("GM_JIT_SHAPE");
-        const std::string shape =
-            kind == 2 && !(js && js[0] == '0') ? gmj::shape_defines(m->M.device_descriptor()) : std::string();
+        const std::string shape = kind == 3 ? gmj::ofa_shape_defines(m->M.device_descriptor())
+                                  : kind == 2 && !(js && js[0] == '0') ? gmj::shape_defines(m->M.device_descriptor())
+                                                                       : std::string();
+        if (kind == 3 && shape.empty()) throw ConfigErr("the model's row shape does not qualify for the OFA kernel");
         const std::string err = gmj::compile_only(m->M.prog, m->M.X.dim(), m->M.U.dim(), m->M.W.dim(), kind, seconds, shape);
         if (!err.empty()) throw std::runtime_error(err);
     });

@@ -20,6 +20,7 @@ namespace gmj {
 struct Kernels {
     const void* build_ws[2] = {nullptr, nullptr}; // k_build_ws<false>, k_build_ws<true>
     const void* prologue = nullptr;              // k_prologue
+    const void* ofa = nullptr;                   // k_expect_ofa_shape (kind 3)
     double compile_s = 0.0;
 };
 
@@ -34,6 +35,12 @@ enum Want { WANT_PROLOGUE = 1, WANT_BUILD_NOQS = 2, WANT_BUILD_QS = 4 };
 // load failure, GM_JIT=0).
 const Kernels* kernels_for(const gmh::Program& P, int n, int m, int p, int want, std::string* why,
                            const std::string& shape = "");
+
+// #defines that specialise the OFA consumer to a row shape (gm_ofa.cuh GM_OFA_SHAPE),
+// or "" when the shape does not qualify; the compiled kernel for them (cached per
+// process and on disk), nullptr with the reason in *why.
+std::string ofa_shape_defines(const GmDev& D);
+const void* ofa_kernel(const std::string& shape, double* compile_s, std::string* why);
 
 // #defines that specialise the per-warp-Q build kernel (k_build_ws<true>) to one row
 // shape (gm_rowdev.cuh GM_FILL_*), or "" when the shape does not qualify.

@@ -61,7 +61,7 @@ void build(const GmDev& D, long long row0, long long nrows, long long* origin_ou
 // Expected value per row, on the fly (synthesis.cpp:100-104) from prologue data.
 void expect_ofa(const GmDev& D, long long nrows, const double* mass, const long long* origin,
                 const double* t0x, const uint8_t* rowflag, const double* V, double* v_in,
-                cudaStream_t s);
+                cudaStream_t s, const void* jit_shape = nullptr);
 
 // Expected value per row from a stored matrix (synthesis.cpp:95-99); row0 is the
 // absolute index of the matrix's first row, rows [row0+r_lo, row0+r_hi) are processed
