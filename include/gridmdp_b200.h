@@ -206,7 +206,7 @@ int64_t gm_launch_count(void);
  * family: 0 build, 1 target-hit, 2 mask, 3 expect-matrix, 4 expect-ofa, 5 maxmin. */
 double gm_last_kernel_ms(int32_t family);
 /* Kernel variant the last launch of a family used, e.g. "k_expect_ofa_pk<P,2,5>" or
- * "k_build_ws<1,3> (NVRTC)"; "" before the first launch. */
+ * "k_build_ws<1,3>+NVRTC"; "" before the first launch. */
 const char* gm_last_kernel_variant(int32_t family);
 /* Enables per-launch CUDA-event timing of the kernel families above (default off). */
 void gm_enable_kernel_timing(int32_t on);

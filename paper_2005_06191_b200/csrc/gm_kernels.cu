@@ -1112,7 +1112,7 @@ void build(const GmDev& D, long long row0, long long nrows, long long* origin_ou
                 void* args[] = {&Dv,    &row0,       &nrows,    &rb_i,      &npw_i, &ncw_i,
                                 &opts_i, &origin_out, &t0x_out, &probs_out, &d_err};
                 note_variant(KF_BUILD, "k_build_ws<%d,%d>%s", qs ? 1 : 0, ctas,
-                             (jit_ws && jit_ws[qs ? 1 : 0]) ? " (NVRTC)" : "");
+                             (jit_ws && jit_ws[qs ? 1 : 0]) ? "+NVRTC" : "");
                 const cudaError_t e = cudaLaunchKernel(k, dim3(static_cast<unsigned>(std::max<long long>(grid, 1))),
                                                        dim3(kThreads), args, smem, s);
                 if (e != cudaSuccess) throw std::runtime_error(std::string("build: ") + cudaGetErrorString(e));
@@ -1209,7 +1209,7 @@ void expect_ofa(const GmDev& D, long long nrows, const double* mass, const long 
     static const char* ou = std::getenv("GM_OFA_U");
     static const char* opk = std::getenv("GM_OFA_PK");
     if (jit_shape && b.tab == TAB_Q && b.table_in_smem == 1 && !ou && !(opk && opk[0] == '1')) {
-        note_variant(KF_EXPECT_OFA, "k_expect_ofa_shape (NVRTC)");
+        note_variant(KF_EXPECT_OFA, "k_expect_ofa_shape<NVRTC>");
         if (b.smem > 48 * 1024)
             cudaFuncSetAttribute(jit_shape, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(b.smem));
         const long long batches = (nrows + b.rb - 1) / b.rb;
