@@ -910,8 +910,11 @@ BatchPlan plan_batches(const GmDev& D, bool ofa) {
     // GM_OFA_TABLE (tuning / tests): "global" or "prefix" forces TAB_P with that table.
     static const char* ft = std::getenv("GM_OFA_TABLE");
     const int force = !ft ? -1 : (std::string(ft) == "global" ? 0 : (std::string(ft) == "prefix" ? 2 : -1));
-    const Opt opts[] = {{TAB_Q, 1, kSoftSmem}, {TAB_Q, 0, kSoftSmem}, {TAB_P, 1, kSoftSmem},
-                        {TAB_P, 2, kSoftSmem}, {TAB_P, 2, kMidSmem}, {TAB_P, 0, kSoftSmem}, {TAB_P, 2, kHardSmem},
+    // GM_OFA_SMEM_KB (tuning): the OFA plans' soft shared-memory budget per CTA (rows per batch)
+    static const char* osk = std::getenv("GM_OFA_SMEM_KB");
+    const size_t soft = (ofa && osk) ? static_cast<size_t>(std::atoi(osk)) * 1024 : kSoftSmem;
+    const Opt opts[] = {{TAB_Q, 1, soft}, {TAB_Q, 0, soft}, {TAB_P, 1, soft},
+                        {TAB_P, 2, soft}, {TAB_P, 2, kMidSmem}, {TAB_P, 0, soft}, {TAB_P, 2, kHardSmem},
                         {TAB_P, 0, kHardSmem}};
     for (const Opt& o : opts) {
         const size_t per = o.tab == TAB_Q ? q_row : p_row;

@@ -405,6 +405,30 @@ struct OfaDot {
     }
 };
 
+// Two rows per lane group in flight (GM_OFA_ROWS 2): two independent fma chains, each
+// in its row's canonical order, sharing the line-offset loads.
+template <int I>
+struct OfaDot2 {
+    static __device__ __forceinline__ void run(double& sA, double& sB, const unsigned* qA, const unsigned* qB,
+                                               const unsigned* la, const double* mA, const double* mB,
+                                               const double* const* vA, const double* const* vB, int lane) {
+        constexpr int S = I % kOfaPer, B = I / kOfaPer;
+        if ((I + 1) * kOfaTpr <= kOfaR || lane + I * kOfaTpr < kOfaR) {
+            const int off = ofa_lds_s32<4 * kOfaDl * B>(la[S]);
+            const double pA = ofa_lds_f64<8 * kOfaDl * B>(qA[S]) * mA[S];
+            const double pB = ofa_lds_f64<8 * kOfaDl * B>(qB[S]) * mB[S];
+            const double va = ldg_at(vA[S], off), vb = ldg_at(vB[S], off);
+            sA = fma(pA, va, sA);
+            sB = fma(pB, vb, sB);
+        }
+        if constexpr (I + 1 < kOfaNit) OfaDot2<I + 1>::run(sA, sB, qA, qB, la, mA, mB, vA, vB, lane);
+    }
+};
+
+#ifndef GM_OFA_ROWS
+#define GM_OFA_ROWS 1
+#endif
+
 extern "C" __global__ void __launch_bounds__(kThreads) k_expect_ofa_shape(GmDev D, long long nrows, int rb,
                                                                         GmFastDiv div_rb,
                                                                         const double* __restrict__ mass,
@@ -437,6 +461,43 @@ extern "C" __global__ void __launch_bounds__(kThreads) k_expect_ofa_shape(GmDev 
         __syncthreads();
         stage_rows(D, Y, mass, nrows, b0, rb, div_rb, TAB_Q);
         __syncthreads();
+#if GM_OFA_ROWS == 2
+        for (int it = 0; it < (rb + 2 * groups - 1) / (2 * groups); ++it) {
+            const int iA = g + 2 * it * groups, iB = iA + groups;
+            const long long rA = b0 + iA, rB = b0 + iB;
+            const bool validA = iA < rb && rA < nrows, validB = iB < rb && rB < nrows;
+            const uint8_t fA = validA ? rowflag[rA] : RF_ABSORBED, fB = validB ? rowflag[rB] : RF_ABSORBED;
+            const bool liveA = !(fA & (RF_ABSORBED | RF_ERROR)), liveB = !(fB & (RF_ABSORBED | RF_ERROR));
+            double sA = 0.0, sB = 0.0;
+            if (liveA || liveB) {
+                // a row without terms borrows the other row's operands (its sum is discarded)
+                const int jA = liveA ? iA : iB, jB = liveB ? iB : iA;
+                const long long oA = origin[b0 + jA], oB = origin[b0 + jB];
+                GM_CHECK_SLAB(D, oA);
+                GM_CHECK_SLAB(D, oB);
+                unsigned qA[kOfaPer], qB[kOfaPer];
+                double mA[kOfaPer], mB[kOfaPer];
+                const double *vA[kOfaPer], *vB[kOfaPer];
+#pragma unroll
+                for (int S = 0; S < kOfaPer; ++S) {
+                    qA[S] = sm0 + 8u * static_cast<unsigned>(Y.offQ + jA * kOfaNl + Ls[S]);
+                    qB[S] = sm0 + 8u * static_cast<unsigned>(Y.offQ + jB * kOfaNl + Ls[S]);
+                    mA[S] = g_sm[jA * Y.mw + D.ml_off + ks[S]];
+                    mB[S] = g_sm[jB * Y.mw + D.ml_off + ks[S]];
+                    vA[S] = V + oA + ks[S];
+                    vB[S] = V + oB + ks[S];
+                }
+                OfaDot2<0>::run(sA, sB, qA, qB, la, mA, mB, vA, vB, lane);
+            }
+            sA = group_reduce(sA, kOfaTpr, Y.offR, g * kOfaTpr);
+            sB = group_reduce(sB, kOfaTpr, Y.offR, g * kOfaTpr);
+            if (lane == 0) {
+                if (validA) v_in[rA] = liveA ? (reach ? sA + t0x[rA] : sA) : 0.0;
+                if (validB) v_in[rB] = liveB ? (reach ? sB + t0x[rB] : sB) : 0.0;
+            }
+        }
+        continue;
+#endif
         for (int it = 0; it < iters; ++it) {
             const int i = g + it * groups;
             const long long row = b0 + i;
