@@ -1287,8 +1287,40 @@ gm_code gm_build_shard_host(gm_model* m, int64_t x0, int64_t x1, gm_matrix** out
         ensure_scratch(m, 4096); // the aux stream and events of the producer pipeline
         const gmj::Kernels* J =
             jit_kernels(m, gmk::build_uses_qs(m->D) ? gmj::WANT_BUILD_QS : gmj::WANT_BUILD_NOQS, n);
-        // the rows in a few slices: slice k's origins / T0x travel to the host on the aux
-        // stream while slice k+1 builds
+        // pinned (device-accessible) host buffers: the build kernel writes each row's
+        // origin / T0x to the host itself, next to the device copy, in one launch — the
+        // transfer runs entirely under the build
+        auto mapped = [](void* p) -> void* {
+            if (!p) return nullptr;
+            cudaPointerAttributes a{};
+            if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+                cudaGetLastError();
+                return nullptr;
+            }
+            return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+        };
+        void* oh = mapped(origins_host);
+        void* th = reach ? mapped(t0x_host) : nullptr;
+        static const char* direct_env = std::getenv("GM_BUILD_HOST_DIRECT");
+        const bool direct = !(direct_env && direct_env[0] == '0') && m->M.noise.family != GM_CUSTOM &&
+                            (origins_host == nullptr || oh) && (!reach || t0x_host == nullptr || th) &&
+                            (oh || th);
+        if (direct) {
+            GmDev Dv = m->D;
+            Dv.origin_host = static_cast<long long*>(oh);
+            Dv.t0x_host = static_cast<double*>(th);
+            {
+                Launch L(gmk::KF_BUILD, m->stream);
+                gmk::build(Dv, r0, n, tm->origins.p, reach ? tm->t0x.p : nullptr, tm->probs.p, m->d_err.p, m->stream,
+                           J ? J->build_ws : nullptr);
+            }
+            ck(cudaStreamSynchronize(m->stream), "build");
+            raise_device_error(m);
+            if (fresh) *out = fresh.release();
+            return;
+        }
+        // pageable buffers: the rows in a few slices, slice k's origins / T0x travel to
+        // the host on the aux stream while slice k+1 builds
         const int64_t slices = n >= (int64_t(1) << 16) ? 4 : 1;
         const int64_t per = (n + slices - 1) / slices;
         cudaEvent_t ev[4];

@@ -137,4 +137,9 @@ struct GmDev {
     const double* lits;
     const int* line_off;     // n_lines relative flat offsets of slab lines
     const unsigned char* absorb; // n_x flags (reach specs), may be null
+    // stage (i): optional second destinations of the origins / target-hit values of a
+    // build launch (launch-relative, like its origin_out / t0x_out): pinned host memory
+    // the kernel writes directly (gm_build_shard_host), or null
+    long long* origin_host;
+    double* t0x_host;
 };

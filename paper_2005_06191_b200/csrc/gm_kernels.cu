@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_build(GmDev D, long long row0, 
                         g_sm[offX + i * GMD_MAXD + d] = x[d];
                     }
                     origin_out[r] = flat;
+                    if (D.origin_host) D.origin_host[r] = flat;
                     if (t0x_out) {
                         const bool absorbed = reach && D.absorb != nullptr && D.absorb[ix];
                         double p = 0.0;
@@ -167,6 +168,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_build(GmDev D, long long row0, 
                         }
                         if (!bok) record_error(err, row0 + r);
                         t0x_out[r] = p;
+                        if (D.t0x_host) D.t0x_host[r] = p;
                     }
                 } else {
                     record_error(err, row0 + r);

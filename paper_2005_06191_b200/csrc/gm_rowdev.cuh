@@ -554,6 +554,7 @@ __device__ __forceinline__ void build_prologue(const GmDev& D, const GmIns* spro
                 GM_CHECK_SLAB(D, flat);
                 GM_CHECK(r < nrows && i < rb);
                 origin_out[r] = flat;
+                if (D.origin_host) D.origin_host[r] = flat;
                 if (t0x_out) {
                     const bool absorbed = reach && D.absorb != nullptr && D.absorb[ix];
                     double p = 0.0;
@@ -568,6 +569,7 @@ __device__ __forceinline__ void build_prologue(const GmDev& D, const GmIns* spro
                     }
                     if (!bok) record_error(err, row0 + r);
                     t0x_out[r] = p;
+                    if (D.t0x_host) D.t0x_host[r] = p;
                 }
             } else {
                 record_error(err, row0 + r);

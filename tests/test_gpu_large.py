@@ -125,9 +125,11 @@ def test_smoke_entry():
     __graft_entry__.smoke()
 
 
-def test_build_shard_host_matches_build_and_copy():
-    """gm_build_shard_host (sliced build, origins / T0x streamed to the host) gives the same
-    rows and metadata as gm_build_shard followed by the copies."""
+@pytest.mark.parametrize("pinned", [False, True])
+def test_build_shard_host_matches_build_and_copy(pinned):
+    """gm_build_shard_host gives the same rows and metadata as gm_build_shard followed by
+    the copies: with pageable host buffers (sliced build, copies under the next slice)
+    and with pinned ones (the build kernel writes origins / T0x to the host itself)."""
     import ctypes as C
 
     from paper_2005_06191_b200 import _capi
@@ -137,8 +139,12 @@ def test_build_shard_host_matches_build_and_copy():
     nx, nuw, R = int(s.n_states), int(s.n_inputs) * int(s.n_disturbances), int(s.row_width)
     x0, x1 = 3, nx - 5
     rows = (x1 - x0) * nuw
-    org = np.empty(rows, np.int64)
-    t0x = np.empty(rows, np.float64)
+    if pinned:
+        to, tt = (torch.empty(rows, dtype=dt, pin_memory=True) for dt in (torch.int64, torch.float64))
+        org, t0x = to.numpy(), tt.numpy()
+    else:
+        org = np.empty(rows, np.int64)
+        t0x = np.empty(rows, np.float64)
     h = C.c_void_p()
     _capi.call("gm_build_shard_host", m.handle, C.c_int64(x0), C.c_int64(x1), C.byref(h), _capi.ptr(org),
                _capi.ptr(t0x))
