@@ -576,6 +576,10 @@ def main():
     line.update(cpu)
     if line.get("cpu_baseline_sweep", {}).get("value") and sweep_s:
         line["cpu_baseline_sweep"]["gpu_speedup_sweep"] = line["cpu_baseline_sweep"]["value"] / sweep_s
+        if "e2e_synthesize" in line:  # the whole user-level synthesis against the reference's (OFA: T steps)
+            line["e2e_synthesize"]["reference_synthesize_s"] = line["cpu_baseline_sweep"]["value"]
+            line["e2e_synthesize"]["speedup_vs_reference"] = (line["cpu_baseline_sweep"]["value"] /
+                                                              line["e2e_synthesize"]["seconds"])
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist.is_initialized():

@@ -287,11 +287,10 @@ gm_code gm_step_device(gm_model* m, gm_matrix* tm, int64_t x_begin, int64_t x_en
 gm_code gm_build_shard(gm_model* m, int64_t x_begin, int64_t x_end, gm_matrix** out,
                        gm_status* st);
 /* gm_build_shard that also delivers the shard's origins (and, for reach specs, the
- * target-hit vector) into host memory. Pinned (device-accessible) buffers: the build
- * kernel writes each row's origin / T0x to the host itself while it builds (one
- * launch; GM_BUILD_HOST_DIRECT=0 disables). Pageable buffers: the rows are built in
- * slices and each slice's metadata is copied while the next slice builds. Either
- * output may be NULL. */
+ * target-hit vector) into host memory: the rows are built in slices and each slice's
+ * metadata is copied while the next slice builds (pass pinned buffers for the copies
+ * to overlap; GM_BUILD_HOST_DIRECT=1 with pinned buffers makes the build kernel write
+ * them to the host itself instead). Either output may be NULL. */
 gm_code gm_build_shard_host(gm_model* m, int64_t state_begin, int64_t state_end, gm_matrix** out,
                             int64_t* origins_out, double* t0x_out, gm_status* st);
 /* Halo of a shard (SURVEY.md §8 e): the flat state interval [*lo, *hi) that the

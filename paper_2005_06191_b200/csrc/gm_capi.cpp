@@ -704,6 +704,12 @@ void step_states(gm_model* m, gm_matrix* tm, int64_t x0, int64_t x1, const doubl
         check_matrix_model(tm, m);
         if (m->M.spec.reach() && !tm->has_t0x)
             throw ConfigErr("bellman step: a reach specification needs the matrix's target-hit vector");
+        if (tm->row_begin <= r0 && tm->row_end >= r1 && n > 0 && gmk::step_small_applies(m->D)) {
+            Launch L(gmk::KF_EXPECT_MATRIX, s);
+            if (gmk::step_small(m->D, x0, x1 - x0, tm->probs.p, r0 - tm->row_begin, tm->origins.p,
+                                tm->has_t0x ? tm->t0x.p : nullptr, v_next, m->d_vin.p, v_out, pol, wst, s))
+                return; // both passes done (small states)
+        }
         if (tm->row_begin > r0 || tm->row_end < r1)
             throw ConfigErr("bellman step: the matrix does not cover the requested states");
         Launch L(gmk::KF_EXPECT_MATRIX, s);
@@ -1287,9 +1293,11 @@ gm_code gm_build_shard_host(gm_model* m, int64_t x0, int64_t x1, gm_matrix** out
         ensure_scratch(m, 4096); // the aux stream and events of the producer pipeline
         const gmj::Kernels* J =
             jit_kernels(m, gmk::build_uses_qs(m->D) ? gmj::WANT_BUILD_QS : gmj::WANT_BUILD_NOQS, n);
-        // pinned (device-accessible) host buffers: the build kernel writes each row's
-        // origin / T0x to the host itself, next to the device copy, in one launch — the
-        // transfer runs entirely under the build
+        // GM_BUILD_HOST_DIRECT=1 with pinned (device-accessible) host buffers: the build
+        // kernel writes each row's origin / T0x to the host itself, next to the device
+        // copy, in one launch. Measured slower (C2b: 49 ms vs 21 ms end to end; the
+        // scattered 8-byte host writes throttle the kernel), so the sliced copies are the
+        // default
         auto mapped = [](void* p) -> void* {
             if (!p) return nullptr;
             cudaPointerAttributes a{};
@@ -1302,7 +1310,7 @@ gm_code gm_build_shard_host(gm_model* m, int64_t x0, int64_t x1, gm_matrix** out
         void* oh = mapped(origins_host);
         void* th = reach ? mapped(t0x_host) : nullptr;
         static const char* direct_env = std::getenv("GM_BUILD_HOST_DIRECT");
-        const bool direct = !(direct_env && direct_env[0] == '0') && m->M.noise.family != GM_CUSTOM &&
+        const bool direct = (direct_env && direct_env[0] == '1') && m->M.noise.family != GM_CUSTOM &&
                             (origins_host == nullptr || oh) && (!reach || t0x_host == nullptr || th) &&
                             (oh || th);
         if (direct) {

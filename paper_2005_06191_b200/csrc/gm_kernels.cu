@@ -445,6 +445,99 @@ __global__ void __launch_bounds__(kThreads, MINB) k_expect_matrix_et2(GmDev D, l
     }
 }
 
+// Stage (ii), stored matrix, both passes in one kernel for small states (all
+// n_u*n_w rows of a state fit one CTA: n_u*n_w*TPR <= 256 threads): each CTA
+// copies the rows of `spb` consecutive states (contiguous in the matrix) into
+// shared memory with coalesced evict-first loads, every row group reduces its row
+// exactly as k_expect_matrix_et (lane-strided fma in increasing t, the TPR-lane
+// butterfly), and one thread per state runs pass 2 as k_maxmin does (strict <
+// over w, strict > over u, lowest-index ties, clamp): the same bits, one launch
+// per step and no v_in round trip (C2a: R = 27, 25 rows per state).
+template <int TPR>
+__global__ void __launch_bounds__(kThreads) k_step_small(GmDev D, long long x0, long long nx, int spb,
+                                                        const double* __restrict__ probs, long long r_base,
+                                                        const long long* __restrict__ origins,
+                                                        const double* __restrict__ t0x,
+                                                        const double* __restrict__ V, double* __restrict__ v_in,
+                                                        double* __restrict__ v_out, uint32_t* __restrict__ pol,
+                                                        uint32_t* __restrict__ wst) {
+    const int R = static_cast<int>(D.R);
+    const int nuw = static_cast<int>(D.n_u * D.n_w);
+    const long long pitch = D.pitch;
+    int* E = reinterpret_cast<int*>(g_sm);
+    const int offS = (R + 1) / 2; // doubles after E
+    double* stage = g_sm + offS;
+    double* vrow = stage + static_cast<long long>(spb) * nuw * pitch;
+    GM_CHECK(static_cast<unsigned>(8 * (offS + spb * nuw * pitch + spb * nuw)) <= gm_dyn_smem_bytes());
+    for (int t = threadIdx.x; t < R; t += kThreads) {
+        const int L = D.div_Wl.div(t);
+        E[t] = D.line_off[L] + (t - L * D.Wl);
+        GM_CHECK(E[t] >= 0 && E[t] <= slab_span(D));
+    }
+    const int G = nuw * TPR;
+    const int st = threadIdx.x / G, w = threadIdx.x - st * G, j = w / TPR, lane = w - j * TPR;
+    const bool reach = D.spec_kind != GM_SPEC_SAFETY;
+    for (long long xs = static_cast<long long>(blockIdx.x) * spb; xs < nx;
+         xs += static_cast<long long>(gridDim.x) * spb) {
+        const int ns = static_cast<int>(nx - xs < spb ? nx - xs : spb);
+        const long long rl0 = r_base + xs * nuw; // first matrix row of the chunk
+        const long long nd = static_cast<long long>(ns) * nuw * pitch;
+        __syncthreads();
+        const double* src = probs + rl0 * pitch;
+        for (long long c = threadIdx.x; c < nd; c += kThreads) stage[c] = __ldcs(src + c);
+        __syncthreads();
+        const bool active = st < ns;
+        const long long x = x0 + xs + (active ? st : 0);
+        const bool skip = !active || (reach && D.absorb != nullptr && D.absorb[x]);
+        const long long r = rl0 + static_cast<long long>(active ? st : 0) * nuw + j;
+        double s = 0.0;
+        if (!skip) {
+            GM_CHECK_SLAB(D, origins[r]);
+            const double* pr = stage + (static_cast<long long>(st) * nuw + j) * pitch;
+            const double* vb = V + origins[r];
+            for (int t = lane; t < R; t += TPR) s = fma(pr[t], ldg_at(vb, E[t]), s);
+        }
+        for (int off = TPR >> 1; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (active && lane == 0) {
+            const double vr = skip ? 0.0 : (reach ? s + t0x[r] : s);
+            vrow[st * nuw + j] = vr;
+            v_in[(xs + st) * nuw + j] = vr; // the step's row values stay readable (gm_copy_row_values)
+        }
+        __syncthreads();
+        if (threadIdx.x < ns) { // pass 2 (synthesis.cpp:112-142), as k_maxmin
+            const long long xi = xs + threadIdx.x, xx = x0 + xi;
+            if (reach && D.absorb != nullptr && D.absorb[xx]) {
+                v_out[xi] = 0.0;
+                if (pol) pol[xi] = 0;
+                if (wst) wst[xi] = 0;
+            } else {
+                const double* q = vrow + threadIdx.x * nuw;
+                double best = -INFINITY;
+                uint32_t bu = 0, bw = 0;
+                for (int iu = 0; iu < D.n_u; ++iu) {
+                    double mn = INFINITY;
+                    uint32_t mw = 0;
+                    for (int iw = 0; iw < D.n_w; ++iw) {
+                        const double v = q[iu * D.n_w + iw];
+                        if (v < mn) {
+                            mn = v;
+                            mw = static_cast<uint32_t>(iw);
+                        }
+                    }
+                    if (mn > best) {
+                        best = mn;
+                        bu = static_cast<uint32_t>(iu);
+                        bw = mw;
+                    }
+                }
+                v_out[xi] = smin(1.0, smax(0.0, best));
+                if (pol) pol[xi] = bu;
+                if (wst) wst[xi] = bw;
+            }
+        }
+    }
+}
+
 // min over w (strict <, ascending), then max over u (strict >, ascending):
 // lowest-index ties (synthesis.cpp:112-142). L lanes per state.
 template <int L>
@@ -1361,6 +1454,46 @@ unsigned long long count_positive(const double* p, long long n, unsigned long lo
     cudaMemcpyAsync(&h, d_count, sizeof h, cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
     return h;
+}
+
+// states per CTA of k_step_small (0: not applicable; GM_STEP_FUSED=0 disables it)
+static long long step_small_spb(const GmDev& D) {
+    static const char* off = std::getenv("GM_STEP_FUSED");
+    if (off && off[0] == '0') return 0;
+    const long long nuw = D.n_u * D.n_w;
+    if (D.tpr > 32 || nuw * D.tpr > kThreads) return 0;
+    const long long per_state = nuw * (D.pitch + 1) * 8;
+    const long long fixed = (D.R + 1) / 2 * 8;
+    return std::max<long long>(0, std::min<long long>(kThreads / (nuw * D.tpr), (48 * 1024 - fixed) / per_state));
+}
+
+bool step_small_applies(const GmDev& D) { return step_small_spb(D) >= 1; }
+
+bool step_small(const GmDev& D, long long x0, long long nx, const double* probs, long long r_base,
+                const long long* origins, const double* t0x, const double* V, double* v_in, double* v_out,
+                uint32_t* pol, uint32_t* wst, cudaStream_t s) {
+    const long long spb = step_small_spb(D);
+    if (spb < 1 || nx <= 0) return false;
+    const long long nuw = D.n_u * D.n_w;
+    const long long per_state = nuw * (D.pitch + 1) * 8;
+    const long long fixed = (D.R + 1) / 2 * 8;
+    const size_t smem = static_cast<size_t>(fixed + spb * per_state);
+    const long long chunks = (nx + spb - 1) / spb;
+    note_variant(KF_EXPECT_MATRIX, "k_step_small<%d>", D.tpr);
+    switch (D.tpr) {
+#define GM_SS(T)                                                                                                      \
+    case T: {                                                                                                         \
+        auto k = k_step_small<T>;                                                                                     \
+        k<<<resident_grid(k, smem, chunks), kThreads, smem, s>>>(D, x0, nx, static_cast<int>(spb), probs, r_base,     \
+                                                                 origins, t0x, V, v_in, v_out, pol, wst);             \
+        break;                                                                                                        \
+    }
+        GM_SS(1) GM_SS(2) GM_SS(4) GM_SS(8) GM_SS(16) GM_SS(32)
+#undef GM_SS
+    default: return false;
+    }
+    check_launch("step_small");
+    return true;
 }
 
 void maxmin(const GmDev& D, long long x0, long long nx, const double* v_in, double* v_out,

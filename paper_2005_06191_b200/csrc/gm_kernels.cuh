@@ -31,6 +31,14 @@ BatchPlan plan_batches(const GmDev& D, bool ofa);
 const char* last_variant(int family);
 
 void absorb_flags(const GmDev& D, uint8_t* d_flags, cudaStream_t s);
+// Both passes of one stored-matrix step for states [x0, x0+nx) in one kernel when a
+// state's rows fit a CTA (k_step_small); probs/origins/t0x are the matrix's arrays,
+// r_base the matrix row of state x0's first row. False: not applicable (the caller
+// runs expect_matrix + maxmin).
+bool step_small_applies(const GmDev& D);
+bool step_small(const GmDev& D, long long x0, long long nx, const double* probs, long long r_base,
+                const long long* origins, const double* t0x, const double* V, double* v_in, double* v_out,
+                uint32_t* pol, uint32_t* wst, cudaStream_t s);
 // Writes n (even) varied doubles (a store-bandwidth probe, not a result).
 void store_probe(double* p, long long n, unsigned long long seed, cudaStream_t s);
 void zero_absorbing(const GmDev& D, double* d_v, cudaStream_t s);

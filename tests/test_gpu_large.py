@@ -12,6 +12,7 @@ oracle on sampled rows/states, plus size-independent properties:
   * matrix == OFA bit for bit on a mid-size configuration.
 """
 import ctypes as C
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -159,3 +160,20 @@ def test_build_shard_host_matches_build_and_copy(pinned):
     _capi.lib.gm_matrix_free(h2)
     assert np.array_equal(org, org2) and np.array_equal(t0x.view(np.uint64), t0x2.view(np.uint64))
     assert np.array_equal(p1.view(np.uint64), p2.view(np.uint64))
+
+
+def test_build_shard_host_direct_host_writes():
+    """GM_BUILD_HOST_DIRECT=1 (the build kernel writes origins / T0x into pinned host
+    memory itself) gives the same metadata as the default sliced copies."""
+    import subprocess
+    import sys
+    code = """
+import sys; sys.path.insert(0, %r); sys.path.insert(0, %r)
+import test_gpu_large as T
+T.test_build_shard_host_matches_build_and_copy(True)
+print("direct ok")
+""" % (str(Path(__file__).resolve().parents[1]), str(Path(__file__).resolve().parent))
+    import os
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, GM_BUILD_HOST_DIRECT="1"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "direct ok" in r.stdout, r.stderr[-2000:]
