@@ -230,13 +230,14 @@ def _synthesize_sharded(backend, n_x: int, horizon: int, reach: bool, matrix: bo
         vals[:T] = full.view(world, T, per).permute(1, 0, 2).reshape(T, world * per)
     if timer:
         timer("sweep_end")
-    if dist.is_initialized():
-        pol_full = torch.empty_like(pol)
-        wst_full = torch.empty_like(wst)
-        for src, dst in ((pol, pol_full), (wst, wst_full)):
-            for k in range(T):
-                dist.all_gather_into_tensor(dst[k], src[k, lo:lo + per].contiguous(), group=group)
-        pol, wst = pol_full, wst_full
+    if dist.is_initialized() and world > 1:
+        # policies and worst disturbances of every step in one collective: each rank's
+        # (2T, per) columns, gathered rank-major, then reordered to (T, world * per)
+        mine = torch.cat([pol[:, lo:lo + per], wst[:, lo:lo + per]], 0).contiguous()
+        full = torch.empty((world * 2 * T, per), dtype=mine.dtype, device=mine.device)
+        dist.all_gather_into_tensor(full, mine, group=group)
+        full = full.view(world, 2 * T, per).permute(1, 0, 2).reshape(2 * T, world * per)
+        pol, wst = full[:T], full[T:]
     return vals[:, :n_x], pol[:, :n_x], wst[:, :n_x]
 
 
