@@ -1456,10 +1456,13 @@ unsigned long long count_positive(const double* p, long long n, unsigned long lo
     return h;
 }
 
-// states per CTA of k_step_small (0: not applicable; GM_STEP_FUSED=0 disables it)
+// states per CTA of k_step_small (0: not applicable). Opt-in (GM_STEP_FUSED=1): measured
+// slower than expect_matrix + maxmin on the small configurations it applies to (C2a
+// sweep 1.2 vs 1.0 ms, C3n 0.4 vs 0.3 ms: the CTA-wide staging and the one-thread-per-
+// state pass 2 serialise more than the second launch costs)
 static long long step_small_spb(const GmDev& D) {
-    static const char* off = std::getenv("GM_STEP_FUSED");
-    if (off && off[0] == '0') return 0;
+    static const char* on = std::getenv("GM_STEP_FUSED");
+    if (!(on && on[0] == '1')) return 0;
     const long long nuw = D.n_u * D.n_w;
     if (D.tpr > 32 || nuw * D.tpr > kThreads) return 0;
     const long long per_state = nuw * (D.pitch + 1) * 8;

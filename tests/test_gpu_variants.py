@@ -69,7 +69,7 @@ SETTINGS = [
     {"GM_OFA_PK": "1"},  # OFA with the hoisted last-axis cell (row_dot_pk; default only for long rows)
     {"GM_OFA_PK": "1", "GM_OFA_TABLE": "prefix"},
     {"GM_OFA_CACHE": "0"},  # OFA row prologue re-run every step instead of cached across the sweep
-    {"GM_STEP_FUSED": "0"},  # small states: expect_matrix + maxmin instead of the fused k_step_small
+    {"GM_STEP_FUSED": "1"},  # small states: both passes in one kernel (k_step_small) instead of two
     {"GM_JIT_SHAPE": "0", "GM_JIT": "1"},  # run-time compiled build without the row-shape specialisation
 ]
 
