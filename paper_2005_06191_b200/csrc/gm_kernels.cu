@@ -353,6 +353,86 @@ __global__ void __launch_bounds__(kThreads, MINB) k_expect_matrix_et(GmDev D, lo
     }
 }
 
+// Stage (ii), stored matrix, short rows (TPR <= 4: R < 64). The rows of a warp's
+// chunk (32/TPR rows) are contiguous in the matrix, so the warp stages the chunk in
+// shared memory with coalesced 8-byte cp.async copies, double-buffered (chunk c+1
+// in flight while chunk c is reduced); each row group then reduces its row from
+// shared memory exactly as k_expect_matrix_et does (lane-strided fma in increasing
+// t, the TPR-lane butterfly): the same bits, without the per-lane strided loads
+// of rows 27-32 doubles apart that leave those sweeps at 25-30 % of HBM.
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int TPR>
+__global__ void __launch_bounds__(kThreads) k_expect_matrix_small(GmDev D, long long row0, long long r_lo,
+                                                                 long long r_hi, int chunk_len,
+                                                                 const double* __restrict__ probs,
+                                                                 const long long* __restrict__ origins,
+                                                                 const double* __restrict__ t0x,
+                                                                 const double* __restrict__ V,
+                                                                 double* __restrict__ v_in) {
+    constexpr int RPC = 32 / TPR; // rows per warp chunk
+    const int R = static_cast<int>(D.R);
+    const long long pitch = D.pitch;
+    int* E = reinterpret_cast<int*>(g_sm);
+    const int offB = (R + 1) / 2;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* buf = g_sm + offB + static_cast<long long>(warp) * 2 * chunk_len;
+    GM_CHECK(static_cast<unsigned>(8 * (offB + (kThreads / 32) * 2 * chunk_len)) <= gm_dyn_smem_bytes());
+    GM_CHECK(chunk_len == RPC * pitch);
+    for (int t = threadIdx.x; t < R; t += kThreads) {
+        const int L = D.div_Wl.div(t);
+        E[t] = D.line_off[L] + (t - L * D.Wl);
+        GM_CHECK(E[t] >= 0 && E[t] <= slab_span(D));
+    }
+    __syncthreads();
+    const bool reach = D.spec_kind != GM_SPEC_SAFETY;
+    const long long nrows = r_hi - r_lo, nuw = D.n_u * D.n_w;
+    const long long nchunks = (nrows + RPC - 1) / RPC;
+    const long long wstride = static_cast<long long>(gridDim.x) * (kThreads / 32);
+    const int j = lane / TPR, q = lane % TPR; // row of the chunk, lane within the row group
+    auto issue = [&](long long c, int b) {
+        if (c < nchunks) {
+            const long long rc = r_lo + c * RPC;
+            const long long len = (nrows - c * RPC < RPC ? nrows - c * RPC : RPC) * pitch;
+            const double* src = probs + rc * pitch;
+            double* dst = buf + b * chunk_len;
+            for (long long e = lane; e < len; e += 32) cp_async8(dst + e, src + e);
+        }
+        cp_async_commit(); // an empty group keeps the wait counts uniform
+    };
+    long long c = static_cast<long long>(blockIdx.x) * (kThreads / 32) + warp;
+    issue(c, 0);
+    for (int b = 0; c < nchunks; c += wstride, b ^= 1) {
+        issue(c + wstride, b ^ 1);
+        cp_async_wait<1>(); // chunk c has landed
+        __syncwarp();
+        const long long rl = c * RPC + j; // local row
+        const bool valid = rl < nrows;
+        const long long r = r_lo + rl;
+        bool skip = !valid;
+        if (valid && reach && D.absorb != nullptr) skip = D.absorb[(row0 + r) / nuw];
+        double s = 0.0;
+        if (!skip) {
+            GM_CHECK_SLAB(D, origins[r]);
+            const double* pr = buf + b * chunk_len + j * pitch;
+            const double* vb = V + origins[r];
+            for (int t = q; t < R; t += TPR) s = fma(pr[t], ldg_at(vb, E[t]), s);
+        }
+        for (int off = TPR >> 1; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (valid && q == 0) v_in[rl] = skip ? 0.0 : (reach ? s + t0x[r] : s);
+        __syncwarp(); // the buffer is refilled by the next issue
+    }
+    cp_async_wait<0>();
+}
+
 // One row's lane-strided partial sum of k_expect_matrix_et (canonical order: terms
 // t = lane, lane+TPR, ... with fma in increasing t; the zero-padded tail adds +0).
 template <int TPR, int U>
@@ -1348,6 +1428,31 @@ void expect_matrix(const GmDev& D, long long row0, long long r_lo, long long r_h
     // registers (21.3 ms), V staged per chunk of states in shared memory (23.2 ms);
     // contiguous rows per CTA (GM_CONTIG=1): equal.
     const size_t et_smem = (kThreads / 32) * sizeof(double) + static_cast<size_t>(D.R) * sizeof(int);
+    // short rows: warp-staged cp.async chunks (k_expect_matrix_small); GM_MATRIX_SMALL=0 off
+    static const char* msm = std::getenv("GM_MATRIX_SMALL");
+    if (!(force && std::string(force) == "walk") && !(msm && msm[0] == '0') && D.tpr <= 4) {
+        const int chunk_len = static_cast<int>((32 / D.tpr) * D.pitch);
+        const size_t smem = static_cast<size_t>((D.R + 1) / 2 + (kThreads / 32) * 2 * chunk_len) * sizeof(double);
+        if (smem <= 100 * 1024) {
+            const long long chunks = (r_hi - r_lo + 32 / D.tpr - 1) / (32 / D.tpr);
+            const long long ctas = (chunks + kThreads / 32 - 1) / (kThreads / 32);
+            note_variant(KF_EXPECT_MATRIX, "k_expect_matrix_small<%d>", D.tpr);
+            switch (D.tpr) {
+#define GM_MS(T)                                                                                              \
+    case T: {                                                                                                 \
+        auto k = k_expect_matrix_small<T>;                                                                    \
+        allow_smem(k, smem);                                                                                  \
+        k<<<resident_grid(k, smem, ctas), kThreads, smem, s>>>(D, row0, r_lo, r_hi, chunk_len, probs, origins, \
+                                                              t0x, V, v_in);                                  \
+        check_launch("expect_matrix");                                                                        \
+        return;                                                                                               \
+    }
+                GM_MS(1) GM_MS(2) GM_MS(4)
+#undef GM_MS
+            default: break;
+            }
+        }
+    }
     if (!(force && std::string(force) == "walk") && et_smem <= kHardSmem) {
         const long long nuw = D.n_u * D.n_w;
         const int div32 = (row0 + r_hi <= INT_MAX && nuw <= INT_MAX) ? 1 : 0;
