@@ -372,13 +372,13 @@ __device__ __forceinline__ void cp_async_wait() {
 
 template <int TPR>
 __global__ void __launch_bounds__(kThreads) k_expect_matrix_small(GmDev D, long long row0, long long r_lo,
-                                                                 long long r_hi, int chunk_len,
+                                                                 long long r_hi, int rpc, int chunk_len,
                                                                  const double* __restrict__ probs,
                                                                  const long long* __restrict__ origins,
                                                                  const double* __restrict__ t0x,
                                                                  const double* __restrict__ V,
                                                                  double* __restrict__ v_in) {
-    constexpr int RPC = 32 / TPR; // rows per warp chunk
+    const int RPC = rpc; // rows per warp chunk (<= 32 / TPR: lanes past them idle in the dot)
     const int R = static_cast<int>(D.R);
     const long long pitch = D.pitch;
     int* E = reinterpret_cast<int*>(g_sm);
@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(kThreads) k_expect_matrix_small(GmDev D, long 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double* buf = g_sm + offB + static_cast<long long>(warp) * 2 * chunk_len;
     GM_CHECK(static_cast<unsigned>(8 * (offB + (kThreads / 32) * 2 * chunk_len)) <= gm_dyn_smem_bytes());
-    GM_CHECK(chunk_len == RPC * pitch);
+    GM_CHECK(chunk_len == RPC * pitch && RPC * TPR <= 32);
     for (int t = threadIdx.x; t < R; t += kThreads) {
         const int L = D.div_Wl.div(t);
         E[t] = D.line_off[L] + (t - L * D.Wl);
@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(kThreads) k_expect_matrix_small(GmDev D, long 
         cp_async_wait<1>(); // chunk c has landed
         __syncwarp();
         const long long rl = c * RPC + j; // local row
-        const bool valid = rl < nrows;
+        const bool valid = j < RPC && rl < nrows;
         const long long r = r_lo + rl;
         bool skip = !valid;
         if (valid && reach && D.absorb != nullptr) skip = D.absorb[(row0 + r) / nuw];
@@ -1431,10 +1431,16 @@ void expect_matrix(const GmDev& D, long long row0, long long r_lo, long long r_h
     // short rows: warp-staged cp.async chunks (k_expect_matrix_small); GM_MATRIX_SMALL=0 off
     static const char* msm = std::getenv("GM_MATRIX_SMALL");
     if (!(force && std::string(force) == "walk") && !(msm && msm[0] == '0') && D.tpr <= 4) {
-        const int chunk_len = static_cast<int>((32 / D.tpr) * D.pitch);
-        const size_t smem = static_cast<size_t>((D.R + 1) / 2 + (kThreads / 32) * 2 * chunk_len) * sizeof(double);
-        if (smem <= 100 * 1024) {
-            const long long chunks = (r_hi - r_lo + 32 / D.tpr - 1) / (32 / D.tpr);
+        // rows per warp chunk: 32 / TPR, halved until the double buffers fit 56 KB per CTA
+        int rpc = 32 / static_cast<int>(D.tpr);
+        auto bytes = [&](int r) {
+            return static_cast<size_t>((D.R + 1) / 2 + (kThreads / 32) * 2 * r * D.pitch) * sizeof(double);
+        };
+        while (rpc > 1 && bytes(rpc) > kSoftSmem) rpc /= 2;
+        const int chunk_len = static_cast<int>(rpc * D.pitch);
+        const size_t smem = bytes(rpc);
+        if (smem <= kSoftSmem) {
+            const long long chunks = (r_hi - r_lo + rpc - 1) / rpc;
             const long long ctas = (chunks + kThreads / 32 - 1) / (kThreads / 32);
             note_variant(KF_EXPECT_MATRIX, "k_expect_matrix_small<%d>", D.tpr);
             switch (D.tpr) {
@@ -1442,7 +1448,7 @@ void expect_matrix(const GmDev& D, long long row0, long long r_lo, long long r_h
     case T: {                                                                                                 \
         auto k = k_expect_matrix_small<T>;                                                                    \
         allow_smem(k, smem);                                                                                  \
-        k<<<resident_grid(k, smem, ctas), kThreads, smem, s>>>(D, row0, r_lo, r_hi, chunk_len, probs, origins, \
+        k<<<resident_grid(k, smem, ctas), kThreads, smem, s>>>(D, row0, r_lo, r_hi, rpc, chunk_len, probs, origins, \
                                                               t0x, V, v_in);                                  \
         check_launch("expect_matrix");                                                                        \
         return;                                                                                               \
