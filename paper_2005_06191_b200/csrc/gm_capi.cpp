@@ -324,7 +324,7 @@ static const gmj::Kernels* jit_kernels(gm_model* m, int want, int64_t rows) {
 // The OFA consumer compiled for the model's row shape (gm_jit.cpp ofa_kernel), or
 // nullptr: same policy as jit_kernels (GM_JIT=1 forces, 0 disables, unset: launches
 // over >= 2^21 rows); GM_OFA_SHAPE=0 keeps the ahead-of-time consumers.
-static const void* ofa_jit(gm_model* m, int64_t rows) {
+static const gmk::OfaJit* ofa_jit(gm_model* m, int64_t rows, gmk::OfaJit& out) {
     static const char* off = std::getenv("GM_OFA_SHAPE");
     if (off && off[0] == '0') return nullptr;
     const char* env = std::getenv("GM_JIT");
@@ -332,7 +332,8 @@ static const void* ofa_jit(gm_model* m, int64_t rows) {
     if (m->M.noise.family == GM_CUSTOM) return nullptr;
     std::string why;
     double cs = 0.0;
-    return gmj::ofa_kernel(gmj::ofa_shape_defines(m->D), &cs, &why);
+    out.shape = gmj::ofa_kernel(gmj::ofa_shape_defines(m->D), &cs, &why, &out.packed);
+    return out.shape ? &out : nullptr;
 }
 
 struct gm_matrix {
@@ -652,7 +653,8 @@ bool ofa_cached_step(gm_model* m, int64_t r0, int64_t n, const double* v_next, c
     }
     const bool reach = m->M.spec.reach();
     double* vin = m->d_vin.p;
-    const void* JO = ofa_jit(m, n);
+    gmk::OfaJit jo;
+    const gmk::OfaJit* JO = ofa_jit(m, n, jo);
     if (hit) {
         for (int64_t c0 = 0; c0 < n; c0 += chunk) {
             const int64_t cn = std::min(chunk, n - c0);
@@ -741,7 +743,8 @@ void step_states(gm_model* m, gm_matrix* tm, int64_t x0, int64_t x1, const doubl
         ensure_scratch(m, chunk);
         const bool reach = m->M.spec.reach();
         const gmj::Kernels* J = jit_kernels(m, gmj::WANT_PROLOGUE, n);
-        const void* JO = ofa_jit(m, n);
+        gmk::OfaJit jo;
+        const gmk::OfaJit* JO = ofa_jit(m, n, jo);
         pipeline(
             m, n, chunk, s,
             [&](int64_t c0, int64_t cn, int b) {

@@ -424,7 +424,17 @@ __global__ void __launch_bounds__(kThreads) k_expect_matrix_small(GmDev D, long 
             GM_CHECK_SLAB(D, origins[r]);
             const double* pr = buf + b * chunk_len + j * pitch;
             const double* vb = V + origins[r];
-            for (int t = q; t < R; t += TPR) s = fma(pr[t], ldg_at(vb, E[t]), s);
+            // 8 gathers in flight per lane, then their fmas in increasing t
+            constexpr int U = 8;
+            int t = q;
+            for (; t + (U - 1) * TPR < R; t += U * TPR) {
+                double v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) v[u] = ldg_at(vb, E[t + u * TPR]);
+#pragma unroll
+                for (int u = 0; u < U; ++u) s = fma(pr[t + u * TPR], v[u], s);
+            }
+            for (; t < R; t += TPR) s = fma(pr[t], ldg_at(vb, E[t]), s);
         }
         for (int off = TPR >> 1; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
         if (valid && q == 0) v_in[rl] = skip ? 0.0 : (reach ? s + t0x[r] : s);
@@ -1378,9 +1388,38 @@ static void launch_ofa(const GmDev& D, const BatchPlan& b, long long nrows, cons
 
 void expect_ofa(const GmDev& D, long long nrows, const double* mass, const long long* origin,
                 const double* t0x, const uint8_t* rowflag, const double* V, double* v_in,
-                cudaStream_t s, const void* jit_shape) {
+                cudaStream_t s, const OfaJit* jit) {
     if (nrows <= 0) return;
     const BatchPlan b = plan_batches(D, true);
+    // packed (Q, line offset) tables: GM_OFA_PACK=0 keeps the two-table shape kernel
+    static const char* opack = std::getenv("GM_OFA_PACK");
+    if (jit && jit->packed && !(opack && opack[0] == '0') && b.tab == TAB_Q && !std::getenv("GM_OFA_U") &&
+        !(std::getenv("GM_OFA_PK") && std::getenv("GM_OFA_PK")[0] == '1')) {
+        const int groups = kThreads / D.tpr;
+        const size_t per_row = (static_cast<size_t>(D.sumW + 1) + D.P_size + 2 * static_cast<size_t>(D.n_lines)) * 8;
+        const size_t fixed = (1 + kThreads / 32) * 8; // alignment slot + group partials
+        long long rb = static_cast<long long>((kSoftSmem - fixed) / per_row);
+        rb = std::min<long long>(rb, kThreads);
+        if (rb >= groups) {
+            rb -= rb % groups;
+            const size_t smem = fixed + per_row * static_cast<size_t>(rb);
+            note_variant(KF_EXPECT_OFA, "k_expect_ofa_packed<NVRTC>");
+            if (smem > 48 * 1024)
+                cudaFuncSetAttribute(jit->packed, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            const long long batches = (nrows + rb - 1) / rb;
+            const int grid = resident_grid(jit->packed, smem, batches);
+            GmDev Dv = D;
+            long long nr = nrows;
+            int rbi = static_cast<int>(rb);
+            GmFastDiv dv = gm_fastdiv(static_cast<uint32_t>(rb));
+            void* args[] = {&Dv, &nr, &rbi, &dv, &mass, &origin, &t0x, &rowflag, &V, &v_in};
+            const cudaError_t e = cudaLaunchKernel(jit->packed, dim3(grid), dim3(kThreads), args, smem, s);
+            if (e != cudaSuccess) throw std::runtime_error(std::string("expect_ofa: ") + cudaGetErrorString(e));
+            check_launch("expect_ofa");
+            return;
+        }
+    }
+    const void* jit_shape = jit ? jit->shape : nullptr;
     // the consumer compiled for this row shape (gm_ofa.cuh k_expect_ofa_shape: same
     // terms, same order) replaces k_expect_ofa<Q,1,U> unless a tuning knob asks for
     // another kernel

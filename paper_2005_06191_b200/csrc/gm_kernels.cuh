@@ -67,9 +67,14 @@ void build(const GmDev& D, long long row0, long long nrows, long long* origin_ou
            double* probs_out, unsigned long long* d_err, cudaStream_t s, const void* const* jit_ws = nullptr);
 
 // Expected value per row, on the fly (synthesis.cpp:100-104) from prologue data.
+// run-time compiled OFA consumers for the model's row shape (gm_ofa.cuh), or null
+struct OfaJit {
+    const void* shape = nullptr;  // k_expect_ofa_shape
+    const void* packed = nullptr; // k_expect_ofa_packed
+};
 void expect_ofa(const GmDev& D, long long nrows, const double* mass, const long long* origin,
                 const double* t0x, const uint8_t* rowflag, const double* V, double* v_in,
-                cudaStream_t s, const void* jit_shape = nullptr);
+                cudaStream_t s, const OfaJit* jit = nullptr);
 
 // Expected value per row from a stored matrix (synthesis.cpp:95-99); row0 is the
 // absolute index of the matrix's first row, rows [row0+r_lo, row0+r_hi) are processed

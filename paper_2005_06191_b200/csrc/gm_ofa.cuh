@@ -528,4 +528,101 @@ extern "C" __global__ void __launch_bounds__(kThreads) k_expect_ofa_shape(GmDev 
         }
     }
 }
+
+// The same consumer with each row's line prefix and the line's V offset packed in one
+// 16-byte shared-memory entry (Q[L] as f64, line_off[L] as s32): one LDS.128 per term
+// instead of an LDS.64 and an LDS.32. Shared layout in doubles: masses [rb][mw] | P
+// [rb][P_size] | QO [rb][n_lines][2] | group partials [8].
+template <int OFF>
+__device__ __forceinline__ void ofa_lds_qo(unsigned addr, double& q, int& off) {
+    unsigned long long a, b;
+    asm volatile("ld.shared.v2.u64 {%0, %1}, [%2+%3];" : "=l"(a), "=l"(b) : "r"(addr), "n"(OFF));
+    q = __longlong_as_double(static_cast<long long>(a));
+    off = static_cast<int>(b);
+}
+
+template <int I>
+struct OfaDotQO {
+    static __device__ __forceinline__ double run(double s, const unsigned* qa, const double* ml,
+                                                 const double* const* vb, int lane) {
+        constexpr int S = I % kOfaPer, B = I / kOfaPer;
+        if ((I + 1) * kOfaTpr <= kOfaR || lane + I * kOfaTpr < kOfaR) {
+            double q;
+            int off;
+            ofa_lds_qo<16 * kOfaDl * B>(qa[S], q, off);
+            s = fma(q * ml[S], ldg_at(vb[S], off), s);
+        }
+        if constexpr (I + 1 < kOfaNit) return OfaDotQO<I + 1>::run(s, qa, ml, vb, lane);
+        return s;
+    }
+};
+
+extern "C" __global__ void __launch_bounds__(kThreads) k_expect_ofa_packed(GmDev D, long long nrows, int rb,
+                                                                         GmFastDiv div_rb,
+                                                                         const double* __restrict__ mass,
+                                                                         const long long* __restrict__ origin,
+                                                                         const double* __restrict__ t0x,
+                                                                         const uint8_t* __restrict__ rowflag,
+                                                                         const double* __restrict__ V,
+                                                                         double* __restrict__ v_in) {
+    const Layout Y(D, rb, TAB_P); // masses and P as the P-table consumers lay them out
+    const int offQO = (Y.offQ + 1) & ~1, offR = offQO + 2 * rb * kOfaNl; // 16-byte entries
+    GM_CHECK(D.tpr == kOfaTpr && D.Wl == kOfaWl && D.R == kOfaR && D.n_lines == kOfaNl);
+    GM_CHECK(static_cast<unsigned>(8 * (offR + kThreads / 32)) <= gm_dyn_smem_bytes());
+    constexpr int groups = kThreads / kOfaTpr;
+    const int g = threadIdx.x / kOfaTpr, lane = threadIdx.x - g * kOfaTpr;
+    const unsigned sm0 = static_cast<unsigned>(__cvta_generic_to_shared(g_sm));
+    int Ls[kOfaPer], ks[kOfaPer];
+#pragma unroll
+    for (int S = 0; S < kOfaPer; ++S) {
+        const int t = lane + kOfaTpr * S;
+        Ls[S] = t / kOfaWl;
+        ks[S] = t - Ls[S] * kOfaWl;
+    }
+    const bool reach = D.spec_kind != GM_SPEC_SAFETY;
+    const int iters = (rb + groups - 1) / groups;
+    for (long long b0 = static_cast<long long>(blockIdx.x) * rb; b0 < nrows;
+         b0 += static_cast<long long>(gridDim.x) * rb) {
+        __syncthreads();
+        stage_rows(D, Y, mass, nrows, b0, rb, div_rb, TAB_P); // masses + P
+        __syncthreads();
+        // Q[L] = P[a] * mm[j] (stage_tables' product) next to the line's V offset
+        for (int c = threadIdx.x; c < rb * kOfaNl; c += blockDim.x) {
+            const int i = c / kOfaNl, L = c - i * kOfaNl;
+            const int a = D.div_Wm.div(L), j = L - a * D.Wm;
+            double* e = g_sm + offQO + 2 * c;
+            e[0] = g_sm[Y.offP + i * D.P_size + a] * g_sm[i * Y.mw + D.mm_off + j];
+            e[1] = __longlong_as_double(static_cast<long long>(D.line_off[L]));
+        }
+        __syncthreads();
+        for (int it = 0; it < iters; ++it) {
+            const int i = g + it * groups;
+            const long long row = b0 + i;
+            const bool valid = i < rb && row < nrows;
+            const uint8_t fl = valid ? rowflag[row] : RF_ABSORBED;
+            double s = 0.0;
+            if (!(fl & (RF_ABSORBED | RF_ERROR))) {
+                GM_CHECK_SLAB(D, origin[row]);
+                const int mlo = i * Y.mw + D.ml_off;
+                const double* vrow = V + origin[row];
+                unsigned qa[kOfaPer];
+                double ml[kOfaPer];
+                const double* vb[kOfaPer];
+#pragma unroll
+                for (int S = 0; S < kOfaPer; ++S) {
+                    qa[S] = sm0 + 16u * static_cast<unsigned>(offQO / 2 + i * kOfaNl + Ls[S]);
+                    ml[S] = g_sm[mlo + ks[S]];
+                    vb[S] = vrow + ks[S];
+                }
+                s = OfaDotQO<0>::run(0.0, qa, ml, vb, lane);
+            }
+            s = group_reduce(s, kOfaTpr, offR, g * kOfaTpr);
+            if (valid && lane == 0) {
+                double r = 0.0;
+                if (!(fl & (RF_ABSORBED | RF_ERROR))) r = reach ? s + t0x[row] : s;
+                v_in[row] = r;
+            }
+        }
+    }
+}
 #endif
