@@ -1391,9 +1391,10 @@ void expect_ofa(const GmDev& D, long long nrows, const double* mass, const long 
                 cudaStream_t s, const OfaJit* jit) {
     if (nrows <= 0) return;
     const BatchPlan b = plan_batches(D, true);
-    // packed (Q, line offset) tables: GM_OFA_PACK=0 keeps the two-table shape kernel
+    // packed (Q, line offset) tables, opt-in (GM_OFA_PACK=1): measured slower (C5 1.126 vs
+    // 0.938 s; the per-row staging of the 16-byte entries outweighs the one saved LDS)
     static const char* opack = std::getenv("GM_OFA_PACK");
-    if (jit && jit->packed && !(opack && opack[0] == '0') && b.tab == TAB_Q && !std::getenv("GM_OFA_U") &&
+    if (jit && jit->packed && (opack && opack[0] == '1') && b.tab == TAB_Q && !std::getenv("GM_OFA_U") &&
         !(std::getenv("GM_OFA_PK") && std::getenv("GM_OFA_PK")[0] == '1')) {
         const int groups = kThreads / D.tpr;
         const size_t per_row = (static_cast<size_t>(D.sumW + 1) + D.P_size + 2 * static_cast<size_t>(D.n_lines)) * 8;
@@ -1467,9 +1468,12 @@ void expect_matrix(const GmDev& D, long long row0, long long r_lo, long long r_h
     // registers (21.3 ms), V staged per chunk of states in shared memory (23.2 ms);
     // contiguous rows per CTA (GM_CONTIG=1): equal.
     const size_t et_smem = (kThreads / 32) * sizeof(double) + static_cast<size_t>(D.R) * sizeof(int);
-    // short rows: warp-staged cp.async chunks (k_expect_matrix_small); GM_MATRIX_SMALL=0 off
+    // one-thread rows (TPR 1, R < 32): warp-staged cp.async chunks (k_expect_matrix_small;
+    // C2a sweep 1.0 -> 0.9 ms). GM_MATRIX_SMALL=0 off, =1 also for TPR 2 / 4 (C3n: 0.35
+    // vs 0.31 ms, slower)
     static const char* msm = std::getenv("GM_MATRIX_SMALL");
-    if (!(force && std::string(force) == "walk") && !(msm && msm[0] == '0') && D.tpr <= 4) {
+    const int small_max_tpr = msm ? (msm[0] == '0' ? 0 : 4) : 1;
+    if (!(force && std::string(force) == "walk") && D.tpr <= small_max_tpr) {
         // rows per warp chunk: 32 / TPR, halved until the double buffers fit 56 KB per CTA
         int rpc = 32 / static_cast<int>(D.tpr);
         auto bytes = [&](int r) {

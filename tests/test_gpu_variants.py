@@ -70,7 +70,9 @@ SETTINGS = [
     {"GM_OFA_PK": "1", "GM_OFA_TABLE": "prefix"},
     {"GM_OFA_CACHE": "0"},  # OFA row prologue re-run every step instead of cached across the sweep
     {"GM_STEP_FUSED": "1"},  # small states: both passes in one kernel (k_step_small) instead of two
-    {"GM_MATRIX_SMALL": "0"},  # short rows through k_expect_matrix_et instead of the warp-staged kernel
+    {"GM_MATRIX_SMALL": "0"},  # one-thread rows through k_expect_matrix_et instead of the warp-staged kernel
+    {"GM_MATRIX_SMALL": "1"},  # the warp-staged kernel also for TPR 2 / 4
+    {"GM_OFA_PACK": "1", "GM_JIT": "1"},  # OFA consumer with packed (Q, line offset) tables
     {"GM_JIT_SHAPE": "0", "GM_JIT": "1"},  # run-time compiled build without the row-shape specialisation
 ]
 
