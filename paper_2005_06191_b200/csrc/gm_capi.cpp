@@ -332,7 +332,7 @@ static const gmk::OfaJit* ofa_jit(gm_model* m, int64_t rows, gmk::OfaJit& out) {
     if (m->M.noise.family == GM_CUSTOM) return nullptr;
     std::string why;
     double cs = 0.0;
-    out.shape = gmj::ofa_kernel(gmj::ofa_shape_defines(m->D), &cs, &why, &out.packed);
+    out.shape = gmj::ofa_kernel(gmj::ofa_shape_defines(m->D), &cs, &why, &out.packed, &out.group);
     return out.shape ? &out : nullptr;
 }
 

@@ -22,6 +22,7 @@ struct Kernels {
     const void* prologue = nullptr;              // k_prologue
     const void* ofa = nullptr;                   // k_expect_ofa_shape (kind 3)
     const void* ofa_packed = nullptr;            // k_expect_ofa_packed (kind 3)
+    const void* ofa_group = nullptr;             // k_expect_ofa_group (kind 3)
     double compile_s = 0.0;
 };
 
@@ -42,7 +43,7 @@ const Kernels* kernels_for(const gmh::Program& P, int n, int m, int p, int want,
 // process and on disk), nullptr with the reason in *why.
 std::string ofa_shape_defines(const GmDev& D);
 const void* ofa_kernel(const std::string& shape, double* compile_s, std::string* why,
-                       const void** packed = nullptr);
+                       const void** packed = nullptr, const void** group = nullptr);
 
 // #defines that specialise the per-warp-Q build kernel (k_build_ws<true>) to one row
 // shape (gm_rowdev.cuh GM_FILL_*), or "" when the shape does not qualify.

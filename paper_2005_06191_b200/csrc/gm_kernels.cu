@@ -1420,6 +1420,31 @@ void expect_ofa(const GmDev& D, long long nrows, const double* mass, const long 
             return;
         }
     }
+    // per-group rows (k_expect_ofa_group: no CTA-wide batch barriers), tpr >= 32;
+    // GM_OFA_GROUP=0 keeps the batched shape kernel
+    static const char* ogrp = std::getenv("GM_OFA_GROUP");
+    if (jit && jit->group && !(ogrp && ogrp[0] == '0') && D.tpr >= 32 && b.tab == TAB_Q && b.table_in_smem == 1 &&
+        !std::getenv("GM_OFA_U") && !(std::getenv("GM_OFA_PK") && std::getenv("GM_OFA_PK")[0] == '1')) {
+        const int groups = kThreads / D.tpr;
+        const size_t mw = static_cast<size_t>(D.sumW + 1);
+        // Layout(D, groups, TAB_Q): masses, P, Q per slot, partials, then the line table (ints)
+        const size_t offR = static_cast<size_t>(groups) * (mw + D.P_size + D.n_lines);
+        const size_t smem = (2 * (offR + kThreads / 32) + static_cast<size_t>(D.n_lines)) * sizeof(int);
+        note_variant(KF_EXPECT_OFA, "k_expect_ofa_group<NVRTC>");
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(jit->group, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        const long long slots = (nrows + groups - 1) / groups;
+        const int grid = resident_grid(jit->group, smem, slots);
+        GmDev Dv = D;
+        long long nr = nrows;
+        int rbi = groups;
+        GmFastDiv dv = gm_fastdiv(static_cast<uint32_t>(groups));
+        void* args[] = {&Dv, &nr, &rbi, &dv, &mass, &origin, &t0x, &rowflag, &V, &v_in};
+        const cudaError_t e = cudaLaunchKernel(jit->group, dim3(grid), dim3(kThreads), args, smem, s);
+        if (e != cudaSuccess) throw std::runtime_error(std::string("expect_ofa: ") + cudaGetErrorString(e));
+        check_launch("expect_ofa");
+        return;
+    }
     const void* jit_shape = jit ? jit->shape : nullptr;
     // the consumer compiled for this row shape (gm_ofa.cuh k_expect_ofa_shape: same
     // terms, same order) replaces k_expect_ofa<Q,1,U> unless a tuning knob asks for

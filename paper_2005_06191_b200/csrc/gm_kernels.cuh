@@ -71,6 +71,7 @@ void build(const GmDev& D, long long row0, long long nrows, long long* origin_ou
 struct OfaJit {
     const void* shape = nullptr;  // k_expect_ofa_shape
     const void* packed = nullptr; // k_expect_ofa_packed
+    const void* group = nullptr;  // k_expect_ofa_group
 };
 void expect_ofa(const GmDev& D, long long nrows, const double* mass, const long long* origin,
                 const double* t0x, const uint8_t* rowflag, const double* V, double* v_in,

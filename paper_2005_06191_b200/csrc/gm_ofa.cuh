@@ -625,4 +625,91 @@ extern "C" __global__ void __launch_bounds__(kThreads) k_expect_ofa_packed(GmDev
         }
     }
 }
+
+// The shape kernel with each lane group owning one row slot and walking its own rows:
+// masses, prefix products and line prefixes of a row are staged by the group's tpr
+// threads under the group's named barrier, so the groups of a CTA never wait for
+// each other (the CTA-wide batch barriers of k_expect_ofa_shape are the kernel's
+// largest stall after the gathers). Same tables, same terms, same bits.
+extern "C" __global__ void __launch_bounds__(kThreads) k_expect_ofa_group(GmDev D, long long nrows, int rb,
+                                                                        GmFastDiv div_rb,
+                                                                        const double* __restrict__ mass,
+                                                                        const long long* __restrict__ origin,
+                                                                        const double* __restrict__ t0x,
+                                                                        const uint8_t* __restrict__ rowflag,
+                                                                        const double* __restrict__ V,
+                                                                        double* __restrict__ v_in) {
+    constexpr int groups = kThreads / kOfaTpr;
+    const Layout Y(D, groups, TAB_Q); // one row slot per group
+    GM_CHECK(D.tpr == kOfaTpr && D.Wl == kOfaWl && D.R == kOfaR && D.n_lines == kOfaNl);
+    GM_CHECK(static_cast<unsigned>(4 * (Y.offL + kOfaNl)) <= gm_dyn_smem_bytes());
+    int* si = reinterpret_cast<int*>(g_sm);
+    for (int c = threadIdx.x; c < kOfaNl; c += blockDim.x) si[Y.offL + c] = D.line_off[c];
+    __syncthreads();
+    const int g = threadIdx.x / kOfaTpr, lane = threadIdx.x - g * kOfaTpr;
+    const int bar = 1 + g; // the group's named barrier (group_reduce uses the same one)
+    const unsigned sm0 = static_cast<unsigned>(__cvta_generic_to_shared(g_sm));
+    int Ls[kOfaPer], ks[kOfaPer];
+    unsigned la[kOfaPer];
+#pragma unroll
+    for (int S = 0; S < kOfaPer; ++S) {
+        const int t = lane + kOfaTpr * S;
+        Ls[S] = t / kOfaWl;
+        ks[S] = t - Ls[S] * kOfaWl;
+        la[S] = sm0 + 4u * static_cast<unsigned>(Y.offL + Ls[S]);
+    }
+    const bool reach = D.spec_kind != GM_SPEC_SAFETY;
+    const int mw = Y.mw;
+    double* m = g_sm + g * mw;
+    double* P = g_sm + Y.offP + g * D.P_size;
+    double* Q = g_sm + Y.offQ + g * kOfaNl;
+    for (long long row = static_cast<long long>(blockIdx.x) * groups + g; row < nrows;
+         row += static_cast<long long>(gridDim.x) * groups) {
+        const uint8_t fl = rowflag[row];
+        const bool live = !(fl & (RF_ABSORBED | RF_ERROR));
+        double s = 0.0;
+        if (live) {
+            named_sync(bar, kOfaTpr); // the slot's previous row is done
+            for (int q = lane; q < mw; q += kOfaTpr) m[q] = q < D.sumW ? mass[static_cast<long long>(q) * nrows + row] : 1.0;
+            named_sync(bar, kOfaTpr);
+            // prefix products (stage_tables' association): per run of the last prefix axis
+            if (D.s_axes == 0) {
+                if (lane == 0) P[0] = 1.0;
+            } else {
+                const int last = D.s_axes - 1, wl = D.W[last], nb = D.P_size / wl;
+                for (int b = lane; b < nb; b += kOfaTpr) {
+                    double acc = 1.0;
+                    int rem = b * wl;
+                    for (int d = 0; d < last; ++d) {
+                        const int j = D.div_Ps[d].div(rem);
+                        rem -= j * D.Ps[d];
+                        acc *= m[D.mass_off[d] + j];
+                    }
+                    const double* ml = m + D.mass_off[last];
+                    for (int j = 0; j < wl; ++j) P[b * wl + j] = acc * ml[j];
+                }
+            }
+            named_sync(bar, kOfaTpr);
+            for (int L = lane; L < kOfaNl; L += kOfaTpr) {
+                const int a = D.div_Wm.div(L), j = L - a * D.Wm;
+                Q[L] = P[a] * m[D.mm_off + j];
+            }
+            named_sync(bar, kOfaTpr);
+            GM_CHECK_SLAB(D, origin[row]);
+            const double* vrow = V + origin[row];
+            unsigned qa[kOfaPer];
+            double ml[kOfaPer];
+            const double* vb[kOfaPer];
+#pragma unroll
+            for (int S = 0; S < kOfaPer; ++S) {
+                qa[S] = sm0 + 8u * static_cast<unsigned>(Y.offQ + g * kOfaNl + Ls[S]);
+                ml[S] = m[D.ml_off + ks[S]];
+                vb[S] = vrow + ks[S];
+            }
+            s = OfaDot<0>::run(0.0, qa, la, ml, vb, lane);
+        }
+        s = group_reduce(s, kOfaTpr, Y.offR, g * kOfaTpr);
+        if (lane == 0) v_in[row] = live ? (reach ? s + t0x[row] : s) : 0.0;
+    }
+}
 #endif
