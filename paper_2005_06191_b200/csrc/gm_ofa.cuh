@@ -335,8 +335,10 @@ __device__ __forceinline__ void expect_ofa_body(GmDev D, long long nrows, int rb
     }
 }
 
-// separate entry points: the pipelined hoisted-cell body needs the 3-CTA register
-// cap (80), the plain body keeps the compiler's own choice (48 registers)
+// separate entry points: the pipelined hoisted-cell body gets a 2-CTA register cap
+// (128: no spills; the 3-CTA cap of 80 spilled 36-240 B and measured 3-7% slower
+// on C4 / C4' / bmw7_mid, scripts/r02_pk_minb.sh), the plain body keeps the
+// compiler's own choice (48 registers)
 template <int TAB, int LS, int U = 4>
 __global__ void __launch_bounds__(kThreads) k_expect_ofa(GmDev D, long long nrows, int rb, GmFastDiv div_rb,
                                                         const double* __restrict__ mass,
@@ -347,8 +349,11 @@ __global__ void __launch_bounds__(kThreads) k_expect_ofa(GmDev D, long long nrow
                                                         double* __restrict__ v_in) {
     expect_ofa_body<TAB, LS, U, false>(D, nrows, rb, div_rb, mass, origin, t0x, rowflag, V, v_in);
 }
+#ifndef GM_OFA_PK_MINB
+#define GM_OFA_PK_MINB 2
+#endif
 template <int TAB, int LS, int U>
-__global__ void __launch_bounds__(kThreads, 3) k_expect_ofa_pk(GmDev D, long long nrows, int rb, GmFastDiv div_rb,
+__global__ void __launch_bounds__(kThreads, GM_OFA_PK_MINB) k_expect_ofa_pk(GmDev D, long long nrows, int rb, GmFastDiv div_rb,
                                                               const double* __restrict__ mass,
                                                               const long long* __restrict__ origin,
                                                               const double* __restrict__ t0x,

@@ -82,6 +82,29 @@ def test_traffic_ofa_step_matches_oracle_on_sampled_states(wl, x0):
     assert ok, n
 
 
+@pytest.mark.parametrize("wl,x0", [("C4", 1207000), ("C4p", 4303000)])
+def test_traffic_ofa_synthesis_chains_steps(wl, x0):
+    """The full-size traffic rings through gm_synthesize for two steps (the OFA
+    sweep with its row prologue cached across steps): each step's values on a
+    sampled state range equal the oracle's Bellman step of the engine's own next-step
+    values, and the policies agree except on ties (under the oracle's per-input
+    values)."""
+    text = W.WORKLOADS[wl]()
+    m = g.parse_config(text, wl, time_steps=2)
+    om = O.load(text)
+    res = g.synthesize(m, m.spec, g.SynthesisOptions(mode="ofa"))
+    variant = _capi.lib.gm_last_kernel_variant(_capi.KF_EXPECT_OFA).decode()
+    print(wl, variant)
+    assert res.values.shape == (m.n_states, 3)
+    x1 = x0 + 96
+    for k in (1, 0):
+        vo, po, _, vin = om.bellman_step(res.values[:, k + 1], x0, x1)
+        assert G.tol_ok(res.values[x0:x1, k], vo).all(), (k, np.abs(res.values[x0:x1, k] - vo).max())
+        ok, n = G.policy_ok(vin.min(axis=2), res.policy[x0:x1, k], po)
+        assert ok, (k, n)
+    assert np.isfinite(res.values).all() and (res.values >= 0).all() and (res.values <= 1 + 1e-9).all()
+
+
 @pytest.mark.parametrize("case", ["ref_vehicle3_desk", "ref_bmw7_desk", "fixture2d_ra"])
 @pytest.mark.parametrize("matrix", [False, True])
 def test_sharding_is_bit_identical(case, matrix):

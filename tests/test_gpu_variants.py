@@ -55,6 +55,22 @@ h.update(np.ascontiguousarray(r.values).tobytes()); h.update(np.ascontiguousarra
 r = g.synthesize(m, m.spec, g.SynthesisOptions(mode="ofa"))
 h.update(np.ascontiguousarray(r.values).tobytes())
 print("vehicle_r729", h.hexdigest(), ofa())
+# R = 15,750 (tpr 128, the prefix-table OFA kernels): the north-star BMW 320i
+# model on a 4 x 4 position grid, two steps
+m = g.load_config(str(G.large_cfg("bmw7_mid")), time_steps=2)
+r = g.synthesize(m, m.spec, g.SynthesisOptions(mode="ofa"))
+h = hashlib.sha256()
+h.update(np.ascontiguousarray(r.values).tobytes()); h.update(np.ascontiguousarray(r.policy).tobytes())
+h.update(np.ascontiguousarray(r.worst_dist).tobytes())
+print("bmw7_mid_T2", h.hexdigest(), ofa())
+# R = 7,000 with the line-prefix table (the north-star C5 at full size, one step):
+# the per-group / batched NVRTC consumers under GM_JIT=1
+m = g.load_config(str(G.large_cfg("C5")), time_steps=1)
+r = g.synthesize(m, m.spec, g.SynthesisOptions(mode="ofa"))
+h = hashlib.sha256()
+h.update(np.ascontiguousarray(r.values).tobytes()); h.update(np.ascontiguousarray(r.policy).tobytes())
+h.update(np.ascontiguousarray(r.worst_dist).tobytes())
+print("C5_T1", h.hexdigest(), ofa())
 """
 
 SETTINGS = [
@@ -92,8 +108,9 @@ def _digest(rows):
 
 # the hoisted last-axis cell needs an unroll U in [4, 8] that is a multiple of the
 # lane's cell period (launch_ofa): fixture2d_ra and ref_vehicle3_desk have one;
-# exp_dist (period 13) and vehicle_r729 (period 9) keep the plain kernel
-PK_CASES = {"fixture2d_ra", "ref_vehicle3_desk"}
+# exp_dist (period 13) and vehicle_r729 (period 9) keep the plain kernel; the wide
+# rows (bmw7_mid_T2: the default there, C5_T1) have one too
+PK_CASES = {"fixture2d_ra", "ref_vehicle3_desk", "bmw7_mid_T2", "C5_T1"}
 
 
 @pytest.fixture(scope="module")
@@ -111,6 +128,9 @@ def test_variant_bit_identical_to_default(default, knob):
             assert v.startswith("k_expect_ofa_pk<") == (c in PK_CASES), (c, v)
     if "GM_OFA_TABLE" in knob:
         assert all(",P," in v or "<P," in v for _, v in got.values()), got
+    if knob.get("GM_JIT") == "1" and "GM_OFA_PACK" not in knob:  # the wide-row NVRTC consumer really ran
+        want = "k_expect_ofa_shape<NVRTC>" if knob.get("GM_OFA_GROUP") == "0" else "k_expect_ofa_group<NVRTC>"
+        assert got["C5_T1"][1] == want, got["C5_T1"]
 
 
 def test_row_pitch_does_not_change_results(default):
