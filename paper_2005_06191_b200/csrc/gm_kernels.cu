@@ -370,7 +370,7 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-template <int TPR>
+template <int TPR, int U>
 __global__ void __launch_bounds__(kThreads) k_expect_matrix_small(GmDev D, long long row0, long long r_lo,
                                                                  long long r_hi, int rpc, int chunk_len,
                                                                  const double* __restrict__ probs,
@@ -424,8 +424,8 @@ __global__ void __launch_bounds__(kThreads) k_expect_matrix_small(GmDev D, long 
             GM_CHECK_SLAB(D, origins[r]);
             const double* pr = buf + b * chunk_len + j * pitch;
             const double* vb = V + origins[r];
-            // 8 gathers in flight per lane, then their fmas in increasing t
-            constexpr int U = 8;
+            // U gathers in flight per lane, then their fmas in increasing t; the last
+            // block is predicated (absent terms add fma(0, 0, s) == s)
             int t = q;
             for (; t + (U - 1) * TPR < R; t += U * TPR) {
                 double v[U];
@@ -434,7 +434,17 @@ __global__ void __launch_bounds__(kThreads) k_expect_matrix_small(GmDev D, long 
 #pragma unroll
                 for (int u = 0; u < U; ++u) s = fma(pr[t + u * TPR], v[u], s);
             }
-            for (; t < R; t += TPR) s = fma(pr[t], ldg_at(vb, E[t]), s);
+            if (t < R) {
+                double v[U], p[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const bool in = t + u * TPR < R;
+                    v[u] = in ? ldg_at(vb, E[t + u * TPR]) : 0.0;
+                    p[u] = in ? pr[t + u * TPR] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) s = fma(p[u], v[u], s);
+            }
         }
         for (int off = TPR >> 1; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
         if (valid && q == 0) v_in[rl] = skip ? 0.0 : (reach ? s + t0x[r] : s);
@@ -1504,24 +1514,33 @@ void expect_matrix(const GmDev& D, long long row0, long long r_lo, long long r_h
         auto bytes = [&](int r) {
             return static_cast<size_t>((D.R + 1) / 2 + (kThreads / 32) * 2 * r * D.pitch) * sizeof(double);
         };
-        while (rpc > 1 && bytes(rpc) > kSoftSmem) rpc /= 2;
+        // per-CTA budget 112 KB (whole 32-row chunks: every lane has a row) and all of a
+        // lane's gathers in flight at once: C2a sweep 0.95 -> 0.87 ms on one box
+        // (scripts/r02_small_u.sh; 56 KB / 8 in flight before). GM_SMALL_SMEM_KB,
+        // GM_SMALL_U (8, 16, 32): tuning
+        static const char* skb = std::getenv("GM_SMALL_SMEM_KB");
+        const size_t budget = skb ? static_cast<size_t>(std::atoi(skb)) * 1024 : 2 * kSoftSmem;
+        static const char* su = std::getenv("GM_SMALL_U");
+        const int U = su ? std::atoi(su) : 32;
+        while (rpc > 1 && bytes(rpc) > budget) rpc /= 2;
         const int chunk_len = static_cast<int>(rpc * D.pitch);
         const size_t smem = bytes(rpc);
-        if (smem <= kSoftSmem) {
+        if (smem <= budget) {
             const long long chunks = (r_hi - r_lo + rpc - 1) / rpc;
             const long long ctas = (chunks + kThreads / 32 - 1) / (kThreads / 32);
-            note_variant(KF_EXPECT_MATRIX, "k_expect_matrix_small<%d>", D.tpr);
-            switch (D.tpr) {
-#define GM_MS(T)                                                                                              \
-    case T: {                                                                                                 \
-        auto k = k_expect_matrix_small<T>;                                                                    \
+            note_variant(KF_EXPECT_MATRIX, "k_expect_matrix_small<%d,%d>", D.tpr, U >= 32 ? 32 : U >= 16 ? 16 : 8);
+            switch (D.tpr * 64 + (U >= 32 ? 32 : U >= 16 ? 16 : 8)) {
+#define GM_MS(T, UU)                                                                                          \
+    case T * 64 + UU: {                                                                                       \
+        auto k = k_expect_matrix_small<T, UU>;                                                                \
         allow_smem(k, smem);                                                                                  \
         k<<<resident_grid(k, smem, ctas), kThreads, smem, s>>>(D, row0, r_lo, r_hi, rpc, chunk_len, probs, origins, \
                                                               t0x, V, v_in);                                  \
         check_launch("expect_matrix");                                                                        \
         return;                                                                                               \
     }
-                GM_MS(1) GM_MS(2) GM_MS(4)
+                GM_MS(1, 8) GM_MS(2, 8) GM_MS(4, 8) GM_MS(1, 16) GM_MS(2, 16) GM_MS(4, 16) GM_MS(1, 32)
+                GM_MS(2, 32) GM_MS(4, 32)
 #undef GM_MS
             default: break;
             }

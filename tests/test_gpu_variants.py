@@ -88,6 +88,7 @@ SETTINGS = [
     {"GM_STEP_FUSED": "1"},  # small states: both passes in one kernel (k_step_small) instead of two
     {"GM_MATRIX_SMALL": "0"},  # one-thread rows through k_expect_matrix_et instead of the warp-staged kernel
     {"GM_MATRIX_SMALL": "1"},  # the warp-staged kernel also for TPR 2 / 4
+    {"GM_MATRIX_SMALL": "1", "GM_SMALL_U": "8", "GM_SMALL_SMEM_KB": "28"},  # 8 gathers in flight, half-empty chunks
     {"GM_OFA_PACK": "1", "GM_JIT": "1"},  # OFA consumer with packed (Q, line offset) tables
     {"GM_OFA_GROUP": "0", "GM_JIT": "1"},  # batched shape OFA consumer instead of the per-group one
     {"GM_JIT_SHAPE": "0", "GM_JIT": "1"},  # run-time compiled build without the row-shape specialisation
