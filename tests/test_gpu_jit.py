@@ -79,7 +79,7 @@ def test_jit_auto_policy_small_launch_uses_interpreter(monkeypatch):
     m = model("tiny")
     g.build_matrix(m)
     used, _, why = jit_status(m)
-    assert used == 0 and "2^21" in why
+    assert used == 0 and "2^21 rows and 2^32 row entries" in why
 
 
 _PROBE = r"""
