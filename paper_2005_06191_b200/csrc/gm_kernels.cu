@@ -1362,8 +1362,8 @@ static void launch_ofa(const GmDev& D, const BatchPlan& b, long long nrows, cons
                        double* v_in, cudaStream_t s) {
     const long long batches = (nrows + b.rb - 1) / b.rb;
     static const char* ou = std::getenv("GM_OFA_U"); // terms in flight per lane (tuning)
-    // hoisted last-axis cell (row_dot_pk, software-pipelined, 3 CTAs/SM register
-    // cap): C4 14.7 -> 12.3 s, C4' 12.0 -> 10.7 s. GM_OFA_PK=1 / 0 forces it on / off.
+    // hoisted last-axis cell (row_dot_pk, software-pipelined, 2 CTAs/SM register
+    // cap): C4 14.7 -> 12.0 s, C4' 12.0 -> 9.6 s. GM_OFA_PK=1 / 0 forces it on / off.
     static const char* opk = std::getenv("GM_OFA_PK");
     const int u = ou ? std::atoi(ou) : 6; // C5: U = 4 1.23 s, 6 1.14 s, 8 1.14 s
     auto k = u == 8 ? k_expect_ofa<TAB, LS, 8> : (u == 6 ? k_expect_ofa<TAB, LS, 6> : k_expect_ofa<TAB, LS, 4>);
