@@ -106,7 +106,15 @@ def main():
     ap.add_argument("--only", default="")
     ap.add_argument("--out", default=None)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-from", default=None,
+                    help="reuse the CPU columns of an earlier configs.md (its JSON records) instead of re-running them")
     a = ap.parse_args()
+    prior = {}
+    if a.cpu_from:
+        for ln in Path(a.cpu_from).read_text().splitlines():
+            if ln.startswith("{"):
+                r = json.loads(ln)
+                prior[r["workload"]] = {k: v for k, v in r.items() if k.startswith("cpu_")}
     import torch
 
     from paper_2005_06191_b200 import workloads as W
@@ -135,7 +143,10 @@ def main():
                "fp64_util": 2 * tps * live / (f64 * 1e12), "kernel_ms": fam}
         if mode == "matrix" and build_s > 0:
             rec["build_probs_per_s"] = rows_n * R / build_s
-        if not a.no_cpu and REF_BIN.exists():
+        if name in prior and "cpu_s" in prior[name]:
+            rec.update(prior[name])
+            rec["speedup"] = rec["cpu_s"] / rec["gpu_total_s"]
+        elif not a.no_cpu and REF_BIN.exists():
             th = os.cpu_count() or 1
             if name in FULL_CPU:
                 cmode = mode
@@ -175,7 +186,9 @@ def main():
             "Bellman steps; OFA has no build). G terms/s = rows·R·T / sweep; HBM-equiv = 8 B per term of the "
             "rows the sweep reads (absorbed states' rows excluded) against HBM (the bytes matrix mode streams); "
             "FP64 util = 2 flops per such term against the DFMA peak. "
-            "CPU: the reference compiled from its sources (oracle/_ref), all host threads.\n\n" + table
+            "CPU: the reference compiled from its sources (oracle/_ref), all host threads"
+            + (f" (CPU columns from {a.cpu_from}, an earlier run on the same pool)" if a.cpu_from else "")
+            + ".\n\n" + table
             + "\n```\n" + "\n".join(json.dumps(r) for r in recs) + "\n```\n")
 
 
