@@ -43,7 +43,7 @@ def test_reference_front_end_untouched():
     assert f"rows: {MAN['cases']['fixture2d_ra']['sizes']['rows']}\n" in r.stdout
 
 
-CASES = ["fixture2d_ra", "ref_vehicle3_desk", "room5_uni", "exp_dist", "beta1d", "mult1d", "chain09"]
+CASES = ["fixture2d_ra", "ref_vehicle3_desk", "ref_bmw7_desk", "room5_uni", "exp_dist", "beta1d", "mult1d", "chain09"]
 
 
 @pytest.mark.gpu
@@ -110,3 +110,22 @@ def test_reference_synthesize_on_several_devices(case, tmp_path):
                        text=True, env=env)
     assert r.returncode == 0, r.stderr
     assert a.read_bytes() == b.read_bytes()
+
+
+@pytest.mark.gpu
+def test_reference_synthesize_on_engine_bmw_full_horizon(tmp_path):
+    """The north-star dynamics through the reference's in-memory types (every BMW
+    expression crosses as its Expr node pool, gm_model_desc): bmw7_mid (1.75 M rows x
+    15,750, T = 8, OFA) equals the engine CLI's container byte for byte and the
+    reference's own full-horizon result within the parity bar (nonzero values)."""
+    cfg = G.large_cfg("bmw7_mid")
+    a, b = tmp_path / "adapter.bin", tmp_path / "engine.bin"
+    r = run("synthesize", "-c", cfg, "-o", a)
+    assert r.returncode == 0, r.stderr
+    e = subprocess.run([str(_capi.CLI_PATH), "synthesize", "-c", str(cfg), "-o", str(b)], capture_output=True, text=True)
+    assert e.returncode == 0, e.stderr
+    assert a.read_bytes() == b.read_bytes()
+    got = G.read_results(a.read_bytes())
+    ref = G.large_results("bmw7_mid")
+    assert np.count_nonzero(ref["values"]) > 0
+    assert G.tol_ok(got["values"], ref["values"]).all()
