@@ -335,7 +335,10 @@ static const gmk::OfaJit* ofa_jit(gm_model* m, int64_t rows, gmk::OfaJit& out) {
     static const char* off = std::getenv("GM_OFA_SHAPE");
     if (off && off[0] == '0') return nullptr;
     const char* env = std::getenv("GM_JIT");
-    if ((env && env[0] == '0') || (!env && !jit_worth_it(m, rows))) return nullptr;
+    // a sweep runs the consumer once per step (C3b, 0.28 M rows x 7,776 x 8 steps:
+    // 21.0 -> 14.0 ms with the per-group kernel)
+    const int64_t steps = m->ofa_cache_steps ? std::max(1, m->M.spec.horizon) : 1;
+    if ((env && env[0] == '0') || (!env && !jit_worth_it(m, rows * steps))) return nullptr;
     if (m->M.noise.family == GM_CUSTOM) return nullptr;
     std::string why;
     double cs = 0.0;
