@@ -321,7 +321,8 @@ static const gmj::Kernels* jit_kernels(gm_model* m, int want, int64_t rows) {
     static const char* js = std::getenv("GM_JIT_SHAPE");
     const std::string shape =
         (want & gmj::WANT_BUILD_QS) && !(js && js[0] == '0') ? gmj::shape_defines(m->D) : std::string();
-    const gmj::Kernels* k = gmj::kernels_for(m->M.prog, m->M.X.dim(), m->M.U.dim(), m->M.W.dim(), want, &why, shape);
+    const gmj::Kernels* k = gmj::kernels_for(m->M.prog, m->M.X.dim(), m->M.U.dim(), m->M.W.dim(), want, &why, shape,
+                                             gmk::build_ctas(m->D, true));
     m->jit_used = k != nullptr;
     m->jit_why = k ? std::string() : why;
     m->jit_compile_s = k ? k->compile_s : 0.0;
@@ -1180,7 +1181,8 @@ gm_code gm_model_jit_compile(const gm_model* m, int32_t kind, double* seconds, g
                                   : kind == 2 && !(js && js[0] == '0') ? gmj::shape_defines(m->M.device_descriptor())
                                                                        : std::string();
         if (kind == 3 && shape.empty()) throw ConfigErr("the model's row shape does not qualify for the OFA kernel");
-        const std::string err = gmj::compile_only(m->M.prog, m->M.X.dim(), m->M.U.dim(), m->M.W.dim(), kind, seconds, shape);
+        const std::string err = gmj::compile_only(m->M.prog, m->M.X.dim(), m->M.U.dim(), m->M.W.dim(), kind, seconds,
+                                                  shape, gmk::build_ctas(m->D, true));
         if (!err.empty()) throw std::runtime_error(err);
     });
 }

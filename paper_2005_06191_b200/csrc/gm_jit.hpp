@@ -35,8 +35,10 @@ enum Want { WANT_PROLOGUE = 1, WANT_BUILD_NOQS = 2, WANT_BUILD_QS = 4 };
 // is its own NVRTC program, compiled on first use: ~2 s k_prologue, ~5 s
 // k_build_ws), or nullptr with the reason in *why (NVRTC missing, compile or
 // load failure, GM_JIT=0).
+// `ctas`: resident CTAs per SM the build kernel is compiled for (its register cap,
+// gmk::build_ctas).
 const Kernels* kernels_for(const gmh::Program& P, int n, int m, int p, int want, std::string* why,
-                           const std::string& shape = "");
+                           const std::string& shape = "", int ctas = 3);
 
 // #defines that specialise the OFA consumer to a row shape (gm_ofa.cuh GM_OFA_SHAPE),
 // or "" when the shape does not qualify; the compiled kernel for them (cached per
@@ -53,6 +55,6 @@ std::string shape_defines(const GmDev& D);
 // k_build_ws<true>) without loading it: "" on success, else the compiler log.
 // Needs no GPU (tests run it on the build host).
 std::string compile_only(const gmh::Program& P, int n, int m, int p, int kind, double* seconds,
-                         const std::string& shape = "");
+                         const std::string& shape = "", int ctas = 3);
 
 } // namespace gmj

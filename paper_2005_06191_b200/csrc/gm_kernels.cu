@@ -1250,6 +1250,12 @@ void origin_minmax(const long long* origins, const uint8_t* rowflag, long long n
     check_launch("origin_minmax");
 }
 
+int build_ctas(const GmDev& D, bool jit) {
+    static const char* bc = std::getenv("GM_BUILD_CTAS"); // tuning
+    if (bc) return std::max(2, std::min(6, std::atoi(bc)));
+    return jit && D.R >= 512 ? 2 : 3;
+}
+
 bool build_uses_qs(const GmDev& D) { return D.n_lines <= 512 && D.n_lines * 8 < 65536 && D.Wl * 8 < 32768; }
 
 void build(const GmDev& D, long long row0, long long nrows, long long* origin_out, double* t0x_out,
@@ -1275,8 +1281,8 @@ void build(const GmDev& D, long long row0, long long nrows, long long* origin_ou
         const size_t fixed_d = D.n_ins + D.n_lits + 3 + (qs ? (D.pitch + 1) / 2 + (kThreads / 32) * (D.n_lines + 1) : 0);
         // two table buffers + two prologue buffers (pro_doubles: <= (5n + 2) rb + 2 for both)
         const size_t per_d = 2 * (mw + D.P_size) + 5 * static_cast<size_t>(D.n) + 2;
-        static const char* bc = std::getenv("GM_BUILD_CTAS"); // resident CTAs per SM (tuning; AOT kernels)
-        const int ctas = bc ? std::max(2, std::min(6, std::atoi(bc))) : 3; // C2b: 3 beats 4 by 2-4 %, 2 is 19 % slower
+        // resident CTAs per SM (AOT kernels, interpreter: 3 beats 4 by 2-4 % on C2b, 2 is 19 % slower)
+        const int ctas = build_ctas(D, jit_ws && jit_ws[qs ? 1 : 0]);
         const size_t budget_d = (216 / ctas) * 1024 / sizeof(double);
         if (fixed_d < budget_d) {
             long long rb = std::min<long long>(64, static_cast<long long>((budget_d - fixed_d) / per_d));

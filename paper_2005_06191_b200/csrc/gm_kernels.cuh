@@ -59,6 +59,10 @@ void build_custom(const GmDev& D, long long row0, long long nrows, long long* or
                   double* probs_out, unsigned long long* d_err, cudaStream_t s);
 // Whether build() uses the per-warp line-prefix variant k_build_ws<true>.
 bool build_uses_qs(const GmDev& D);
+// Resident k_build_ws CTAs per SM (its register cap): GM_BUILD_CTAS, else 2 for the
+// run-time compiled kernel on rows of >= 512 entries (store-bound: C2b 19.35 ->
+// 18.6 ms, C5 shard 19.1 -> 18.3 ms, no spills), else 3 (C1, R = 169: 4.06 vs 4.43 ms).
+int build_ctas(const GmDev& D, bool jit);
 // min / max of the flat slab origins of rows whose flag is 0 (not absorbed, no error);
 // mm[0] (init LLONG_MAX) and mm[1] (init -1) accumulate across calls
 void origin_minmax(const long long* origins, const uint8_t* rowflag, long long n, long long* mm, cudaStream_t s);

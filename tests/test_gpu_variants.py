@@ -79,6 +79,7 @@ SETTINGS = [
     {"GM_ET_VARIANT": "2", "GM_OFA_U": "4", "GM_CONTIG": "1"},
     {"GM_ET_VARIANT": "5"},  # one row per warp at TPR = 32 (default: two)
     {"GM_BUILD_CTAS": "5", "GM_OFA_U": "8"},
+    {"GM_BUILD_CTAS": "2", "GM_JIT": "1"},  # run-time compiled build at the 2-CTA register cap
     {"GM_JIT": "1"},
     {"GM_OFA_TABLE": "prefix"},  # OFA from the leading-prefix table + prefix offset table
     {"GM_OFA_TABLE": "global", "GM_OFA_U": "4"},  # same table, line offsets from global memory
