@@ -717,6 +717,13 @@ void step_states(gm_model* m, gm_matrix* tm, int64_t x0, int64_t x1, const doubl
         check_matrix_model(tm, m);
         if (m->M.spec.reach() && !tm->has_t0x)
             throw ConfigErr("bellman step: a reach specification needs the matrix's target-hit vector");
+        if (tm->row_begin <= r0 && tm->row_end >= r1 && n > 0 && gmk::step_warp_applies(m->D)) {
+            Launch L(gmk::KF_EXPECT_MATRIX, s);
+            const int64_t rb = r0 - tm->row_begin;
+            if (gmk::step_warp(m->D, x0, x1 - x0, tm->probs.p + rb * m->D.pitch, tm->origins.p + rb,
+                               tm->has_t0x ? tm->t0x.p + rb : nullptr, v_next, m->d_vin.p, v_out, pol, wst, s))
+                return; // both passes done, one warp per state
+        }
         if (tm->row_begin <= r0 && tm->row_end >= r1 && n > 0 && gmk::step_small_applies(m->D)) {
             Launch L(gmk::KF_EXPECT_MATRIX, s);
             if (gmk::step_small(m->D, x0, x1 - x0, tm->probs.p, r0 - tm->row_begin, tm->origins.p,

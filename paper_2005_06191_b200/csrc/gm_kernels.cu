@@ -638,6 +638,150 @@ __global__ void __launch_bounds__(kThreads) k_step_small(GmDev D, long long x0, 
     }
 }
 
+// Stage (ii), stored matrix, the whole step for small states with one warp per
+// state (both passes; C2a: 25 rows of 27 entries per state). The warp copies its
+// state's rows (contiguous in the matrix) into its shared-memory slot with
+// coalesced 8-byte cp.async copies, re-pitched to `ps` (conflict-free row reads);
+// row groups of TPR lanes reduce the rows exactly as k_expect_matrix_et (lane-
+// strided fma in increasing t, the TPR-lane butterfly) into the slot's row values;
+// the copy of the warp's next state is issued, and the warp runs pass 2 over the
+// row values as k_maxmin<32> (strict < over w, strict > over u, lowest-index ties,
+// clamp). The same bits as expect_matrix + maxmin, one launch per step, no v_in
+// round trip (v_in is still written: the step's row values stay readable), and
+// no CTA-wide barrier after the offset table.
+template <int TPR, int U>
+__global__ void __launch_bounds__(kThreads) k_step_warp(GmDev D, long long x0, long long nx, int ps, int wslot,
+                                                      const double* __restrict__ probs,
+                                                      const long long* __restrict__ origins,
+                                                      const double* __restrict__ t0x,
+                                                      const double* __restrict__ V, double* __restrict__ v_in,
+                                                      double* __restrict__ v_out, uint32_t* __restrict__ pol,
+                                                      uint32_t* __restrict__ wst) {
+    constexpr int RPP = 32 / TPR; // rows per pass of the warp
+    const int R = static_cast<int>(D.R), P = static_cast<int>(D.pitch);
+    const int nu = static_cast<int>(D.n_u), nw = static_cast<int>(D.n_w), nuw = nu * nw;
+    int* E = reinterpret_cast<int*>(g_sm);
+    const int offW = (R + 1) / 2; // doubles after E
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* stage = g_sm + offW + static_cast<long long>(warp) * wslot;
+    double* vrow = stage + nuw * ps;
+    long long* sorg = reinterpret_cast<long long*>(vrow + nuw); // the state's row origins, copied with its rows
+    GM_CHECK(static_cast<unsigned>(8 * (offW + (kThreads / 32) * wslot)) <= gm_dyn_smem_bytes());
+    GM_CHECK(wslot >= nuw * (ps + 2) && ps >= R);
+    for (int t = threadIdx.x; t < R; t += kThreads) {
+        const int Ln = D.div_Wl.div(t);
+        E[t] = D.line_off[Ln] + (t - Ln * D.Wl);
+        GM_CHECK(E[t] >= 0 && E[t] <= slab_span(D));
+    }
+    __syncthreads();
+    const bool reach = D.spec_kind != GM_SPEC_SAFETY;
+    const bool has_abs = reach && D.absorb != nullptr;
+    // the state's rows are one contiguous block: flat copies, (row, column) of the
+    // lane's element advanced incrementally
+    const int row0 = lane / P, col0 = lane - row0 * P, qs = 32 / P, rs = 32 - qs * P;
+    const int nel = nuw * P;
+    auto issue = [&](long long x, bool abs_x) {
+        if (x < nx && !abs_x) {
+            for (int j = lane; j < nuw; j += 32)
+                cp_async8(reinterpret_cast<double*>(sorg + j), reinterpret_cast<const double*>(origins + x * nuw + j));
+            const double* src = probs + x * nuw * static_cast<long long>(P);
+            int row = row0, col = col0;
+            for (int e = lane; e < nel; e += 32) {
+                if (col < R) cp_async8(stage + row * ps + col, src + e);
+                row += qs;
+                col += rs;
+                if (col >= P) {
+                    col -= P;
+                    ++row;
+                }
+            }
+        }
+        cp_async_commit();
+    };
+    const long long wstride = static_cast<long long>(gridDim.x) * (kThreads / 32);
+    long long x = static_cast<long long>(blockIdx.x) * (kThreads / 32) + warp;
+    auto absorbed_at = [&](long long xx) { return xx < nx && has_abs && D.absorb[x0 + xx] != 0; };
+    bool absorbed = absorbed_at(x);
+    issue(x, absorbed);
+    const int j0 = lane / TPR, q = lane - j0 * TPR;
+    for (; x < nx; x += wstride) {
+        const bool abs_next = absorbed_at(x + wstride); // loaded early: the next issue needs it
+        cp_async_wait<0>();
+        __syncwarp();
+        if (!absorbed) {
+            for (int j = j0; j - j0 < nuw; j += RPP) { // pass 1: RPP rows at a time (warp-uniform trip count)
+                const bool valid = j < nuw;
+                const long long r = x * nuw + (valid ? j : 0); // local row
+                double s = 0.0;
+                if (valid) {
+                    GM_CHECK_SLAB(D, sorg[j]);
+                    const double* pr = stage + j * ps;
+                    const double* vb = V + sorg[j];
+                    int t = q;
+                    for (; t + (U - 1) * TPR < R; t += U * TPR) {
+                        double v[U];
+#pragma unroll
+                        for (int u = 0; u < U; ++u) v[u] = ldg_at(vb, E[t + u * TPR]);
+#pragma unroll
+                        for (int u = 0; u < U; ++u) s = fma(pr[t + u * TPR], v[u], s);
+                    }
+                    for (; t < R; t += TPR) s = fma(pr[t], ldg_at(vb, E[t]), s);
+                }
+                for (int off = TPR >> 1; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+                if (valid && q == 0) {
+                    const double vr = reach ? s + t0x[r] : s;
+                    vrow[j] = vr;
+                    v_in[r] = vr;
+                }
+            }
+        } else {
+            for (int j = lane; j < nuw; j += 32) v_in[x * nuw + j] = 0.0;
+        }
+        __syncwarp();                 // row values written, the stage read
+        issue(x + wstride, abs_next); // the next state's rows land during pass 2
+        // pass 2 (synthesis.cpp:112-142), as k_maxmin<32>
+        double best = -INFINITY;
+        uint32_t bu = 0, bw = 0;
+        if (!absorbed) {
+            for (int iu = lane; iu < nu; iu += 32) {
+                double mn = INFINITY;
+                uint32_t mw = 0;
+                const double* qv = vrow + iu * nw;
+                for (int iw = 0; iw < nw; ++iw) {
+                    const double v = qv[iw];
+                    if (v < mn) {
+                        mn = v;
+                        mw = static_cast<uint32_t>(iw);
+                    }
+                }
+                if (mn > best) {
+                    best = mn;
+                    bu = static_cast<uint32_t>(iu);
+                    bw = mw;
+                }
+            }
+        }
+        for (int off = 16; off >= 1; off >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+            const uint32_t ou = __shfl_xor_sync(0xffffffffu, bu, off);
+            const uint32_t ow = __shfl_xor_sync(0xffffffffu, bw, off);
+            if (ob > best || (ob == best && ou < bu)) {
+                best = ob;
+                bu = ou;
+                bw = ow;
+            }
+        }
+        if (lane == 0) {
+            v_out[x] = absorbed ? 0.0 : smin(1.0, smax(0.0, best));
+            if (pol) pol[x] = absorbed ? 0u : bu;
+            if (wst) wst[x] = absorbed ? 0u : bw;
+        }
+        __syncwarp(); // vrow is rewritten by the next state's pass 1
+        absorbed = abs_next;
+    }
+    cp_async_wait<0>();
+}
+
 // min over w (strict <, ascending), then max over u (strict >, ascending):
 // lowest-index ties (synthesis.cpp:112-142). L lanes per state.
 template <int L>
@@ -1700,6 +1844,61 @@ bool step_small(const GmDev& D, long long x0, long long nx, const double* probs,
     default: return false;
     }
     check_launch("step_small");
+    return true;
+}
+
+// k_step_warp geometry: the row re-pitch and the per-warp shared-memory slot in
+// doubles (0: not applicable). GM_STEP_WARP=0 keeps expect_matrix + maxmin.
+static void step_warp_plan(const GmDev& D, int& ps, int& wslot) {
+    ps = wslot = 0;
+    static const char* on = std::getenv("GM_STEP_WARP");
+    if (on && on[0] == '0') return;
+    const long long nuw = D.n_u * D.n_w;
+    if (D.tpr > 4 || nuw > 512 || D.pitch > 64) return;
+    int p = static_cast<int>(D.tpr); // a multiple of TPR with an odd quotient: conflict-free row reads
+    while (p < D.R || (p / D.tpr) % 2 == 0) p += static_cast<int>(D.tpr);
+    const long long slot = nuw * (p + 2); // rows, row values, origins
+    if (slot * 8 > 24 * 1024) return; // at least 8 warps of slots per SM
+    ps = p;
+    wslot = static_cast<int>(slot + (slot & 1)); // 16-byte aligned slots
+}
+
+bool step_warp_applies(const GmDev& D) {
+    int ps, ws;
+    step_warp_plan(D, ps, ws);
+    return ws > 0;
+}
+
+bool step_warp(const GmDev& D, long long x0, long long nx, const double* probs, const long long* origins,
+               const double* t0x, const double* V, double* v_in, double* v_out, uint32_t* pol, uint32_t* wst,
+               cudaStream_t s) {
+    int ps, wslot;
+    step_warp_plan(D, ps, wslot);
+    if (wslot <= 0 || nx <= 0) return false;
+    const size_t smem = (static_cast<size_t>((D.R + 1) / 2) + static_cast<size_t>(kThreads / 32) * wslot) * 8;
+    const long long ctas = (nx + kThreads / 32 - 1) / (kThreads / 32);
+    // gathers in flight per lane (tuning: GM_STEP_WARP_U = 8, 16, 32)
+    static const char* su = std::getenv("GM_STEP_WARP_U");
+    const int U = su ? std::atoi(su) : 16;
+    const void* k = nullptr;
+#define GM_SW(T, UU) if (D.tpr == T && U == UU) k = reinterpret_cast<const void*>(&k_step_warp<T, UU>);
+    GM_SW(1, 8) GM_SW(1, 16) GM_SW(1, 32) GM_SW(2, 8) GM_SW(2, 16) GM_SW(2, 32) GM_SW(4, 8) GM_SW(4, 16) GM_SW(4, 32)
+#undef GM_SW
+    if (!k) return false;
+    note_variant(KF_EXPECT_MATRIX, "k_step_warp<%d,%d>", static_cast<int>(D.tpr), U);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    int per_sm = 0;
+    // GM_STEP_WARP_CTAS / GM_STEP_WARP_CARVEOUT (tuning): resident CTAs per SM, shared-memory carveout %
+    static const char* sc = std::getenv("GM_STEP_WARP_CTAS");
+    static const char* sv = std::getenv("GM_STEP_WARP_CARVEOUT");
+    if (sv) cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(sv));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, smem);
+    if (sc) per_sm = std::min(per_sm, std::atoi(sc));
+    const long long grid = std::max<long long>(1, std::min<long long>(ctas, std::max(per_sm, 1) * 1LL * num_sms()));
+    GmDev Dv = D;
+    void* args[] = {&Dv, &x0, &nx, &ps, &wslot, &probs, &origins, &t0x, &V, &v_in, &v_out, &pol, &wst};
+    const cudaError_t e = cudaLaunchKernel(k, dim3(static_cast<unsigned>(grid)), dim3(kThreads), args, smem, s);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("step_warp: ") + cudaGetErrorString(e));
     return true;
 }
 

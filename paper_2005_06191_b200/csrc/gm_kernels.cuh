@@ -35,6 +35,12 @@ void absorb_flags(const GmDev& D, uint8_t* d_flags, cudaStream_t s);
 // state's rows fit a CTA (k_step_small); probs/origins/t0x are the matrix's arrays,
 // r_base the matrix row of state x0's first row. False: not applicable (the caller
 // runs expect_matrix + maxmin).
+// the whole step with one warp per state (k_step_warp): R < 64 (TPR <= 4), a state's
+// rows within 24 KB of shared memory; probs/origins/t0x start at x0's first row
+bool step_warp_applies(const GmDev& D);
+bool step_warp(const GmDev& D, long long x0, long long nx, const double* probs, const long long* origins,
+               const double* t0x, const double* V, double* v_in, double* v_out, uint32_t* pol, uint32_t* wst,
+               cudaStream_t s);
 bool step_small_applies(const GmDev& D);
 bool step_small(const GmDev& D, long long x0, long long nx, const double* probs, long long r_base,
                 const long long* origins, const double* t0x, const double* V, double* v_in, double* v_out,

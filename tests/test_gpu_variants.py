@@ -86,10 +86,11 @@ SETTINGS = [
     {"GM_OFA_PK": "1"},  # OFA with the hoisted last-axis cell (row_dot_pk; default only for long rows)
     {"GM_OFA_PK": "1", "GM_OFA_TABLE": "prefix"},
     {"GM_OFA_CACHE": "0"},  # OFA row prologue re-run every step instead of cached across the sweep
-    {"GM_STEP_FUSED": "1"},  # small states: both passes in one kernel (k_step_small) instead of two
-    {"GM_MATRIX_SMALL": "0"},  # one-thread rows through k_expect_matrix_et instead of the warp-staged kernel
-    {"GM_MATRIX_SMALL": "1"},  # the warp-staged kernel also for TPR 2 / 4
-    {"GM_MATRIX_SMALL": "1", "GM_SMALL_U": "8", "GM_SMALL_SMEM_KB": "28"},  # 8 gathers in flight, half-empty chunks
+    {"GM_STEP_FUSED": "1", "GM_STEP_WARP": "0"},  # small states: both passes in one CTA-wide kernel (k_step_small)
+    {"GM_STEP_WARP": "0"},  # small states: expect_matrix + maxmin instead of one warp per state (k_step_warp)
+    {"GM_MATRIX_SMALL": "0", "GM_STEP_WARP": "0"},  # one-thread rows through k_expect_matrix_et instead of the warp-staged kernel
+    {"GM_MATRIX_SMALL": "1", "GM_STEP_WARP": "0"},  # the warp-staged kernel also for TPR 2 / 4
+    {"GM_MATRIX_SMALL": "1", "GM_SMALL_U": "8", "GM_SMALL_SMEM_KB": "28", "GM_STEP_WARP": "0"},  # 8 gathers in flight, half-empty chunks
     {"GM_OFA_PACK": "1", "GM_JIT": "1"},  # OFA consumer with packed (Q, line offset) tables
     {"GM_OFA_GROUP": "0", "GM_JIT": "1"},  # batched shape OFA consumer instead of the per-group one
     {"GM_JIT_SHAPE": "0", "GM_JIT": "1"},  # run-time compiled build without the row-shape specialisation
