@@ -1189,7 +1189,7 @@ gm_code gm_model_jit_compile(const gm_model* m, int32_t kind, double* seconds, g
                                                                        : std::string();
         if (kind == 3 && shape.empty()) throw ConfigErr("the model's row shape does not qualify for the OFA kernel");
         const std::string err = gmj::compile_only(m->M.prog, m->M.X.dim(), m->M.U.dim(), m->M.W.dim(), kind, seconds,
-                                                  shape, gmk::build_ctas(m->D, true));
+                                                  shape, gmk::build_ctas(m->M.device_descriptor(), true));
         if (!err.empty()) throw std::runtime_error(err);
     });
 }

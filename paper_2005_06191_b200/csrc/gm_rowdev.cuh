@@ -598,21 +598,27 @@ __device__ __forceinline__ double lds_imm(unsigned addr) {
     asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(addr), "n"(OFF));
     return v;
 }
-// The lane's elements t = lane + 32 i of one row, i = 0 .. pitch/32 - 1, unrolled at
-// compile time: element i = s + PER*b is Q[L(s) + DL*b] * ml[k(s)], one LDS, one DMUL,
-// one evict-first STG with immediate offsets; elements past R (row padding) store +0.0.
+// The lane's elements t = lane + 32 i of one row, i = 0 .. ceil(pitch/32) - 1, unrolled
+// at compile time: element i = s + PER*b is Q[L(s) + DL*b] * ml[k(s)], one LDS, one
+// DMUL, one evict-first STG with immediate offsets; elements past R (row padding)
+// store +0.0, lanes past the pitch (a pitch that is not a multiple of 32) none.
+// s = i mod PER < GM_FILL_NS = min(PER, number of chunks) register slots.
 template <int I>
 struct FillRow {
     static __device__ __forceinline__ void run(const unsigned* fq, const double* mv, double* o, int lane) {
         constexpr int PER = GM_FILL_PER, S = I % PER, B = I / PER;
         constexpr int OFF = 8 * (32 * PER / GM_FILL_WL) * B;
+        static_assert(S < GM_FILL_NS, "register slot");
         if constexpr (32 * I + 31 < GM_FILL_R) {
             __stcs(o + 32 * I, lds_imm<OFF>(fq[S]) * mv[S]);
-        } else {
+        } else if constexpr (32 * I + 31 < GM_FILL_PITCH) {
             const double q = lane + 32 * I < GM_FILL_R ? lds_imm<OFF>(fq[S]) : 0.0;
             __stcs(o + 32 * I, q * mv[S]);
+        } else {
+            const double q = lane + 32 * I < GM_FILL_R ? lds_imm<OFF>(fq[S]) : 0.0;
+            if (lane + 32 * I < GM_FILL_PITCH) __stcs(o + 32 * I, q * mv[S]);
         }
-        if constexpr (I + 1 < GM_FILL_PITCH / 32) FillRow<I + 1>::run(fq, mv, o, lane);
+        if constexpr (I + 1 < (GM_FILL_PITCH + 31) / 32) FillRow<I + 1>::run(fq, mv, o, lane);
     }
 };
 #endif
@@ -658,12 +664,12 @@ __global__ void __launch_bounds__(kThreads, MINB) k_build_ws(GmDev D, long long 
     // element i = s + PER*b of the lane reads Q[fq[s] + DL*b] * ml[fm[s]]
     // (32*PER is a multiple of Wl, so the cell repeats with period PER).
     constexpr int F_WL = GM_FILL_WL, F_WM = GM_FILL_WM, F_NL = GM_FILL_NL, F_PER = GM_FILL_PER;
-    constexpr int F_R = GM_FILL_R, F_NIT = GM_FILL_PITCH / 32, F_DL = 32 * F_PER / F_WL, F_NQ = (F_NL + 31) / 32;
-    unsigned fq[F_PER]; // shared-window byte addresses of Q[L(s)] in this warp's scratch
+    constexpr int F_R = GM_FILL_R, F_NQ = (F_NL + 31) / 32, F_NS = GM_FILL_NS;
+    unsigned fq[F_NS]; // shared-window byte addresses of Q[L(s)] in this warp's scratch
     {
         const unsigned sm0 = static_cast<unsigned>(__cvta_generic_to_shared(g_sm));
 #pragma unroll
-        for (int s = 0; s < F_PER; ++s)
+        for (int s = 0; s < F_NS; ++s)
             fq[s] = sm0 + 8u * static_cast<unsigned>(offQs + warp * (F_NL + 1) + (lane + 32 * s) / F_WL);
         // every Q element a lane reads (t < R) lies in its warp's scratch
         GM_CHECK(D.Wl == F_WL && D.Wm == F_WM && D.n_lines == F_NL && D.R == F_R && D.pitch == GM_FILL_PITCH);
@@ -767,9 +773,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_build_ws(GmDev D, long long 
                         if (F_NL % 32 == 0 || L < F_NL) Qs[L] = Pr[L / F_WM] * m[D.mm_off + L % F_WM];
                     }
                     __syncwarp();
-                    double mv[F_PER];
+                    double mv[F_NS];
 #pragma unroll
-                    for (int s2 = 0; s2 < F_PER; ++s2) mv[s2] = m[D.ml_off + (lane + 32 * s2) % F_WL];
+                    for (int s2 = 0; s2 < F_NS; ++s2) mv[s2] = m[D.ml_off + (lane + 32 * s2) % F_WL];
                     FillRow<0>::run(fq, mv, out + lane, lane);
                     __syncwarp();
 #else
