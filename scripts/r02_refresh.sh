@@ -2,7 +2,7 @@
 # (GPU columns re-measured, CPU columns reused from the first table), launch list,
 # ncu --set full of the bench's top kernels
 set -u
-O=gpurun_out/r02c
+O=gpurun_out/r02d
 mkdir -p $O
 timeout 2400 python -m pytest tests -q -m gpu --timeout 900 -rf > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 $O/pytest_gpu.log
 timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench rc=$?"
