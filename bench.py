@@ -571,6 +571,15 @@ def main():
                             "roofline_l1tex": ncu_l1tex(wname),
                             "kernel_variant": _capi.lib.gm_last_kernel_variant(_capi.KF_EXPECT_OFA).decode()}
             bet.release()
+            if world == 1:  # the user-level call: gridmdp.synthesize, value / policy tables on the host
+                t0 = time.perf_counter()
+                res = g.synthesize(mt, mt.spec, g.SynthesisOptions(mode="ofa"))
+                extra[wname]["e2e_synthesize"] = {
+                    "seconds": time.perf_counter() - t0,
+                    "d2h_bytes": int(res.values.nbytes + res.policy.nbytes + res.worst_dist.nbytes),
+                    "note": "wall clock, one call after the timed sweep (compiled kernels cached)"}
+                del res
+                g.release_cached_memory()
         line["extra"] = extra
 
     line.update(cpu)
