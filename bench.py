@@ -572,12 +572,14 @@ def main():
                             "kernel_variant": _capi.lib.gm_last_kernel_variant(_capi.KF_EXPECT_OFA).decode()}
             bet.release()
             if world == 1:  # the user-level call: gridmdp.synthesize, value / policy tables on the host
+                del g.synthesize(mt, mt.spec, g.SynthesisOptions(mode="ofa")).values  # warm (first-call setup)
                 t0 = time.perf_counter()
                 res = g.synthesize(mt, mt.spec, g.SynthesisOptions(mode="ofa"))
                 extra[wname]["e2e_synthesize"] = {
                     "seconds": time.perf_counter() - t0,
                     "d2h_bytes": int(res.values.nbytes + res.policy.nbytes + res.worst_dist.nbytes),
-                    "note": "wall clock, one call after the timed sweep (compiled kernels cached)"}
+                    "note": "wall clock of one call after a warm call (first-call setup: ~0.75 s, "
+                            "scripts/c5_e2e_probe.py)"}
                 del res
                 g.release_cached_memory()
         line["extra"] = extra
