@@ -390,7 +390,11 @@ typedef enum gm_exchange {
 } gm_exchange;
 typedef enum gm_transport {
     GM_XPORT_NCCL = 0,     /* ncclAllGather / ncclSend+ncclRecv (NVLink / NVSwitch); distinct devices */
-    GM_XPORT_PEER = 1      /* cudaMemcpyPeerAsync after a host barrier; any device list, repeats allowed */
+    GM_XPORT_PEER = 1,     /* cudaMemcpyPeerAsync after a host barrier; any device list, repeats allowed */
+    GM_XPORT_STORE = 2     /* no copy: the Bellman pass-2 epilogue stores each value straight into the
+                              value tables of the devices that read it (peer memory over NVLink /
+                              NVSwitch), then per-step events; <= 9 devices, peer access required,
+                              repeats allowed */
 } gm_transport;
 
 typedef struct gm_multi_stats {

@@ -223,7 +223,9 @@ SynthesisResult synthesize(const SystemModel& m, const Spec& spec, const Synthes
     const std::vector<int32_t> dev = adapter_devices();
     if (dev.size() > 1) { // state shards over the listed GPUs, V exchanged by NCCL (parallel.hpp:23-51's role)
         const char* tp = std::getenv("GRIDMDP_B200_TRANSPORT");
-        const int32_t transport = tp && std::string(tp) == "peer" ? GM_XPORT_PEER : GM_XPORT_NCCL;
+        const int32_t transport = tp && std::string(tp) == "peer"    ? GM_XPORT_PEER
+                                 : tp && std::string(tp) == "store" ? GM_XPORT_STORE
+                                                                    : GM_XPORT_NCCL;
         ok(gm_synthesize_multi(mh.h, static_cast<int32_t>(dev.size()), dev.data(), GM_XCHG_AUTO, transport, &r.h,
                                nullptr, &st),
            st);

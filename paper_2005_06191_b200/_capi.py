@@ -73,7 +73,7 @@ class Sizes(C.Structure):
 
 
 GM_XCHG_AUTO, GM_XCHG_HALO, GM_XCHG_ALLGATHER = 0, 1, 2
-GM_XPORT_NCCL, GM_XPORT_PEER = 0, 1
+GM_XPORT_NCCL, GM_XPORT_PEER, GM_XPORT_STORE = 0, 1, 2
 
 
 class MultiStats(C.Structure):

@@ -707,8 +707,10 @@ bool ofa_cached_step(gm_model* m, int64_t r0, int64_t n, const double* v_next, c
 
 // One backward step over states [x0, x1) (bellman_impl, synthesis.cpp:61-143).
 // v_next: full device V (absorbing zeroed); outputs indexed from x0.
+// `mir`: the pass-2 epilogue also stores the values into other devices' tables
+// (gm_multi.cpp, the "store" transport).
 void step_states(gm_model* m, gm_matrix* tm, int64_t x0, int64_t x1, const double* v_next,
-                 double* v_out, uint32_t* pol, uint32_t* wst, cudaStream_t s) {
+                 double* v_out, uint32_t* pol, uint32_t* wst, cudaStream_t s, const gmk::GmMirror* mir = nullptr) {
     const int64_t nuw = m->M.n_u() * m->M.n_w();
     const int64_t r0 = x0 * nuw, r1 = x1 * nuw;
     const int64_t n = r1 - r0;
@@ -721,10 +723,10 @@ void step_states(gm_model* m, gm_matrix* tm, int64_t x0, int64_t x1, const doubl
             Launch L(gmk::KF_EXPECT_MATRIX, s);
             const int64_t rb = r0 - tm->row_begin;
             if (gmk::step_warp(m->D, x0, x1 - x0, tm->probs.p + rb * m->D.pitch, tm->origins.p + rb,
-                               tm->has_t0x ? tm->t0x.p + rb : nullptr, v_next, m->d_vin.p, v_out, pol, wst, s))
+                               tm->has_t0x ? tm->t0x.p + rb : nullptr, v_next, m->d_vin.p, v_out, pol, wst, s, mir))
                 return; // both passes done, one warp per state
         }
-        if (tm->row_begin <= r0 && tm->row_end >= r1 && n > 0 && gmk::step_small_applies(m->D)) {
+        if (tm->row_begin <= r0 && tm->row_end >= r1 && n > 0 && !(mir && mir->n) && gmk::step_small_applies(m->D)) {
             Launch L(gmk::KF_EXPECT_MATRIX, s);
             if (gmk::step_small(m->D, x0, x1 - x0, tm->probs.p, r0 - tm->row_begin, tm->origins.p,
                                 tm->has_t0x ? tm->t0x.p : nullptr, v_next, m->d_vin.p, v_out, pol, wst, s))
@@ -778,7 +780,7 @@ void step_states(gm_model* m, gm_matrix* tm, int64_t x0, int64_t x1, const doubl
             });
     }
     Launch L(gmk::KF_MAXMIN, s);
-    gmk::maxmin(m->D, x0, x1 - x0, m->d_vin.p, v_out, pol, wst, s);
+    gmk::maxmin(m->D, x0, x1 - x0, m->d_vin.p, v_out, pol, wst, s, mir);
 }
 
 void ensure_t0x(gm_model* m, gm_matrix* tm) {
@@ -2008,6 +2010,19 @@ void gm_release_cached_memory(void) { flush_cache(); }
 } // extern "C"
 
 // ---------------------------------------------------------------- internal hooks (gm_internal.hpp)
+
+gm_code gmi_step_device_mirrored(gm_model* m, gm_matrix* tm, int64_t x0, int64_t x1, const double* d_v_next,
+                                  double* d_v_out, uint32_t* d_pol, uint32_t* d_wst, void* stream,
+                                  const gmk::GmMirror* mir, gm_status* st) {
+    return guarded(st, [&] {
+        if (x0 < 0 || x1 > m->M.n_x() || x0 > x1) throw std::out_of_range("step_device: state range");
+        if (mir && (mir->n < 0 || mir->n > gmk::kMaxMirrors)) throw std::out_of_range("step_device: mirror count");
+        prepare(m);
+        if (tm) ensure_t0x(m, tm);
+        m->ofa_cache_steps = true;
+        step_states(m, tm, x0, x1, d_v_next, d_v_out, d_pol, d_wst, static_cast<cudaStream_t>(stream), mir);
+    });
+}
 
 gm_result* gmi_result_new(const gm_model* m, int mode, const uint8_t* absorbing) {
     std::unique_ptr<gm_result> r(new gm_result);

@@ -3,6 +3,7 @@
 #pragma once
 
 #include "gridmdp_b200.h"
+#include "gm_kernels.cuh"
 
 #include <functional>
 #include <string>
@@ -17,3 +18,8 @@ void gmi_result_tables(gm_result* r, double** values, uint32_t** policy, uint32_
 gm_code gmi_guarded(gm_status* st, const std::function<void()>& f);
 // Rethrows a gm_status code as the matching exception type.
 [[noreturn]] void gmi_throw(int code, const std::string& msg);
+// gm_step_device whose pass-2 epilogue also stores the step's values into other
+// devices' value tables (mir: up to gmk::kMaxMirrors peer columns + state intervals).
+gm_code gmi_step_device_mirrored(gm_model* m, gm_matrix* tm, int64_t x0, int64_t x1, const double* d_v_next,
+                                  double* d_v_out, uint32_t* d_pol, uint32_t* d_wst, void* stream,
+                                  const gmk::GmMirror* mir, gm_status* st);

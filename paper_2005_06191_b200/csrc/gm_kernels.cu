@@ -638,6 +638,13 @@ __global__ void __launch_bounds__(kThreads) k_step_small(GmDev D, long long x0, 
     }
 }
 
+// The pass-2 epilogue's peer stores (GmMirror): the value of absolute state x into
+// every other device's value table whose read interval holds x.
+__device__ __forceinline__ void mirror_store(const GmMirror& mir, long long x, double v) {
+    for (int i = 0; i < mir.n; ++i)
+        if (x >= mir.lo[i] && x < mir.hi[i]) mir.dst[i][x] = v;
+}
+
 // Stage (ii), stored matrix, the whole step for small states with one warp per
 // state (both passes; C2a: 25 rows of 27 entries per state). The warp copies its
 // state's rows (contiguous in the matrix) into its shared-memory slot with
@@ -656,7 +663,7 @@ __global__ void __launch_bounds__(kThreads) k_step_warp(GmDev D, long long x0, l
                                                       const double* __restrict__ t0x,
                                                       const double* __restrict__ V, double* __restrict__ v_in,
                                                       double* __restrict__ v_out, uint32_t* __restrict__ pol,
-                                                      uint32_t* __restrict__ wst) {
+                                                      uint32_t* __restrict__ wst, GmMirror mir) {
     constexpr int RPP = 32 / TPR; // rows per pass of the warp
     const int R = static_cast<int>(D.R), P = static_cast<int>(D.pitch);
     const int nu = static_cast<int>(D.n_u), nw = static_cast<int>(D.n_w), nuw = nu * nw;
@@ -772,7 +779,9 @@ __global__ void __launch_bounds__(kThreads) k_step_warp(GmDev D, long long x0, l
             }
         }
         if (lane == 0) {
-            v_out[x] = absorbed ? 0.0 : smin(1.0, smax(0.0, best));
+            const double vx = absorbed ? 0.0 : smin(1.0, smax(0.0, best));
+            v_out[x] = vx;
+            mirror_store(mir, x0 + x, vx);
             if (pol) pol[x] = absorbed ? 0u : bu;
             if (wst) wst[x] = absorbed ? 0u : bw;
         }
@@ -789,7 +798,7 @@ __global__ void __launch_bounds__(kThreads) k_maxmin(GmDev D, long long x0, long
                                                     const double* __restrict__ v_in,
                                                     double* __restrict__ v_out,
                                                     uint32_t* __restrict__ pol,
-                                                    uint32_t* __restrict__ wst) {
+                                                    uint32_t* __restrict__ wst, GmMirror mir) {
     const long long gt = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
     const long long xi = gt / L;
     const int lane = static_cast<int>(gt % L);
@@ -834,11 +843,13 @@ __global__ void __launch_bounds__(kThreads) k_maxmin(GmDev D, long long x0, long
     if (!valid || lane != 0) return;
     if (absorbed) {
         v_out[xi] = 0.0;
+        mirror_store(mir, ix, 0.0);
         if (pol) pol[xi] = 0;
         if (wst) wst[xi] = 0;
         return;
     }
     v_out[xi] = smin(1.0, smax(0.0, best));
+    mirror_store(mir, ix, v_out[xi]);
     if (pol) pol[xi] = static_cast<uint32_t>(bu);
     if (wst) wst[xi] = static_cast<uint32_t>(bw);
 }
@@ -1871,7 +1882,7 @@ bool step_warp_applies(const GmDev& D) {
 
 bool step_warp(const GmDev& D, long long x0, long long nx, const double* probs, const long long* origins,
                const double* t0x, const double* V, double* v_in, double* v_out, uint32_t* pol, uint32_t* wst,
-               cudaStream_t s) {
+               cudaStream_t s, const GmMirror* mir) {
     int ps, wslot;
     step_warp_plan(D, ps, wslot);
     if (wslot <= 0 || nx <= 0) return false;
@@ -1896,14 +1907,16 @@ bool step_warp(const GmDev& D, long long x0, long long nx, const double* probs, 
     if (sc) per_sm = std::min(per_sm, std::atoi(sc));
     const long long grid = std::max<long long>(1, std::min<long long>(ctas, std::max(per_sm, 1) * 1LL * num_sms()));
     GmDev Dv = D;
-    void* args[] = {&Dv, &x0, &nx, &ps, &wslot, &probs, &origins, &t0x, &V, &v_in, &v_out, &pol, &wst};
+    GmMirror m0 = mir ? *mir : GmMirror{};
+    void* args[] = {&Dv, &x0, &nx, &ps, &wslot, &probs, &origins, &t0x, &V, &v_in, &v_out, &pol, &wst, &m0};
     const cudaError_t e = cudaLaunchKernel(k, dim3(static_cast<unsigned>(grid)), dim3(kThreads), args, smem, s);
     if (e != cudaSuccess) throw std::runtime_error(std::string("step_warp: ") + cudaGetErrorString(e));
     return true;
 }
 
 void maxmin(const GmDev& D, long long x0, long long nx, const double* v_in, double* v_out,
-            uint32_t* pol, uint32_t* wst, cudaStream_t s) {
+            uint32_t* pol, uint32_t* wst, cudaStream_t s, const GmMirror* mir) {
+    const GmMirror m0 = mir ? *mir : GmMirror{};
     if (nx <= 0) return;
     // L lanes per state, each scanning about three inputs (lane-strided, increasing u),
     // then a lowest-index-on-ties butterfly: C2b (n_u = 25) 8 lanes
@@ -1915,7 +1928,7 @@ void maxmin(const GmDev& D, long long x0, long long nx, const double* v_in, doub
     switch (L) {
 #define GM_MM(LL)                                                                                   \
     case LL:                                                                                        \
-        k_maxmin<LL><<<grid_for(nx * LL, kThreads), kThreads, 0, s>>>(D, x0, nx, v_in, v_out, pol, wst); \
+        k_maxmin<LL><<<grid_for(nx * LL, kThreads), kThreads, 0, s>>>(D, x0, nx, v_in, v_out, pol, wst, m0); \
         break;
         GM_MM(1) GM_MM(2) GM_MM(4) GM_MM(8) GM_MM(16) GM_MM(32)
 #undef GM_MM

@@ -9,6 +9,16 @@
 
 namespace gmk {
 
+// Pass-2 epilogue stores of a step's values into other devices' value tables (the
+// multi-device "store" transport, gm_multi.cpp): value of absolute state x also goes
+// to dst[i][x] for lo[i] <= x < hi[i] (peer memory over NVLink / NVSwitch).
+constexpr int kMaxMirrors = 8;
+struct GmMirror {
+    int n = 0;
+    double* dst[kMaxMirrors] = {};
+    long long lo[kMaxMirrors] = {}, hi[kMaxMirrors] = {};
+};
+
 // row flags written by the row prologue
 enum : uint8_t { RF_ABSORBED = 1, RF_ERROR = 2 };
 // prologue options
@@ -40,7 +50,7 @@ void absorb_flags(const GmDev& D, uint8_t* d_flags, cudaStream_t s);
 bool step_warp_applies(const GmDev& D);
 bool step_warp(const GmDev& D, long long x0, long long nx, const double* probs, const long long* origins,
                const double* t0x, const double* V, double* v_in, double* v_out, uint32_t* pol, uint32_t* wst,
-               cudaStream_t s);
+               cudaStream_t s, const GmMirror* mir = nullptr);
 bool step_small_applies(const GmDev& D);
 bool step_small(const GmDev& D, long long x0, long long nx, const double* probs, long long r_base,
                 const long long* origins, const double* t0x, const double* V, double* v_in, double* v_out,
@@ -96,7 +106,7 @@ void expect_matrix(const GmDev& D, long long row0, long long r_lo, long long r_h
 
 // min over disturbances, max over inputs per state (synthesis.cpp:112-142).
 void maxmin(const GmDev& D, long long x0, long long nx, const double* v_in, double* v_out,
-            uint32_t* pol, uint32_t* wst, cudaStream_t s);
+            uint32_t* pol, uint32_t* wst, cudaStream_t s, const GmMirror* mir = nullptr);
 
 // Number of stored probabilities > 0 in n doubles (export_prism header, io.cpp:296-298).
 unsigned long long count_positive(const double* p, long long n, unsigned long long* d_count, cudaStream_t s);

@@ -240,6 +240,29 @@ void exchange_peer(Job& J, int d, int k) {
     }
 }
 
+// The store transport: the peers that read this device's states wrote them into its
+// column k during their step k (gmi_step_device_mirrored); wait for those steps.
+void exchange_store(Job& J, int d, int k) {
+    Dev& D = *J.dev[static_cast<size_t>(d)];
+    for (const Range& r : J.X.recvs[static_cast<size_t>(d)])
+        cck(cudaStreamWaitEvent(D.s, J.dev[static_cast<size_t>(r.peer)]->step_ev[static_cast<size_t>(k)], 0),
+            "store wait");
+}
+
+// This device's pass-2 epilogue targets for step k: every peer column whose read
+// interval (the exchange plan's send ranges) holds some of this device's states.
+gmk::GmMirror mirrors_for(Job& J, int d, int k) {
+    gmk::GmMirror mir;
+    for (const Range& r : J.X.sends[static_cast<size_t>(d)]) {
+        if (mir.n == gmk::kMaxMirrors) throw std::runtime_error("store transport: more than 8 peers per device");
+        mir.dst[mir.n] = J.dev[static_cast<size_t>(r.peer)]->vals + static_cast<size_t>(k) * static_cast<size_t>(J.P);
+        mir.lo[mir.n] = r.a;
+        mir.hi[mir.n] = r.b;
+        ++mir.n;
+    }
+    return mir;
+}
+
 void exchange_nccl(Job& J, int d, int k) {
     Dev& D = *J.dev[static_cast<size_t>(d)];
     const Nccl& N = nccl();
@@ -308,13 +331,20 @@ void device_main(Job& J, int d) {
     // stage (ii): T backward steps, V exchanged after each
     // NCCL also runs for one device (a one-rank in-place all-gather): the transport
     // is then exercised on any machine with a GPU
-    const bool use_nccl = J.transport == GM_XPORT_NCCL;
+    const bool use_nccl = J.transport == GM_XPORT_NCCL, use_store = J.transport == GM_XPORT_STORE;
     for (int k = T - 1; k >= 0; --k) {
         ok = step_guard(J, [&] {
             gm_status st{};
-            sck(gm_step_device(D.model, D.tm, x0, x1, D.vals + P * (k + 1), D.vals + P * k + x0, D.pol + per * k,
-                               D.wst + per * k, D.s, &st),
-                st);
+            if (use_store && J.n > 1) {
+                const gmk::GmMirror mir = mirrors_for(J, d, k);
+                sck(gmi_step_device_mirrored(D.model, D.tm, x0, x1, D.vals + P * (k + 1), D.vals + P * k + x0,
+                                             D.pol + per * k, D.wst + per * k, D.s, &mir, &st),
+                    st);
+            } else {
+                sck(gm_step_device(D.model, D.tm, x0, x1, D.vals + P * (k + 1), D.vals + P * k + x0, D.pol + per * k,
+                                   D.wst + per * k, D.s, &st),
+                    st);
+            }
             if (k == T - 1) { // device errors (domain, quadrature) surface after the first step
                 cck(cudaStreamSynchronize(D.s), "bellman step");
                 sck(gm_check_device_errors(D.model, &st), st);
@@ -329,6 +359,7 @@ void device_main(Job& J, int d) {
         if (J.n > 1 || use_nccl) {
             ok = step_guard(J, [&] {
                 if (use_nccl) exchange_nccl(J, d, k);
+                else if (use_store) exchange_store(J, d, k);
                 else exchange_peer(J, d, k);
             });
             if (!ok) { // NCCL peers cannot continue without this device: stop everyone at the next sync
@@ -369,8 +400,10 @@ gm_code gm_synthesize_multi(gm_model* m, int32_t n_dev, const int32_t* devices, 
         if (n_dev < 1) throw std::out_of_range("synthesize_multi: at least one device");
         if (exchange < GM_XCHG_AUTO || exchange > GM_XCHG_ALLGATHER)
             gmi_throw(GM_ERR_CONFIG, "synthesize_multi: unknown exchange");
-        if (transport != GM_XPORT_NCCL && transport != GM_XPORT_PEER)
+        if (transport != GM_XPORT_NCCL && transport != GM_XPORT_PEER && transport != GM_XPORT_STORE)
             gmi_throw(GM_ERR_CONFIG, "synthesize_multi: unknown transport");
+        if (transport == GM_XPORT_STORE && n_dev > gmk::kMaxMirrors + 1)
+            gmi_throw(GM_ERR_CONFIG, "synthesize_multi: the store transport handles at most 9 devices");
         gm_sizes sz;
         gm_status s2{};
         sck(gm_model_sizes(m, &sz, &s2), s2);
@@ -410,13 +443,18 @@ gm_code gm_synthesize_multi(gm_model* m, int32_t n_dev, const int32_t* devices, 
             J.comms.resize(static_cast<size_t>(n_dev));
             nck(N.commInitAll(J.comms.data(), n_dev, J.devices.data()), "ncclCommInitAll");
         }
-        if (transport == GM_XPORT_PEER) // direct NVLink copies where the pair supports it
+        if (transport == GM_XPORT_PEER || transport == GM_XPORT_STORE) // direct NVLink access between the pairs
             for (int a : J.devices)
                 for (int b : J.devices) {
+                    if (a == b) continue;
                     int can = 0;
-                    if (a != b && cudaDeviceCanAccessPeer(&can, a, b) == cudaSuccess && can) {
+                    if (cudaDeviceCanAccessPeer(&can, a, b) == cudaSuccess && can) {
                         cudaSetDevice(a);
                         if (cudaDeviceEnablePeerAccess(b, 0) != cudaSuccess) cudaGetLastError(); // already enabled
+                    } else if (transport == GM_XPORT_STORE) {
+                        cudaGetLastError();
+                        gmi_throw(GM_ERR_CUDA, "synthesize_multi: the store transport needs peer access between "
+                                               "devices " + std::to_string(a) + " and " + std::to_string(b));
                     }
                 }
         // absorbing flags (spec.cpp:51-60) from the caller's model, then the host result

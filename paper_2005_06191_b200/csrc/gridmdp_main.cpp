@@ -153,7 +153,7 @@ int cmd_synthesize(const Args& a) {
         std::cout << "time_synthesize_s: " << since(t0) << "\n";
         if (gpus > 1)
             std::cout << "v_exchange: " << (ms.exchange_used == GM_XCHG_HALO ? "halo" : "allgather") << " "
-                      << (ms.transport_used == GM_XPORT_NCCL ? "nccl" : "peer") << " ("
+                      << (ms.transport_used == GM_XPORT_NCCL ? "nccl" : ms.transport_used == GM_XPORT_STORE ? "store" : "peer") << " ("
                       << (ms.exchange_used == GM_XCHG_HALO ? ms.halo_states : ms.allgather_states)
                       << " states per step)\n";
     } else {
@@ -391,8 +391,9 @@ int main(int argc, char** argv) {
             const std::string t = val();
             if (t == "nccl") a.transport = GM_XPORT_NCCL;
             else if (t == "peer") a.transport = GM_XPORT_PEER;
+            else if (t == "store") a.transport = GM_XPORT_STORE;
             else {
-                std::cerr << "--transport: " << t << " not in {nccl,peer}\n";
+                std::cerr << "--transport: " << t << " not in {nccl,peer,store}\n";
                 return 105;
             }
         } else if (k == "--dump-matrix" && a.verb == "abstract") a.dump = val();

@@ -609,15 +609,17 @@ def synthesize_multi(m: SystemModel, devices, spec: Optional[Spec] = None, opts:
                      exchange: str = "auto", transport: str = "nccl"):
     """synthesize over several GPUs of this process (gm_synthesize_multi): state shards,
     one host thread + stream per device, V exchanged per step by `exchange`
-    ("auto" | "halo" | "allgather") over `transport` ("nccl" | "peer"; "peer" accepts a
-    device listed several times). Returns (SynthesisResult, stats dict)."""
+    ("auto" | "halo" | "allgather") over `transport` ("nccl" | "peer" | "store"; "peer"
+    and "store" accept a device listed several times; "store": the pass-2 epilogue
+    writes each value straight into the peers' value tables). Returns
+    (SynthesisResult, stats dict)."""
     spec = spec or m.spec
     opts = opts or m.options
     m.use_spec(spec)
     m.use_options(opts)
     dev = (C.c_int32 * len(devices))(*devices)
     xchg = {"auto": _capi.GM_XCHG_AUTO, "halo": _capi.GM_XCHG_HALO, "allgather": _capi.GM_XCHG_ALLGATHER}[exchange]
-    xport = {"nccl": _capi.GM_XPORT_NCCL, "peer": _capi.GM_XPORT_PEER}[transport]
+    xport = {"nccl": _capi.GM_XPORT_NCCL, "peer": _capi.GM_XPORT_PEER, "store": _capi.GM_XPORT_STORE}[transport]
     h = C.c_void_p()
     ms = _capi.MultiStats()
     call("gm_synthesize_multi", m.handle, C.c_int32(len(devices)), C.cast(dev, C.c_void_p), C.c_int32(xchg),

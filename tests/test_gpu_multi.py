@@ -1,8 +1,9 @@
 """Multi-GPU synthesis on one GPU (the only device this environment has):
 
 * gm_synthesize_multi (C++, one process, one host thread + stream per device) with
-  the device list repeated over the peer transport — 2, 3 and 5 shards, halo and
-  all-gather exchanges, matrix and OFA — must be bit-identical to gm_synthesize;
+  the device list repeated over the peer and store transports — 2, 3 and 5 shards,
+  halo and all-gather exchanges, matrix and OFA — must be bit-identical to
+  gm_synthesize;
   NCCL runs for real as a one-rank communicator (ncclCommInitAll + in-place
   ncclAllGather every step);
 * the `gridmdp synthesize --gpus / --devices` CLI writes the same container;
@@ -47,12 +48,16 @@ CASES = ["fixture2d_ra", "ref_vehicle3_desk", "ref_bmw7_desk", "room5_uni", "ref
 @pytest.mark.parametrize("case", CASES)
 @pytest.mark.parametrize("mode", ["matrix", "ofa"])
 @pytest.mark.parametrize("exchange", ["halo", "allgather"])
-def test_multi_peer_bit_identical(case, mode, exchange):
+@pytest.mark.parametrize("transport", ["peer", "store"])
+def test_multi_bit_identical(case, mode, exchange, transport):
+    """peer: copies of the exchanged ranges after each step; store: no copy, the
+    pass-2 epilogue (k_maxmin / k_step_warp) writes each value into the value tables
+    of the shards that read it."""
     m = _model(case)
     opts = g.SynthesisOptions(mode=mode)
     ref = g.synthesize(m, m.spec, opts)
     for n in (2, 3, 5):
-        got, st = g.synthesize_multi(m, [0] * n, m.spec, opts, exchange=exchange, transport="peer")
+        got, st = g.synthesize_multi(m, [0] * n, m.spec, opts, exchange=exchange, transport=transport)
         _same(got, ref)
         assert st["n_devices"] == n and st["exchange_used"] == exchange
         assert G.tol_ok(got.values, G.golden_results(case)["values"]).all()
@@ -101,9 +106,10 @@ def test_multi_c5_north_star():
         pytest.skip("C5 golden missing")
     m = g.load_config(str(G.large_cfg("C5")))
     ref = g.synthesize(m)
-    got, st = g.synthesize_multi(m, [0, 0, 0, 0], transport="peer")
-    _same(got, ref)
-    assert G.tol_ok(got.values, G.large_results("C5")["values"]).all()
+    for transport in ("peer", "store"):
+        got, st = g.synthesize_multi(m, [0, 0, 0, 0], transport=transport)
+        _same(got, ref)
+        assert G.tol_ok(got.values, G.large_results("C5")["values"]).all()
 
 
 def cli(*args):
@@ -111,7 +117,8 @@ def cli(*args):
 
 
 @pytest.mark.parametrize("flags", [["--gpus", "1"], ["--devices", "0,0", "--transport", "peer"],
-                                   ["--devices", "0,0,0", "--transport", "peer", "--exchange", "allgather"]])
+                                   ["--devices", "0,0,0", "--transport", "peer", "--exchange", "allgather"],
+                                   ["--devices", "0,0,0", "--transport", "store"]])
 def test_cli_multi_gpu_container(flags, tmp_path):
     case = "ref_vehicle3_desk"
     a, b = tmp_path / "a.bin", tmp_path / "b.bin"
